@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark: preconditioned-GMRES iterations/s on BASELINE.json configs[2] (the headline:
+1024^2 cells, ell = 10, alpha = 1e-4, anisotropic log-normal kappa, NC2 with k = 8, rtol 1e-10).
+
+One "step" = one full FGMRES solve (rows a1-a4 + a6 of SURVEY.md §8(a)) of the seeded
+synthetic problem with b already resident in HBM; aac_setup (row a0) runs once before the
+timed region. Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config headline] [--impl ours|reference]
+
+N > 1: launched by torchrun, one rank per GPU, row slabs with an NCCL halo exchange
+(strong scaling: the global problem is fixed). `--impl reference` times the ORACLE
+(the CPU reference of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "precond GMRES its/s (fp64, N=1024², ℓ=10); stencil HBM GB/s as % of peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------ oracle side
+def oracle_sample(name: str, its: int = 1):
+    """Time the oracle (as it stands) on a bounded sample of the workload: `its` FGMRES
+    iterations of the full-size problem. Returns (its/s, seconds, sample description)."""
+    from oracle import chebyshev as ch
+    from oracle import gmres as og
+    from oracle import operator as op
+    from oracle import saddle
+    p = synth.make_problem(name)
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    if p.method == "sp":
+        lev = saddle.hierarchy(w)
+        prec = lambda r: saddle.sp_apply(w, r, p.ell, p.alpha, p.k, lev)  # noqa: E731
+    else:
+        al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * p.k, p.method, p.k)
+        prec = lambda r: ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)  # noqa: E731
+    t0 = time.perf_counter()
+    res = og.fgmres(lambda x: op.apply_allatonce(w, x), prec, p.b, 0.0, its)
+    dt = time.perf_counter() - t0
+    return res.iters / dt, dt, f"{res.iters} oracle FGMRES iteration(s) of the full {name} problem"
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec = synth.config(args.config)
+    # numpy elementwise work is single-threaded; BLAS dots may use more threads
+    threads = int(os.environ.get("OMP_NUM_THREADS", "1"))
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state (no JIT, no caches worth priming)
+    vals, secs = [], 0.0
+    desc = ""
+    for _ in range(args.steps):
+        v, dt, desc = oracle_sample(args.config, 1)
+        vals.append(v)
+        secs += dt
+    value = args.steps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "its/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_block(args, spec, None),
+        "cpu_baseline": {"value": value, "unit": "its/s", "cores": threads, "kind": "oracle",
+                         "sample": f"per step: {desc}"},
+        "e2e": {"value": value, "unit": "its/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_block(args, spec, extra):
+    cfg = {
+        "workload": f"{spec.name}: BASELINE.json configs[{list(synth.CONFIGS).index(spec.name)}], "
+                    f"{'x'.join([str(spec.n)] * spec.dim)} cells, ell={spec.ell}, alpha={spec.alpha}, "
+                    f"{spec.method.upper()} k={spec.k}, GMRES rtol={spec.rtol}",
+        "method": args.method or spec.method, "k": args.k or spec.k, "ell": spec.ell,
+        "alpha": spec.alpha, "rtol": spec.rtol, "seed": 0,
+        "parallelism": f"slab{args.gpus}",
+        "l2": "inputs larger than L2: each step streams the Krylov basis (GBs) through HBM",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, idx: int):
+        self.idx = idx
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def loop():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([s.strip() for s in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(r[0]) for r in self.rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_03947_b200 import from_problem, slab_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.tensor(list(_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().tolist())
+
+    spec = synth.config(args.config)
+    method = args.method or spec.method
+    k = args.k or spec.k
+    p = synth.make_problem(args.config)
+    nz, ny, nx = p.shape
+    ell = p.ell
+    if world > 1:
+        n_slab = ny if p.dim == 2 else nz
+        lo, hi = slab_range(n_slab, world, rank)
+    t0 = time.perf_counter()
+    s = from_problem(p, rank=rank, nranks=world, nccl_id=nccl_id, max_krylov=args.maxit)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    bfull = p.b.reshape(ell, nz, ny, nx)
+    if world > 1:
+        bl = bfull[:, lo:hi] if p.dim == 3 else bfull[:, :, lo:hi]
+    else:
+        bl = bfull
+    b_host = np.ascontiguousarray(bl.reshape(ell, -1))
+    b = torch.from_numpy(b_host).to(dev)
+    x = torch.empty_like(b)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        _, info = s.gmres(method, k, b, x, rtol=spec.rtol, maxit=args.maxit)
+    iters = info["iters"] if args.warmup else None
+
+    # ---- timed region: device-resident inputs
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    l0 = s.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    tot_its = 0
+    for _ in range(args.steps):
+        _, info = s.gmres(method, k, b, x, rtol=spec.rtol, maxit=args.maxit)
+        tot_its += info["iters"]
+    ev1.record(stream)
+    barrier()
+    launches = s.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    ms_max = _max_over_ranks(ms, world, dev)
+    value = tot_its / (ms_max / 1e3)
+
+    # ---- end-to-end: host b in pinned memory -> device, solve, x -> host
+    bh = torch.from_numpy(b_host).pin_memory()
+    xh = torch.empty_like(bh).pin_memory()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    e2e_its = 0
+    for _ in range(args.steps):
+        _, info_e = s.gmres_host(method, k, bh.numpy(), xh.numpy(), rtol=spec.rtol, maxit=args.maxit)
+        e2e_its += info_e["iters"]
+    e1.record(stream)
+    barrier()
+    e2e_ms = _max_over_ranks(e0.elapsed_time(e1), world, dev)
+
+    # ---- per-kernel CUDA-event timing (separate pass over the same steps) for the roofline
+    s.profile_reset()
+    s.profile(True)
+    for _ in range(args.steps):
+        s.gmres(method, k, b, x, rtol=spec.rtol, maxit=args.maxit)
+    prof = s.profile_read()
+    s.profile(False)
+    peak, peak_src = _peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    tot_prof_ms = sum(v["ms"] for v in prof.values())
+    stencil = prof.get("cheb_sweep", {})
+    rl = None
+    if dom[1]["ms"] > 0:
+        ach = dom[1]["model_bytes"] / (dom[1]["ms"] / 1e3) / 1e9
+        rl = {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": peak, "unit": "GB/s",
+              "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+              "share_of_step": dom[1]["ms"] / tot_prof_ms,
+              "model_bytes_per_launch": dom[1]["model_bytes"] / max(1, dom[1]["launches"])}
+    kernels = {kn: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                    "GBps": (v["model_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+               for kn, v in prof.items() if v["launches"]}
+    extra = {"gmres_iters_per_solve": info["iters"], "relres_true": info["relres_true"],
+             "setup_s": setup_s, "mu_max": s.mu_max, "alloc": s.allocation(method, k),
+             "matvecs_paper_units_per_solve": info["matvecs_paper_units"],
+             "kernels": kernels}
+    if stencil.get("ms"):
+        sg = stencil["model_bytes"] / (stencil["ms"] / 1e3) / 1e9
+        extra["stencil_GBps"] = sg
+        extra["stencil_pct_of_peak"] = 100.0 * sg / peak
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, desc = oracle_sample(args.config, 1)
+        cpu = {"value": v, "unit": "its/s", "cores": int(os.environ.get("OMP_NUM_THREADS", "1")),
+               "kind": "oracle", "sample": f"{desc} ({dt:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "its/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_block(args, spec, extra),
+            "e2e": {"value": e2e_its / (e2e_ms / 1e3), "unit": "its/s",
+                    "h2d_bytes_per_step": int(b_host.nbytes), "d2h_bytes_per_step": int(b_host.nbytes)},
+            "gpu_launches": int(launches), "clocks": clk, "roofline": rl, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _nccl_unique_id() -> bytes:
+    import ctypes
+    import glob
+
+    import torch
+    cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib",
+                                   "libnccl.so*")) + ["libnccl.so.2"]
+    for c in cands:
+        try:
+            lib = ctypes.CDLL(c)
+            buf = (ctypes.c_char * 128)()
+            if lib.ncclGetUniqueId(buf) == 0:
+                return bytes(buf)
+        except OSError:
+            continue
+    raise RuntimeError("cannot create an NCCL unique id")
+
+
+def _max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="headline", choices=list(synth.CONFIGS))
+    ap.add_argument("--method", default=None, choices=[None, "nc1", "nc2", "sp"])
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--maxit", type=int, default=60)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

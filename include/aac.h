@@ -1,0 +1,147 @@
+/*
+ * aac.h -- C ABI of the B200-native all-at-once diffusion-covariance solver
+ * (arXiv 2506.03947, "Block alpha-circulant preconditioners for all-at-once
+ * diffusion-based covariance operators").
+ *
+ * The library solves calA x = b (Eq. eq:A), where
+ *     calA = I_ell (x) A - Sigma (x) I_N,   Sigma = lower block shift,
+ *     A    = I + c (-div kappa grad)_h      (cell-centred, zero-flux Neumann),
+ * by flexible GMRES right-preconditioned with the block alpha-circulant
+ * preconditioner P_alpha (Eq. eq:exactPBE) applied approximately
+ * through its DFT form (Eqs. eq:Paform, eq:blockproblem):
+ *     Gamma_alpha scaling -> length-ell DFT across blocks -> ell shifted solves
+ *     (A - Lambda_k I) y_k = w_k -> inverse DFT -> Gamma_alpha^{-1} unscaling,
+ * the shifted solves by nested Chebyshev semi-iteration (NC1 / NC2 = Algorithm 1,
+ * PAPER.md:286-446, 652-690) or by the real saddle-point reformulation with
+ * MINRES / PCG (SP).
+ *
+ * Conventions (all calls):
+ *  - fp64 everywhere. Block vectors are DEVICE pointers to ell contiguous planes
+ *    of this rank's slab: x[j * n_local + p], p = (z*ny + y)*nx + x (x fastest),
+ *    j = 0..ell-1 the time block. Slabs split the slowest non-trivial axis
+ *    (y in 2D, z in 3D) into contiguous ranges, rank order = slab order
+ *    (aac_slab_range). The caller owns every vector; the library never retains
+ *    a caller pointer after a call returns.
+ *  - All work is enqueued on the cudaStream_t given to aac_setup, in stream
+ *    order. aac_gmres / aac_gmres_host synchronise that stream (they poll the
+ *    Arnoldi residual); aac_matvec / aac_precond_apply do not.
+ *  - Multi-rank (nranks > 1): every rank calls every function collectively
+ *    (SPMD) with the same scalar arguments; NCCL (loaded at run time) carries
+ *    the halo exchange and the reductions over NVLink.
+ *  - A context is not thread-safe.
+ *  - Return codes: AAC_OK, AAC_ENOCONV (> 0: completed with a condition) or a
+ *    negative error; aac_last_error() then holds a message.
+ */
+#ifndef AAC_H
+#define AAC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aac_ctx aac_ctx;
+
+enum {
+  AAC_OK = 0,
+  AAC_ENOCONV = 1,   /* GMRES reached maxit; x holds the last iterate, info filled */
+  AAC_EINVAL = -1,   /* bad argument (message in aac_last_error)                   */
+  AAC_ECUDA = -2,    /* a CUDA runtime call or kernel launch failed                */
+  AAC_ENCCL = -3,    /* NCCL unavailable or failed                                 */
+  AAC_ENOMEM = -4    /* device or host allocation failed                           */
+};
+
+enum { AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3 };
+
+typedef struct {
+  int dim;          /* 1, 2 or 3                                                     */
+  int64_t n[3];     /* global cells per axis (x, y, z); unused axes = 1               */
+  int rank;         /* this rank, 0 <= rank < nranks                                  */
+  int nranks;       /* number of slabs (1 for a single GPU; must be 1 when dim == 1)  */
+} aac_grid;
+
+/* Half-open slab [lo, hi) of the slab axis owned by `rank` (balanced contiguous
+ * split, the first n % nranks ranks get one extra layer). Host-only, needs no GPU.
+ * Returns AAC_EINVAL on nranks < 1, rank out of range or n < nranks.             */
+int aac_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi);
+
+/* Create a solver context on the current CUDA device.
+ *  kx, ky, kz : HOST pointers to the GLOBAL interior-face diffusivities kappa_f
+ *               (anisotropy already applied), natural layouts
+ *                 kx[nz][ny][nx-1], ky[nz][ny-1][nx], kz[nz-1][ny][nx]
+ *               (NULL allowed for an axis with n = 1). Copied; not retained.
+ *  c          : diffusion coefficient; face weight w_f = c * kappa_f * n_a^2
+ *               (h_a = 1/n_a), so A = I + c(-div kappa grad)_h (BASELINE.json).
+ *  ell        : number of time blocks, even, 2 <= ell <= 16.
+ *  alpha      : 0 < alpha < 1 (Lemma lemma:Zalpha needs alpha != mu_j^ell and
+ *               mu_min(A) = 1 exactly under Neumann BCs).
+ *  max_krylov : Krylov storage for aac_gmres (maxit <= max_krylov).
+ *  cuda_stream: cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ *               NULL = legacy default stream.
+ *  nccl_id    : HOST pointer to a 128-byte ncclUniqueId shared by all ranks;
+ *               ignored (may be NULL) when nranks == 1.
+ * Errors: AAC_EINVAL (odd/small ell, alpha outside (0,1), c < 0, kappa <= 0 or
+ * non-finite, n < 2 on a used axis, bad slab), AAC_ENOMEM, AAC_ECUDA, AAC_ENCCL. */
+int aac_setup(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+              double c, int ell, double alpha, int max_krylov, void* cuda_stream,
+              const void* nccl_id, aac_ctx** out);
+
+/* y = calA x: y_0 = A x_0, y_j = A x_j - x_{j-1}.
+ * x, y: device, [ell][n_local]; x != y. One halo exchange when nranks > 1.       */
+int aac_matvec(aac_ctx* ctx, const double* x, double* y);
+
+/* z ~= P_alpha^{-1} r (Eq. eq:Paform) with inner method AAC_NC1 / AAC_NC2
+ * (k Chebyshev iterations per shifted system, NC2 redistributes a budget of
+ * ell*k by Algorithm 1) or AAC_SP (k MINRES / PCG iterations).
+ * r, z: device, [ell][n_local]; r != z. Errors: AAC_EINVAL on k < 1 or an
+ * unknown method.                                                                */
+int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z);
+
+typedef struct {
+  int iters;                    /* Arnoldi steps = preconditioner applications     */
+  int converged;                /* 1 if |g_{j+1}| <= rtol ||b|| (or breakdown)     */
+  double relres_est;            /* |g_{j+1}| / ||b|| at exit                       */
+  double relres_true;           /* ||b - calA x|| / ||b|| (one extra apply)        */
+  long long matvecs_paper_units;/* products with A in the paper's Table 1 units    */
+  long long stencil_sweeps;     /* stencil passes actually executed (per plane)    */
+} aac_gmres_info;
+
+/* Flexible GMRES (x_0 = 0, unrestarted, CGS2, Givens) for calA x = b, right-
+ * preconditioned by aac_precond_apply(method, k) (BASELINE.json north_star).
+ * b, x: device [ell][n_local]; b != x. info may be NULL.
+ * Returns AAC_OK on convergence, AAC_ENOCONV after maxit steps.                   */
+int aac_gmres(aac_ctx* ctx, int method, int k, const double* b, double* x,
+              double rtol, int maxit, aac_gmres_info* info);
+
+/* As aac_gmres with HOST b and x (pinned or pageable); the host<->device copies
+ * are enqueued inside the call (the end-to-end path).                            */
+int aac_gmres_host(aac_ctx* ctx, int method, int k, const double* b_host, double* x_host,
+                   double rtol, int maxit, aac_gmres_info* info);
+
+/* Spectral bounds used by the inner solvers (mu_min = 1 exactly, mu_max =
+ * global Gershgorin max) and the per-block inner iteration counts for
+ * (method, k), block k = 0..ell-1 (alloc may be NULL). n_local may be NULL.      */
+int aac_query(aac_ctx* ctx, int method, int k, double* mu_min, double* mu_max, int* alloc,
+              int64_t* n_local);
+
+/* Per-kernel CUDA-event timing (off by default). When enabled, every launch of
+ * the library is bracketed by events on the context stream; aac_profile_read
+ * returns the accumulated device milliseconds, launch count and the model
+ * (algorithmic) DRAM bytes of kernel class `id` (0 <= id < aac_profile_count()),
+ * and its name. aac_launch_count counts every kernel launch since setup.         */
+int aac_profile_enable(aac_ctx* ctx, int enable);
+int aac_profile_count(void);
+int aac_profile_read(aac_ctx* ctx, int id, const char** name, double* ms, long long* launches,
+                     double* model_bytes);
+int aac_profile_reset(aac_ctx* ctx);
+long long aac_launch_count(const aac_ctx* ctx);
+
+const char* aac_last_error(const aac_ctx* ctx);   /* also valid for ctx == NULL */
+void aac_destroy(aac_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AAC_H */

@@ -1,0 +1,151 @@
+// aac_internal.cuh -- context, geometry and launch plumbing of libaac (sm_100a, fp64).
+// Not part of the C ABI (include/aac.h is). See DESIGN.md §5 for the data layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aac.h"
+
+#define AAC_MAX_ELL 16
+#define AAC_MAX_BLK (AAC_MAX_ELL / 2 + 1)
+
+// ------------------------------------------------------------------------------------------
+// Geometry of this rank's slab, passed BY VALUE to every stencil kernel.
+// Points p = (z*ny + y)*nx + x of the local slab (x fastest). The slab axis is y for dim 2
+// and z for dim 3; `S` is the size of one layer across the slab axis (nx in 2D, nx*ny in 3D).
+// Face weights use the "lower face" convention: wx[p] = weight of the face between (x-1) and
+// x (0 at x = 0), and likewise wy, wz; each array carries one extra layer so that the upper
+// face of p is always w?[p + stride] (zero on physical boundaries; the slab's top face on
+// the last local layer of the slab axis). Halo layers (ell planes of S values) hold the
+// neighbour ranks' boundary layers of the stencil input.
+struct Geo {
+  int nx, ny, nz;        // LOCAL extents (slab axis already cut)
+  long long N;           // nx*ny*nz
+  long long S;           // layer size across the slab axis
+  int has_lo, has_hi;    // neighbour ranks below / above along the slab axis
+  const double* wx;
+  const double* wy;
+  const double* wz;
+};
+
+// ------------------------------------------------------------------------------------------
+// Kernel classes for per-kernel CUDA-event profiling (aac_profile_*).
+enum KernelId {
+  KID_MATVEC = 0,      // calA apply (stencil over all ell planes)
+  KID_FWD,             // gamma-scale + block DFT (+ first Chebyshev step when fused)
+  KID_SWEEP,           // Chebyshev three-term sweep (stencil + axpby) on active planes
+  KID_INV,             // last Chebyshev step + inverse DFT + gamma^{-1}
+  KID_DOT,             // multi-dot partials
+  KID_UPD,             // CGS update (+ fused dots / norm)
+  KID_REDUCE,          // fixed-order reduction of partials
+  KID_SCALAR,          // single-thread Arnoldi / Givens / back substitution
+  KID_AXPY,            // vector scale / lincomb
+  KID_SP_STENCIL,      // SP: shifted / saddle stencil applies
+  KID_SP_MG,           // SP: multigrid smoother / transfer / coarse solve
+  KID_SP_VEC,          // SP: Krylov vector updates and dots
+  KID_HALO,            // halo pack/copy
+  KID_COUNT
+};
+
+struct ProfRec { int id; cudaEvent_t a, b; };
+
+struct NcPlan {            // inner Chebyshev plan for (method, k)
+  int method = 0, k = 0;
+  int nblk = 0;            // ell/2 + 1 packed blocks
+  int p[AAC_MAX_BLK];      // iterations per packed block
+  int pmax = 0;
+  std::vector<double> a_re, a_im, b_re, b_im;   // [blk][s] s = 1..p-1, row stride pmax
+};
+
+struct SpPlan;             // saddle-point plan (aac_sp.cuh)
+
+struct aac_ctx {
+  // problem
+  int dim = 0, ell = 0, rank = 0, nranks = 1;
+  long long n[3] = {1, 1, 1};          // global extents
+  long long lo = 0, hi = 0;            // slab range along the slab axis
+  double c = 0.0, alpha = 0.0;
+  double mu_min = 1.0, mu_max = 1.0;
+  Geo geo{};
+  int max_krylov = 0;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  // device memory (library-owned)
+  double* d_w = nullptr;               // wx | wy | wz
+  double* d_what = nullptr;            // [ell][N] packed half-complex DFT of the input
+  double* d_X = nullptr;               // [3][ell][N] Chebyshev iterate slots
+  double* d_tmp = nullptr;             // [ell][N] scratch (true residual, SP)
+  double* d_V = nullptr;               // [(max_krylov+1)][ell][N]
+  double* d_Z = nullptr;               // [max_krylov][ell][N]
+  double* d_W = nullptr;               // [ell][N] Arnoldi work vector
+  double* d_bx = nullptr;              // [2][ell][N] staging for aac_gmres_host
+  double* d_halo = nullptr;            // [2][ell][S]  lo | hi
+  double* d_part = nullptr;            // partial sums [max_ctas][max_krylov+2]
+  double* d_red = nullptr;             // reduced sums  (several vectors of max_krylov+2)
+  double* d_H = nullptr;               // Hessenberg (max_krylov+1) x max_krylov, col-major
+  double* d_giv = nullptr;             // cs | sn | g | y
+  double* d_stat = nullptr;            // small scalars (device)
+  double* h_stat = nullptr;            // pinned mirror
+  int part_ctas = 0;
+  // plans
+  NcPlan nc[2];                        // cached NC plans
+  int nc_next = 0;
+  SpPlan* sp = nullptr;
+  // NCCL (dlopen'ed)
+  void* nccl_comm = nullptr;
+  // bookkeeping
+  long long launches = 0;
+  long long sweeps = 0;
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[KID_COUNT] = {0};
+  long long prof_n[KID_COUNT] = {0};
+  double prof_bytes[KID_COUNT] = {0};
+  std::string err;
+};
+
+// ------------------------------------------------------------------------------------------
+int aac_fail(aac_ctx* ctx, int code, const char* fmt, ...);
+
+#define CUDA_TRY(ctx, call)                                                                 \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return aac_fail((ctx), AAC_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                      cudaGetErrorString(e_));                                              \
+  } while (0)
+
+#define AAC_TRY(call)        \
+  do {                       \
+    int r_ = (call);         \
+    if (r_ < 0) return r_;   \
+  } while (0)
+
+// Bracket one launch with profiling events when enabled; count it; check launch errors.
+struct LaunchScope {
+  aac_ctx* ctx;
+  int id;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(aac_ctx* c, int kid, double bytes);
+  int end();
+};
+
+#define LAUNCH(ctx, kid, bytes, ...)                                                         \
+  do {                                                                                      \
+    LaunchScope ls_((ctx), (kid), (bytes));                                                 \
+    __VA_ARGS__;                                                                            \
+    AAC_TRY(ls_.end());                                                                     \
+  } while (0)
+
+inline unsigned grid1d(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  return (unsigned)(g < 1 ? 1 : g);
+}

@@ -1,0 +1,108 @@
+// comm.cuh -- NCCL over NVLink/NVSwitch for the slab decomposition.
+//
+// NCCL is loaded at run time (dlopen "libnccl.so.2": the copy torch already mapped into the
+// process), only when nranks > 1, so single-GPU use and CPU-only imports never touch it.
+// Exchange steps of the path: one halo exchange of the stencil input before every stencil
+// sweep (neighbour boundary layers along the slab axis, contiguous per plane) and sum
+// all-reduces of the GMRES inner products / max all-reduce of the Gershgorin bound.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "aac_internal.cuh"
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi g_nccl;
+
+static int nccl_load(aac_ctx* ctx) {
+  if (g_nccl.h) return AAC_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return aac_fail(ctx, AAC_ENCCL, "dlopen libnccl.so.2 failed: %s", dlerror());
+#define SYM(name, field)                                                               \
+  *(void**)(&g_nccl.field) = dlsym(h, name);                                           \
+  if (!g_nccl.field) return aac_fail(ctx, AAC_ENCCL, "NCCL symbol %s missing", name);
+  SYM("ncclCommInitRank", CommInitRank)
+  SYM("ncclCommDestroy", CommDestroy)
+  SYM("ncclAllReduce", AllReduce)
+  SYM("ncclSend", Send)
+  SYM("ncclRecv", Recv)
+  SYM("ncclGroupStart", GroupStart)
+  SYM("ncclGroupEnd", GroupEnd)
+  SYM("ncclGetErrorString", GetErrorString)
+#undef SYM
+  g_nccl.h = h;
+  return AAC_OK;
+}
+
+#define NCCL_TRY(ctx, call)                                                                 \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return aac_fail((ctx), AAC_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                      g_nccl.GetErrorString(r_));                                           \
+  } while (0)
+
+static int comm_init(aac_ctx* ctx, const void* nccl_id) {
+  if (ctx->nranks == 1) return AAC_OK;
+  if (!nccl_id) return aac_fail(ctx, AAC_EINVAL, "nccl_id required when nranks > 1");
+  AAC_TRY(nccl_load(ctx));
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof(id));
+  ncclComm_t comm;
+  NCCL_TRY(ctx, g_nccl.CommInitRank(&comm, ctx->nranks, id, ctx->rank));
+  ctx->nccl_comm = (void*)comm;
+  return AAC_OK;
+}
+
+static void comm_destroy(aac_ctx* ctx) {
+  if (ctx->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)ctx->nccl_comm);
+  ctx->nccl_comm = nullptr;
+}
+
+// In-place all-reduce of n doubles on the context stream (no-op on one rank).
+static int comm_allreduce(aac_ctx* ctx, double* d, int n, ncclRedOp_t op) {
+  if (ctx->nranks == 1 || n <= 0) return AAC_OK;
+  NCCL_TRY(ctx, g_nccl.AllReduce(d, d, (size_t)n, ncclFloat64, op, (ncclComm_t)ctx->nccl_comm,
+                                 ctx->stream));
+  return AAC_OK;
+}
+
+// Halo exchange of the stencil inputs: for each (plane pointer, plane index q) send the
+// first / last slab layer to the rank below / above and receive the neighbours' layers into
+// halo_lo[q] / halo_hi[q]. Layers are contiguous (S doubles), so no packing is needed.
+static int comm_halo(aac_ctx* ctx, const double* const* planes, const int* qs, int count) {
+  if (ctx->nranks == 1 || count == 0) return AAC_OK;
+  const Geo& g = ctx->geo;
+  const long long S = g.S;
+  double* hlo = ctx->d_halo;
+  double* hhi = ctx->d_halo + (long long)ctx->ell * S;
+  ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
+  NCCL_TRY(ctx, g_nccl.GroupStart());
+  for (int i = 0; i < count; ++i) {
+    const double* u = planes[i];
+    const int q = qs[i];
+    if (g.has_lo) {
+      NCCL_TRY(ctx, g_nccl.Send(u, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream));
+      NCCL_TRY(ctx, g_nccl.Recv(hlo + q * S, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream));
+    }
+    if (g.has_hi) {
+      NCCL_TRY(ctx, g_nccl.Send(u + g.N - S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream));
+      NCCL_TRY(ctx, g_nccl.Recv(hhi + q * S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream));
+    }
+  }
+  NCCL_TRY(ctx, g_nccl.GroupEnd());
+  return AAC_OK;
+}

@@ -1,0 +1,161 @@
+"""Thin Python front end of libaac (marshalling only; names follow include/aac.h).
+
+    s = Solver(dim, n, kx, ky, kz, c, ell, alpha)      # aac_setup
+    y = s.matvec(x)                                      # aac_matvec           (y = calA x)
+    z = s.precond_apply("nc2", 8, r)                     # aac_precond_apply    (z ~ P^{-1} r)
+    x, info = s.gmres("nc2", 8, b, rtol=1e-10)           # aac_gmres            (device tensors)
+    x, info = s.gmres_host("nc2", 8, b_numpy)            # aac_gmres_host       (host arrays)
+
+Block vectors are torch.float64 CUDA tensors of shape [ell, n_local] (or anything that
+reshapes to it) holding this rank's slab; see include/aac.h for the layout.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import METHODS, aac_gmres_info, aac_grid, check, lib
+
+
+def slab_range(n: int, nranks: int, rank: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    check(lib.aac_slab_range(n, nranks, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _method(m):
+    return METHODS[m] if isinstance(m, str) else int(m)
+
+
+class Solver:
+    def __init__(self, dim, n, kx, ky=None, kz=None, c=0.0, ell=10, alpha=1e-4, *,
+                 max_krylov=64, device=None, stream=None, rank=0, nranks=1, nccl_id=None):
+        n = tuple(int(v) for v in n) + (1,) * (3 - len(n))   # (nx, ny, nz)
+        self.dim, self.n, self.ell, self.alpha, self.c = dim, n, ell, alpha, c
+        self.rank, self.nranks = rank, nranks
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        g = aac_grid(dim, (ctypes.c_int64 * 3)(*n), rank, nranks)
+        keep = []
+
+        def arr(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return _dptr(a)
+
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        ctx = ctypes.c_void_p()
+        check(lib.aac_setup(ctypes.byref(g), arr(kx), arr(ky), arr(kz), float(c), int(ell),
+                            float(alpha), int(max_krylov), ctypes.c_void_p(self.stream.cuda_stream),
+                            idbuf, ctypes.byref(ctx)))
+        self.ctx = ctx
+        nl = ctypes.c_int64()
+        mu0, mu1 = ctypes.c_double(), ctypes.c_double()
+        check(lib.aac_query(ctx, 1, 1, ctypes.byref(mu0), ctypes.byref(mu1), None,
+                            ctypes.byref(nl)), ctx)
+        self.n_local, self.mu_min, self.mu_max = nl.value, mu0.value, mu1.value
+        self.max_krylov = max_krylov
+
+    # -- helpers -----------------------------------------------------------------------
+    def _vec(self, t: torch.Tensor) -> torch.Tensor:
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+            raise TypeError("block vectors must be float64 CUDA tensors")
+        if t.numel() != self.ell * self.n_local or not t.is_contiguous():
+            raise ValueError(f"expected a contiguous tensor of {self.ell}x{self.n_local} doubles")
+        return t
+
+    def empty(self) -> torch.Tensor:
+        return torch.empty(self.ell, self.n_local, dtype=torch.float64, device=self.device)
+
+    # -- C ABI calls ---------------------------------------------------------------------
+    def matvec(self, x, y=None):
+        x = self._vec(x)
+        y = self.empty() if y is None else self._vec(y)
+        check(lib.aac_matvec(self.ctx, x.data_ptr(), y.data_ptr()), self.ctx)
+        return y
+
+    def precond_apply(self, method, k, r, z=None):
+        r = self._vec(r)
+        z = self.empty() if z is None else self._vec(z)
+        check(lib.aac_precond_apply(self.ctx, _method(method), int(k), r.data_ptr(), z.data_ptr()),
+              self.ctx)
+        return z
+
+    def gmres(self, method, k, b, x=None, rtol=1e-10, maxit=None):
+        b = self._vec(b)
+        x = self.empty() if x is None else self._vec(x)
+        info = aac_gmres_info()
+        rc = lib.aac_gmres(self.ctx, _method(method), int(k), b.data_ptr(), x.data_ptr(),
+                           float(rtol), int(maxit or self.max_krylov), ctypes.byref(info))
+        check(rc, self.ctx, ok=(_lib.AAC_OK, _lib.AAC_ENOCONV))
+        return x, info.asdict()
+
+    def gmres_host(self, method, k, b: np.ndarray, x: np.ndarray | None = None, rtol=1e-10,
+                   maxit=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.size != self.ell * self.n_local:
+            raise ValueError("b has the wrong size")
+        x = np.empty_like(b) if x is None else x
+        info = aac_gmres_info()
+        rc = lib.aac_gmres_host(self.ctx, _method(method), int(k), _dptr(b), _dptr(x), float(rtol),
+                                int(maxit or self.max_krylov), ctypes.byref(info))
+        check(rc, self.ctx, ok=(_lib.AAC_OK, _lib.AAC_ENOCONV))
+        return x, info.asdict()
+
+    def allocation(self, method, k):
+        al = (ctypes.c_int * self.ell)()
+        check(lib.aac_query(self.ctx, _method(method), int(k), None, None, al, None), self.ctx)
+        return list(al)
+
+    # -- profiling -----------------------------------------------------------------------
+    def profile(self, enable=True):
+        check(lib.aac_profile_enable(self.ctx, int(enable)), self.ctx)
+
+    def profile_reset(self):
+        check(lib.aac_profile_reset(self.ctx), self.ctx)
+
+    def profile_read(self):
+        out = {}
+        for i in range(lib.aac_profile_count()):
+            name = ctypes.c_char_p()
+            ms, nb = ctypes.c_double(), ctypes.c_double()
+            nl = ctypes.c_longlong()
+            check(lib.aac_profile_read(self.ctx, i, ctypes.byref(name), ctypes.byref(ms),
+                                       ctypes.byref(nl), ctypes.byref(nb)), self.ctx)
+            out[name.value.decode()] = {"ms": ms.value, "launches": nl.value, "model_bytes": nb.value}
+        return out
+
+    def launch_count(self):
+        return lib.aac_launch_count(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            torch.cuda.current_stream(self.device).synchronize()
+            lib.aac_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_problem(prob, *, rank=0, nranks=1, nccl_id=None, max_krylov=64, **kw) -> Solver:
+    """Construct a Solver from a synth.Problem-like object (dim, shape, c, ell, alpha, kx..)."""
+    nz, ny, nx = prob.shape
+    return Solver(prob.dim, (nx, ny, nz), prob.kx, prob.ky if prob.dim >= 2 else None,
+                  prob.kz if prob.dim >= 3 else None, prob.c, prob.ell, prob.alpha,
+                  rank=rank, nranks=nranks, nccl_id=nccl_id, max_krylov=max_krylov, **kw)

@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): relative 2-norm <= 1e-12 per calA or preconditioner apply,
+<= 1e-9 on the GMRES solution, iteration counts equal within +-1. Integer outputs (the
+NC2 allocation) are compared bit-exactly. Sizes span several CTA tiles with ragged tails;
+the full-size headline is checked against oracle values stored by
+scripts/make_oracle_golden.py (oracle-only) and by properties that hold at any size.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import synth  # noqa: E402
+from oracle import chebyshev as ch  # noqa: E402
+from oracle import circulant as circ  # noqa: E402
+from oracle import gmres as og  # noqa: E402
+from oracle import operator as op  # noqa: E402
+
+HERE = os.path.dirname(__file__)
+
+
+def _solver(p, max_krylov=64):
+    from paper_2506_03947_b200 import from_problem
+    return from_problem(p, max_krylov=max_krylov)
+
+
+def _dev(a, ell):
+    return torch.from_numpy(np.ascontiguousarray(a).reshape(ell, -1)).cuda()
+
+
+def _rel(a, b):
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+CASES = [
+    ("1d", {}),
+    ("2d256", dict(shape=(1, 53, 37))),
+    ("2d256", dict(shape=(1, 2, 2), ell=2)),
+    ("headline", dict(shape=(1, 130, 67))),
+    ("2d256", dict(n=256, alpha=1e-4)),
+    ("3d", dict(shape=(9, 13, 11))),
+    ("3d", dict(shape=(17, 17, 17), ell=4)),
+]
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_matvec_parity(name, kw):
+    p = synth.make_problem(name, **kw)
+    s = _solver(p)
+    w = op.weights(p)
+    assert s.mu_max == pytest.approx(op.gershgorin_max(w), rel=1e-14)
+    x = np.random.default_rng(7).standard_normal((p.ell,) + p.shape)
+    y = s.matvec(_dev(x, p.ell)).cpu().numpy()
+    assert _rel(y, op.apply_allatonce(w, x)) <= 1e-12
+    s.close()
+
+
+PRE = [
+    ("1d", {}, "nc1", 10), ("1d", {}, "nc2", 10), ("1d", {}, "nc1", 1),
+    ("2d256", dict(shape=(1, 53, 37)), "nc1", 5), ("2d256", dict(shape=(1, 53, 37)), "nc2", 5),
+    ("2d256", dict(shape=(1, 53, 37), alpha=1e-4), "nc1", 2),
+    ("2d256", dict(shape=(1, 41, 40), ell=2), "nc1", 4),
+    ("2d256", dict(shape=(1, 41, 40), ell=16, alpha=0.3), "nc2", 6),
+    ("headline", dict(shape=(1, 130, 67)), "nc2", 8),
+    ("headline", dict(shape=(1, 64, 64), c=0.0), "nc2", 8),
+    ("3d", dict(shape=(9, 13, 11)), "nc1", 10), ("3d", dict(shape=(9, 13, 11)), "nc2", 3),
+]
+
+
+@pytest.mark.parametrize("name,kw,method,k", PRE)
+def test_precond_parity(name, kw, method, k):
+    p = synth.make_problem(name, **kw)
+    s = _solver(p)
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    assert s.allocation(method, k) == al                      # integer decision: bit-exact
+    r = np.random.default_rng(3).standard_normal((p.ell,) + p.shape)
+    z = s.precond_apply(method, k, _dev(r, p.ell)).cpu().numpy()
+    zo = ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)
+    assert _rel(z, zo) <= 1e-12
+    s.close()
+
+
+def test_precond_c_zero_equals_exact_P_alpha():
+    """c = 0: every block is solved exactly at p = 1, so P_NC^{-1} = P_alpha^{-1}."""
+    p = synth.make_problem("headline", shape=(1, 12, 9), c=0.0)
+    s = _solver(p)
+    w = op.weights(p)
+    r = np.random.default_rng(4).standard_normal((p.ell,) + p.shape)
+    z = s.precond_apply("nc2", 8, _dev(r, p.ell)).cpu().numpy()
+    zd = np.linalg.solve(circ.dense_P_alpha(op.dense_A(w), p.ell, p.alpha), r.ravel())
+    assert _rel(z, zd) <= 1e-12 * circ.gamma_condition(p.ell, p.alpha)
+    s.close()
+
+
+GM = [
+    ("1d", {}, None, None),
+    ("2d256", dict(n=256), "nc1", 5),
+    ("2d256", dict(n=256, alpha=1e-4), "nc1", 20),
+    ("headline", dict(n=256), "nc2", 8),
+    ("headline", dict(shape=(1, 100, 73)), "nc1", 8),
+    ("3d", dict(shape=(16, 16, 16)), "nc1", 10),
+]
+
+
+def _oracle_gmres(p, method, k, maxit=200):
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    return og.fgmres(lambda x: op.apply_allatonce(w, x),
+                     lambda r: ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al), p.b, p.rtol, maxit)
+
+
+@pytest.mark.parametrize("name,kw,method,k", GM)
+def test_gmres_parity(name, kw, method, k):
+    p = synth.make_problem(name, **kw)
+    method = method or p.method
+    k = k or p.k
+    s = _solver(p, max_krylov=80)
+    x, info = s.gmres(method, k, _dev(p.b, p.ell), rtol=p.rtol, maxit=80)
+    ro = _oracle_gmres(p, method, k, 80)
+    assert info["converged"] == 1 and ro.converged
+    assert abs(info["iters"] - ro.iters) <= 1
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    assert info["relres_true"] <= 1.5 * p.rtol
+    # paper-unit accounting (Table 1): ell + sum(alloc) per outer iteration
+    al = s.allocation(method, k)
+    assert info["matvecs_paper_units"] == info["iters"] * (p.ell + sum(al))
+    s.close()
+
+
+def test_gmres_equal_iteration_count_agreement():
+    """Forced equal m (rtol = 0, maxit = m): GPU and oracle iterates agree far below 1e-9."""
+    p = synth.make_problem("2d256", shape=(1, 40, 45))
+    s = _solver(p, max_krylov=8)
+    x, info = s.gmres("nc1", 5, _dev(p.b, p.ell), rtol=0.0, maxit=6)
+    ro = _oracle_gmres(p, "nc1", 5, 6)
+    assert info["iters"] == 6 and info["converged"] == 0
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-11
+    s.close()
+
+
+@pytest.mark.parametrize("rhs,expect", [("b1", 1), ("all", 2)])
+def test_gmres_c_zero_exact_counts(rhs, expect):
+    p = synth.make_problem("headline", n=16, c=0.0, rhs=rhs)
+    s = _solver(p, max_krylov=8)
+    x, info = s.gmres("nc2", 8, _dev(p.b, p.ell), rtol=1e-10, maxit=8)
+    assert info["iters"] == expect and info["converged"] == 1
+    s.close()
+
+
+def test_gmres_host_path_matches_device_path():
+    p = synth.make_problem("headline", shape=(1, 48, 40))
+    s = _solver(p, max_krylov=40)
+    xd, info_d = s.gmres("nc2", 8, _dev(p.b, p.ell), rtol=p.rtol, maxit=40)
+    xh, info_h = s.gmres_host("nc2", 8, p.b.reshape(p.ell, -1), rtol=p.rtol, maxit=40)
+    assert info_d["iters"] == info_h["iters"]
+    assert np.array_equal(xd.cpu().numpy(), xh)                # deterministic reductions
+    s.close()
+
+
+def test_gmres_zero_rhs_and_enoconv():
+    p = synth.make_problem("headline", shape=(1, 20, 20))
+    s = _solver(p, max_krylov=4)
+    x, info = s.gmres("nc2", 8, torch.zeros(p.ell, p.N, dtype=torch.float64, device="cuda"), maxit=4)
+    assert info["iters"] == 0 and info["converged"] == 1 and not x.abs().max().item()
+    x, info = s.gmres("nc1", 1, _dev(p.b, p.ell), rtol=1e-14, maxit=3)
+    assert info["iters"] == 3 and info["converged"] == 0
+    s.close()
+
+
+def test_bad_arguments_raise():
+    from paper_2506_03947_b200 import AacError
+    p = synth.make_problem("headline", shape=(1, 8, 8))
+    s = _solver(p, max_krylov=4)
+    r = _dev(np.ones((p.ell, p.N)), p.ell)
+    with pytest.raises(AacError):
+        s.precond_apply("nc1", 0, r)
+    with pytest.raises(AacError):
+        s.gmres("nc1", 2, r, maxit=5)                           # maxit > max_krylov
+    s.close()
+
+
+# ---------------------------------------------------------------- full-size headline
+def test_headline_full_size_apply_parity():
+    """calA and P_NC2 applies at N = 1024^2, ell = 10 (the bench launch configuration)."""
+    p = synth.make_problem("headline")
+    s = _solver(p, max_krylov=4)
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * p.k, "nc2")
+    assert al == [9, 9, 8, 7, 6, 6, 6, 7, 8, 9] and s.allocation("nc2", p.k) == al
+    r = np.random.default_rng(11).standard_normal((p.ell,) + p.shape)
+    assert _rel(s.matvec(_dev(r, p.ell)).cpu().numpy(), op.apply_allatonce(w, r)) <= 1e-12
+    z = s.precond_apply("nc2", p.k, _dev(r, p.ell)).cpu().numpy()
+    assert _rel(z, ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)) <= 1e-12
+    s.close()
+
+
+def test_headline_full_size_gmres_vs_stored_oracle():
+    g = json.load(open(os.path.join(HERE, "golden", "oracle_headline.json")))
+    p = synth.make_problem("headline")
+    s = _solver(p, max_krylov=40)
+    x, info = s.gmres("nc2", p.k, _dev(p.b, p.ell), rtol=p.rtol, maxit=40)
+    assert abs(info["iters"] - g["iters"]) <= 1 and info["converged"] == 1
+    assert info["relres_true"] <= 1.5 * p.rtol
+    xs = x.cpu().numpy().ravel()
+    idx = np.array(g["sample_idx"])
+    ref = np.array(g["sample_x"])
+    assert np.linalg.norm(xs[idx] - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert np.linalg.norm(xs) == pytest.approx(g["x_norm"], rel=1e-9)
+    s.close()
