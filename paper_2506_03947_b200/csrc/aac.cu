@@ -440,7 +440,7 @@ static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z)
       B.q = q;
       B.first = (s == 1);
       B.xs = B.first ? nullptr : slot(s, q);
-      B.xm = B.first ? nullptr : slot(s - 1, q);
+      B.xm = s <= 2 ? nullptr : slot(s - 1, q);
       B.xo = slot(s + 1, q);
       B.ar = P.a_re[kb * P.pmax + s]; B.ai = P.a_im[kb * P.pmax + s];
       B.br = P.b_re[kb * P.pmax + s]; B.bi = P.b_im[kb * P.pmax + s];

@@ -66,7 +66,7 @@ struct NcBlk {
   int q;                     // first plane of the block
   int first;                 // local step s == 1: x_1 = w/theta (virtual), x_0 = 0
   const double* xs;          // x_s, plane q (ignored when first)
-  const double* xm;          // x_{s-1}, plane q (ignored when first)
+  const double* xm;          // x_{s-1}, plane q (NULL when s <= 2: x_1 = w/theta is virtual)
   double* xo;                // x_{s+1}, plane q
   double ar, ai, br, bi;     // a_s = rho_s rho_{s-1}, b_s = 2 rho_s / delta (complex)
   double lr, li;             // Lambda_k
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, NcSweep P, const double* _
       } else {
         xs = B.xs[p];
         Axs = apply_A<DIM>(g, q, B.xs, hl, hh);
-        xm = B.xm[p];
+        xm = B.xm ? B.xm[p] : wr[p] * B.tr;
       }
       const double res = wr[p] - (Axs - B.lr * xs);
       B.xo[p] = xs + B.ar * (xs - xm) + B.br * res;
@@ -122,8 +122,14 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, NcSweep P, const double* _
         ui = B.xs[N + p];
         Aur = apply_A<DIM>(g, q, B.xs, hl, hh);
         Aui = apply_A<DIM>(g, q, B.xs + N, hl + g.S, hh + g.S);
-        mr = B.xm[p];
-        mi = B.xm[N + p];
+        if (B.xm) {
+          mr = B.xm[p];
+          mi = B.xm[N + p];
+        } else {                               // x_1 = w / theta
+          const double w0 = wr[p], w1 = wi[p];
+          mr = w0 * B.tr - w1 * B.ti;
+          mi = w0 * B.ti + w1 * B.tr;
+        }
       }
       // residual w - (A - Lambda) x
       const double rr = wr[p] - (Aur - (B.lr * ur - B.li * ui));
