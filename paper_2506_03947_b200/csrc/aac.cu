@@ -4,11 +4,13 @@
 //   aac_gmres  -> per Arnoldi step: aac_precond_apply -> aac_matvec -> CGS2 (3 passes)
 //                 -> device Givens -> host poll of |g_{j+1}|/beta
 //   aac_precond_apply (NC) -> k_forward -> (P_max - 1) x k_sweep -> k_inverse
+#include <algorithm>
 #include <complex>
 #include <cstdarg>
-#include <mutex>
+#include <cstdlib>
 
 #include "aac_internal.cuh"
+#include "arnoldi.cuh"
 #include "comm.cuh"
 #include "krylov.cuh"
 #include "nc.cuh"
@@ -131,7 +133,6 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   ctx->c = c;
   ctx->alpha = alpha;
   ctx->max_krylov = max_krylov;
-  ctx->stream = (cudaStream_t)cuda_stream;
   cudaGetDevice(&ctx->device);
 
   Geo& G = ctx->geo;
@@ -145,7 +146,9 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   const long long N = G.N;
 
   // Face weights w_f = c kappa_f n_a^2, lower-face layout with one padding layer (host build).
-  const long long lenx = N + 1, leny = N + G.nx, lenz = N + G.S;
+  // sub-array lengths padded to 4 doubles: 16-byte vector loads stay aligned in every array
+  auto pad4 = [](long long v) { return (v + 3) / 4 * 4; };
+  const long long lenx = pad4(N + 1), leny = pad4(N + G.nx), lenz = pad4(N + G.S);
   std::vector<double> hw(lenx + leny + lenz, 0.0);
   double* wx = hw.data();
   double* wy = wx + lenx;
@@ -208,22 +211,41 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
     return rc;
   }
 
+  // library-owned stream + events (graph capture cannot use the legacy default stream)
+  ctx->user_stream = (cudaStream_t)cuda_stream;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_it[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_it[1], cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    aac_destroy(ctx);
+    return aac_fail(nullptr, AAC_ECUDA, "stream/event creation failed");
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (getenv("AAC_NO_GRAPH")) ctx->use_graphs = false;
+  if (ctx->nranks > 1) ctx->use_graphs = false;
+
   // device allocations
   auto alloc = [&](double** p, long long n) -> bool {
     return cudaMalloc((void**)p, (size_t)(n > 0 ? n : 1) * sizeof(double)) == cudaSuccess;
   };
   const long long L = (long long)ell * N;
-  const long long maxctas = (L + KRY_CHUNK - 1) / KRY_CHUNK;
-  ctx->part_ctas = (int)maxctas;
+  const int ldh = max_krylov + 1;
+  ctx->ka_grid = 8 * ctx->num_sms;
+  const long long fwd_ctas = (N + 255) / 256 + 1;
+  ctx->part_len = std::max<long long>((long long)ctx->ka_grid * 2 * ldh, fwd_ctas);
+  ctx->part_len = std::max<long long>(ctx->part_len, 4096);
   bool ok = alloc(&ctx->d_w, hw.size()) && alloc(&ctx->d_what, L) && alloc(&ctx->d_X, 3 * L) &&
-            alloc(&ctx->d_tmp, L) && alloc(&ctx->d_V, (max_krylov + 1) * L) &&
-            alloc(&ctx->d_Z, max_krylov * L) && alloc(&ctx->d_W, L) &&
-            alloc(&ctx->d_halo, 2LL * ell * G.S) &&
-            alloc(&ctx->d_part, maxctas * (max_krylov + 2)) &&
-            alloc(&ctx->d_red, 4LL * (max_krylov + 2)) &&
-            alloc(&ctx->d_H, (long long)(max_krylov + 1) * max_krylov) &&
-            alloc(&ctx->d_giv, 4LL * (max_krylov + 2)) && alloc(&ctx->d_stat, 64);
-  if (ok) ok = cudaMallocHost((void**)&ctx->h_stat, 64 * sizeof(double)) == cudaSuccess;
+            alloc(&ctx->d_tmp, L) && alloc(&ctx->d_V, (long long)(max_krylov + 1) * L) &&
+            alloc(&ctx->d_Z, (long long)max_krylov * L) && alloc(&ctx->d_W, L) &&
+            alloc(&ctx->d_halo, 2LL * ell * G.S) && alloc(&ctx->d_part, ctx->part_len) &&
+            alloc(&ctx->d_red, 3LL * ldh + 8) && alloc(&ctx->d_H, (long long)ldh * max_krylov) &&
+            alloc(&ctx->d_G, (long long)ldh * ldh) && alloc(&ctx->d_giv, 6LL * ldh) &&
+            alloc(&ctx->d_stat, 64) &&
+            cudaMalloc((void**)&ctx->d_st, sizeof(IterState)) == cudaSuccess;
+  if (ok) ok = cudaMallocHost((void**)&ctx->h_stat, 64 * sizeof(double)) == cudaSuccess &&
+               cudaMallocHost((void**)&ctx->h_st, sizeof(IterState)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     aac_destroy(ctx);
@@ -234,7 +256,8 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   G.wy = ctx->d_w + lenx;
   G.wz = ctx->d_w + lenx + leny;
   if (cudaMemcpy(ctx->d_w, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemset(ctx->d_halo, 0, 2LL * ell * G.S * sizeof(double)) != cudaSuccess) {
+      cudaMemset(ctx->d_halo, 0, 2LL * ell * G.S * sizeof(double)) != cudaSuccess ||
+      cudaMemset(ctx->d_st, 0, sizeof(IterState)) != cudaSuccess) {
     aac_destroy(ctx);
     return aac_fail(nullptr, AAC_ECUDA, "setup copy failed");
   }
@@ -259,14 +282,21 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
 
 extern "C" void aac_destroy(aac_ctx* ctx) {
   if (!ctx) return;
-  cudaStreamSynchronize(ctx->stream);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   sp_destroy(ctx);
+  for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
   double* ptrs[] = {ctx->d_w, ctx->d_what, ctx->d_X, ctx->d_tmp, ctx->d_V, ctx->d_Z,
                     ctx->d_W, ctx->d_bx, ctx->d_halo, ctx->d_part, ctx->d_red, ctx->d_H,
-                    ctx->d_giv, ctx->d_stat};
+                    ctx->d_G, ctx->d_giv, ctx->d_stat};
   for (double* p : ptrs)
     if (p) cudaFree(p);
+  if (ctx->d_st) cudaFree(ctx->d_st);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
+  if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto& r : ctx->prof_recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -282,34 +312,62 @@ extern "C" const char* aac_last_error(const aac_ctx* ctx) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Stream handoff: every entry point runs on the library stream, ordered after the caller's
+// stream and before anything the caller enqueues afterwards.
+struct StreamScope {
+  aac_ctx* ctx;
+  explicit StreamScope(aac_ctx* c) : ctx(c) {
+    cudaEventRecord(ctx->ev_in, ctx->user_stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0);
+  }
+  ~StreamScope() {
+    cudaEventRecord(ctx->ev_out, ctx->stream);
+    cudaStreamWaitEvent(ctx->user_stream, ctx->ev_out, 0);
+  }
+};
+
+static inline bool vec2(const aac_ctx* ctx) { return (ctx->geo.nx % 2) == 0; }
+
+// ------------------------------------------------------------------------------------------
 // calA apply
-static int matvec_impl(aac_ctx* ctx, const double* x, double* y) {
+template <int DIM, int VEC>
+static int launch_matvec(aac_ctx* ctx, const double* x, double* y, double bytes) {
   const Geo& g = ctx->geo;
-  const int ell = ctx->ell;
-  if (ctx->nranks > 1) {
-    const double* planes[AAC_MAX_ELL];
-    int qs[AAC_MAX_ELL];
-    for (int j = 0; j < ell; ++j) {
-      planes[j] = x + (long long)j * g.N;
-      qs[j] = j;
-    }
-    AAC_TRY(comm_halo(ctx, planes, qs, ell));
-  }
   const double* hlo = ctx->d_halo;
-  const double* hhi = ctx->d_halo + (long long)ell * g.S;
-  const double V = 8.0 * ell * g.N, C = 8.0 * ctx->dim * g.N;
-  const unsigned grid = grid1d(g.N, 256);
-  switch (ctx->dim) {
-    case 1: LAUNCH(ctx, KID_MATVEC, 2 * V + C, k_matvec<1><<<grid, 256, 0, ctx->stream>>>(g, ell, x, y, hlo, hhi)); break;
-    case 2: LAUNCH(ctx, KID_MATVEC, 2 * V + C, k_matvec<2><<<grid, 256, 0, ctx->stream>>>(g, ell, x, y, hlo, hhi)); break;
-    default: LAUNCH(ctx, KID_MATVEC, 2 * V + C, k_matvec<3><<<grid, 256, 0, ctx->stream>>>(g, ell, x, y, hlo, hhi)); break;
+  const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
+  LAUNCH(ctx, KID_MATVEC, bytes,
+         k_matvec<DIM, VEC><<<grid1d(g.N / VEC, 256), 256, 0, ctx->stream>>>(g, ctx->ell, x, y, hlo, hhi));
+  return AAC_OK;
+}
+
+static int halo_planes(aac_ctx* ctx, const double* x) {
+  if (ctx->nranks == 1) return AAC_OK;
+  const double* planes[AAC_MAX_ELL];
+  int qs[AAC_MAX_ELL];
+  for (int j = 0; j < ctx->ell; ++j) {
+    planes[j] = x + (long long)j * ctx->geo.N;
+    qs[j] = j;
   }
-  ctx->sweeps += ell;
+  return comm_halo(ctx, planes, qs, ctx->ell);
+}
+
+static int matvec_impl(aac_ctx* ctx, const double* x, double* y) {
+  AAC_TRY(halo_planes(ctx, x));
+  const double V = 8.0 * ctx->ell * ctx->geo.N, C = 8.0 * ctx->dim * ctx->geo.N;
+  const double bytes = 2 * V + C;
+  const bool v2 = vec2(ctx);
+  switch (ctx->dim) {
+    case 1: AAC_TRY(v2 ? launch_matvec<1, 2>(ctx, x, y, bytes) : launch_matvec<1, 1>(ctx, x, y, bytes)); break;
+    case 2: AAC_TRY(v2 ? launch_matvec<2, 2>(ctx, x, y, bytes) : launch_matvec<2, 1>(ctx, x, y, bytes)); break;
+    default: AAC_TRY(v2 ? launch_matvec<3, 2>(ctx, x, y, bytes) : launch_matvec<3, 1>(ctx, x, y, bytes)); break;
+  }
+  ctx->sweeps += ctx->ell;
   return AAC_OK;
 }
 
 extern "C" int aac_matvec(aac_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y) return aac_fail(ctx, AAC_EINVAL, "aac_matvec: bad pointers");
+  StreamScope ss(ctx);
   return matvec_impl(ctx, x, y);
 }
 
@@ -354,6 +412,16 @@ static void shift_of_block(const aac_ctx* ctx, int kb, double* lr, double* li) {
   if (kb == h) { *lr = -root; *li = 0.0; return; }
   *lr = root * cos(2.0 * M_PI * kb / ell);          // Lambda_k = alpha^{1/ell} e^{-2 pi i k/ell}
   *li = -root * sin(2.0 * M_PI * kb / ell);
+}
+
+static void inv_theta(const aac_ctx* ctx, int kb, double* tr, double* ti) {
+  double lr, li;
+  shift_of_block(ctx, kb, &lr, &li);
+  const std::complex<double> it =
+      1.0 / std::complex<double>(0.5 * (ctx->mu_max + ctx->mu_min) - lr, -li);
+  const int h = ctx->ell / 2;
+  *tr = it.real();
+  *ti = (kb != 0 && kb != h) ? it.imag() : 0.0;
 }
 
 static const NcPlan& nc_plan(aac_ctx* ctx, int method, int k) {
@@ -412,100 +480,246 @@ static inline int plane_of_block(int ell, int kb) {
   return kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1);
 }
 
-static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
-  const NcPlan& P = nc_plan(ctx, method, k);
+static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
+  ArnoldiCtx ac{};
+  const int ldh = ctx->max_krylov + 1;
+  ac.st = ctx->d_st;
+  ac.H = ctx->d_H;
+  ac.ldh = ldh;
+  ac.cs = ctx->d_giv;
+  ac.sn = ctx->d_giv + ldh;
+  ac.g = ctx->d_giv + 2 * ldh;
+  ac.sigma = ctx->d_giv + 4 * ldh;
+  ac.c = ctx->d_giv + 5 * ldh;
+  ac.G = ctx->d_G;
+  ac.red = ctx->d_red;
+  ac.local_only = ctx->nranks > 1;
+  return ac;
+}
+
+// ------------------------------------------------------------------------------------------
+// Dynamic shared memory beyond 48 KB needs an explicit opt-in per kernel.
+template <typename K>
+static int smem_optin(aac_ctx* ctx, K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return AAC_OK;
+}
+
+template <int ELLC, bool TMA>
+static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
+  const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
+  FwdUpd U{ctx->d_W, ctx->d_V, L, ctx->d_part, arnoldi_ctx(ctx)};
+  const Dft D = make_dft(ctx);
+  const size_t smem = TMA ? (size_t)FS * ELLC * FT * sizeof(double) : 0;
+  AAC_TRY(smem_optin(ctx, k_fwd_upd<ELLC, TMA>, smem));
+  LAUNCH(ctx, KID_FWD, bytes,
+         (k_fwd_upd<ELLC, TMA><<<grid1d(N, FT), FT, smem, ctx->stream>>>(N, D, ctx->d_what, U)));
+  return AAC_OK;
+}
+
+static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
+  const bool tma = (ctx->geo.N % 2) == 0;         // 16-byte aligned plane tiles
+  if (ctx->ell <= 10) return tma ? launch_fwd_upd_t<10, true>(ctx, bytes) : launch_fwd_upd_t<10, false>(ctx, bytes);
+  return tma ? launch_fwd_upd_t<16, true>(ctx, bytes) : launch_fwd_upd_t<16, false>(ctx, bytes);
+}
+
+// ------------------------------------------------------------------------------------------
+// Preconditioner: forward DFT (optionally fused with the Arnoldi update), Chebyshev sweeps,
+// last sweep fused with the inverse DFT. gmres_mode: input is the Arnoldi update (W, V, c),
+// output Z_j with j read on the device; otherwise r -> z.
+template <int DIM, int VEC>
+static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zbase, bool gmres_mode) {
   const Geo& g = ctx->geo;
   const int ell = ctx->ell, h = ell / 2;
   const long long N = g.N, L = (long long)ell * N;
   const double V = 8.0 * L, C = 8.0 * ctx->dim * N;
   const Dft D = make_dft(ctx);
-  const unsigned grid = grid1d(N, 256);
-  LAUNCH(ctx, KID_FWD, 2 * V, k_forward<<<grid, 256, 0, ctx->stream>>>(N, D, r, ctx->d_what));
+  const IterState* st = gmres_mode ? ctx->d_st : nullptr;
+  if (gmres_mode) {
+    // model bytes: read W + V_0..V_{j-1}, write V_j and hat w (j averaged out: counted as 3V)
+    AAC_TRY(launch_fwd_upd(ctx, 3 * V));
+    if (ctx->nranks > 1) {
+      AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
+      LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+    }
+  } else {
+    if (ell <= 10)
+      LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+    else
+      LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+  }
+  const long long zjs = gmres_mode ? L : 0;
+  if (P.pmax == 1) {
+    NcFinal F{};
+    for (int kb = 0; kb <= h; ++kb) inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
+    LAUNCH(ctx, KID_INV, 2 * V,
+           k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, ctx->d_what, zbase, zjs, st));
+    return AAC_OK;
+  }
   double* X = ctx->d_X;
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * g.S;
+  const unsigned gsw = grid1d(N / VEC, SW_TX);
   for (int t = 1; t < P.pmax; ++t) {
+    const bool last = (t == P.pmax - 1);
     NcSweep S{};
     S.nblk = h + 1;
     const double* planes[AAC_MAX_ELL];
     int qs[AAC_MAX_ELL], nh = 0, nplanes = 0;
     for (int kb = 0; kb <= h; ++kb) {
-      NcBlk& B = S.b[kb];
       const int s = t - (P.pmax - P.p[kb]);          // aligned ends: block starts late
-      if (s < 1) { B.kind = 0; continue; }
       const bool cplx = (kb != 0 && kb != h);
       const int q = plane_of_block(ell, kb);
-      B.kind = cplx ? 2 : 1;
+      if (s < 1) {                                     // inactive now; passive at the end
+        S.passive[kb] = 1;
+        inv_theta(ctx, kb, &S.ptr[kb], &S.pti[kb]);
+        continue;
+      }
+      NcBlk& B = S.b[S.nact++];
+      B.kb = kb;
+      B.cplx = cplx ? 1 : 0;
       B.q = q;
-      B.first = (s == 1);
-      B.xs = B.first ? nullptr : slot(s, q);
-      B.xm = s <= 2 ? nullptr : slot(s - 1, q);
-      B.xo = slot(s + 1, q);
+      double tr, ti;
+      inv_theta(ctx, kb, &tr, &ti);
+      const double* wq = ctx->d_what + (long long)q * N;
+      if (s == 1) {                    // x_1 = w/theta, x_0 = 0
+        B.ps = wq; B.sr = tr; B.si = ti;
+        B.pm = wq; B.mr = 0.0; B.mi = 0.0;
+      } else {
+        B.ps = slot(s, q); B.sr = 1.0; B.si = 0.0;
+        if (s == 2) { B.pm = wq; B.mr = tr; B.mi = ti; }
+        else { B.pm = slot(s - 1, q); B.mr = 1.0; B.mi = 0.0; }
+      }
+      B.xo = last ? nullptr : slot(s + 1, q);
       B.ar = P.a_re[kb * P.pmax + s]; B.ai = P.a_im[kb * P.pmax + s];
       B.br = P.b_re[kb * P.pmax + s]; B.bi = P.b_im[kb * P.pmax + s];
       shift_of_block(ctx, kb, &B.lr, &B.li);
-      const std::complex<double> it = 1.0 / std::complex<double>(0.5 * (ctx->mu_max + ctx->mu_min) - B.lr, -B.li);
-      B.tr = it.real();
-      B.ti = cplx ? it.imag() : 0.0;
       const int np = cplx ? 2 : 1;
       for (int e = 0; e < np; ++e) {
-        planes[nh] = (B.first ? ctx->d_what + (long long)q * N : slot(s, q)) + (long long)e * N;
+        planes[nh] = B.ps + (long long)e * N;
         qs[nh++] = q + e;
       }
       nplanes += np;
     }
     AAC_TRY(comm_halo(ctx, planes, qs, nh));
-    const double bytes = 8.0 * N * 4.0 * nplanes + C;
-    switch (ctx->dim) {
-      case 1: LAUNCH(ctx, KID_SWEEP, bytes, k_sweep<1><<<grid, 256, 0, ctx->stream>>>(g, S, ctx->d_what, hlo, hhi)); break;
-      case 2: LAUNCH(ctx, KID_SWEEP, bytes, k_sweep<2><<<grid, 256, 0, ctx->stream>>>(g, S, ctx->d_what, hlo, hhi)); break;
-      default: LAUNCH(ctx, KID_SWEEP, bytes, k_sweep<3><<<grid, 256, 0, ctx->stream>>>(g, S, ctx->d_what, hlo, hhi)); break;
+    const dim3 blk(SW_TX, S.nact);
+    if (last) {
+      const size_t smem = (size_t)ell * SW_TX * VEC * sizeof(double);
+      const double bytes = 8.0 * N * 3.0 * nplanes + C + V;     // x_s, x_{s-1}, w in; z out
+      LAUNCH(ctx, KID_INV, bytes,
+             (k_sweep<DIM, VEC, true><<<gsw, blk, smem, ctx->stream>>>(g, S, D, ctx->d_what, hlo, hhi, zbase, zjs, st)));
+    } else {
+      const double bytes = 8.0 * N * 4.0 * nplanes + C;
+      LAUNCH(ctx, KID_SWEEP, bytes,
+             (k_sweep<DIM, VEC, false><<<gsw, blk, 0, ctx->stream>>>(g, S, D, ctx->d_what, hlo, hhi, nullptr, 0, st)));
     }
     ctx->sweeps += nplanes;
   }
-  NcFinal F{};
-  F.nblk = h + 1;
-  for (int kb = 0; kb <= h; ++kb) {
-    double lr, li;
-    shift_of_block(ctx, kb, &lr, &li);
-    const std::complex<double> it = 1.0 / std::complex<double>(0.5 * (ctx->mu_max + ctx->mu_min) - lr, -li);
-    F.tr[kb] = it.real();
-    F.ti[kb] = (kb != 0 && kb != h) ? it.imag() : 0.0;
-    F.y[kb] = P.p[kb] == 1 ? nullptr : slot(P.p[kb], plane_of_block(ell, kb));
-  }
-  LAUNCH(ctx, KID_INV, 2 * V, k_inverse<<<grid, 256, 0, ctx->stream>>>(N, D, F, ctx->d_what, z));
   return AAC_OK;
+}
+
+static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z, bool gmres_mode) {
+  const NcPlan& P = nc_plan(ctx, method, k);
+  const bool v2 = vec2(ctx);
+  switch (ctx->dim) {
+    case 1: return v2 ? nc_apply_t<1, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<1, 1>(ctx, P, r, z, gmres_mode);
+    case 2: return v2 ? nc_apply_t<2, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<2, 1>(ctx, P, r, z, gmres_mode);
+    default: return v2 ? nc_apply_t<3, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<3, 1>(ctx, P, r, z, gmres_mode);
+  }
 }
 
 extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
   if (k < 1) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
-  if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z);
+  StreamScope ss(ctx);
+  if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z, false);
   if (method == AAC_SP) return sp_apply(ctx, k, r, z);
   return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
 }
 
 // ------------------------------------------------------------------------------------------
-// Fixed-order reductions used by GMRES.
-static int reduce_to(aac_ctx* ctx, int nctas, int nv, double* out) {
-  LAUNCH(ctx, KID_REDUCE, 8.0 * nctas * nv,
-         k_reduce<<<nv, 256, 0, ctx->stream>>>(ctx->d_part, nctas, nv, out));
-  return comm_allreduce(ctx, out, nv, ncclSum);
+// GMRES
+template <int DIM, int ELLC, bool TMA>
+static int launch_arnoldi(aac_ctx* ctx) {
+  const Geo& g = ctx->geo;
+  const int ldh = ctx->max_krylov + 1;
+  KAParams P{ctx->d_Z, ctx->d_V, ctx->d_W, (long long)ctx->ell * g.N, ctx->d_part,
+             ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, arnoldi_ctx(ctx)};
+  const size_t smem = (arnoldi_ring_doubles<ELLC>() + (size_t)(AT / 32 + 1) * 2 * ldh) * sizeof(double);
+  // persistent grid: exactly the resident capacity (no partial second wave)
+  static thread_local int occ_cache[2][4][2] = {};
+  int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0];
+  if (!occ) {
+    AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA>, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA>, AT, smem);
+    if (occ < 1) occ = 1;
+  }
+  const long long ntile = (g.N + AT - 1) / AT;
+  const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ntile);
+  const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
+  LAUNCH(ctx, KID_MATVEC, 2 * V + C, (k_arnoldi<DIM, ELLC, TMA><<<grid, AT, smem, ctx->stream>>>(g, ctx->ell, P)));
+  return AAC_OK;
 }
 
-static size_t red_smem(int nv) { return (size_t)(KRY_THREADS / 32) * (nv > 1 ? nv : 1) * sizeof(double); }
+template <int DIM>
+static int arnoldi_dim(aac_ctx* ctx) {
+  const bool tma = (ctx->geo.N % 2) == 0;
+  if (ctx->ell <= 10) return tma ? launch_arnoldi<DIM, 10, true>(ctx) : launch_arnoldi<DIM, 10, false>(ctx);
+  return tma ? launch_arnoldi<DIM, 16, true>(ctx) : launch_arnoldi<DIM, 16, false>(ctx);
+}
 
-// out[0] = ||w - coef_sign*sum coef_i V_i||^2 ; optional store into w_out
-static int norm2_update(aac_ctx* ctx, const double* V, int nv, const double* coef, double sign,
-                        const double* w_in, double* w_out, double* out) {
-  const long long L = (long long)ctx->ell * ctx->geo.N;
-  const int nctas = (int)((L + KRY_CHUNK - 1) / KRY_CHUNK);
-  const double bytes = 8.0 * L * (nv + 1 + (w_out ? 1 : 0));
-  LAUNCH(ctx, KID_UPD, bytes,
-         k_update<MODE_NORM><<<nctas, KRY_THREADS, red_smem(1), ctx->stream>>>(
-             V, L, nv, coef, sign, w_in, w_out, L, ctx->d_part));
-  return reduce_to(ctx, nctas, 1, out);
+static int arnoldi_impl(aac_ctx* ctx) {
+  switch (ctx->dim) {
+    case 1: return arnoldi_dim<1>(ctx);
+    case 2: return arnoldi_dim<2>(ctx);
+    default: return arnoldi_dim<3>(ctx);
+  }
+}
+
+// One Arnoldi step (device j): precondition V_j -> Z_j (forward fused with the update that
+// forms V_j), then w = calA Z_j with the CGS2 projections and Gram column.
+static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
+  if (method == AAC_SP) {
+    AAC_TRY(sp_gmres_precond(ctx, k));
+  } else {
+    AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true));
+  }
+  if (ctx->nranks > 1) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
+  AAC_TRY(arnoldi_impl(ctx));
+  if (ctx->nranks > 1) {
+    AAC_TRY(comm_allreduce(ctx, ctx->d_red, 2 * (host_j + 1), ncclSum));
+    LAUNCH(ctx, KID_SCALAR, 0, k_scalar_cgs2<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+  }
+  return AAC_OK;
+}
+
+static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
+  for (auto& ge : ctx->graphs)
+    if (ge.method == method && ge.k == k) { *out = &ge; return AAC_OK; }
+  const long long l0 = ctx->launches;
+  CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = arnoldi_step(ctx, method, k, 0);
+  if (rc == AAC_OK) {
+    cudaError_t e = cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e != cudaSuccess) rc = aac_fail(ctx, AAC_ECUDA, "capture memcpy: %s", cudaGetErrorString(e));
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != AAC_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return aac_fail(ctx, AAC_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  GraphEntry ge{method, k, nullptr, (int)(ctx->launches - l0)};
+  ctx->launches = l0;                      // capture launched nothing
+  e = cudaGraphInstantiate(&ge.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return aac_fail(ctx, AAC_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  ctx->graphs.push_back(ge);
+  *out = &ctx->graphs.back();
+  return AAC_OK;
 }
 
 static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* x, double rtol,
@@ -518,84 +732,86 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
   const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
   const int ldh = ctx->max_krylov + 1;
-  const int nctas = (int)((L + KRY_CHUNK - 1) / KRY_CHUNK);
-  double* h1 = ctx->d_red;
-  double* h2 = ctx->d_red + (ctx->max_krylov + 2);
-  double* nr = ctx->d_red + 2 * (ctx->max_krylov + 2);
-  double* cs = ctx->d_giv;
-  double* sn = cs + (ctx->max_krylov + 2);
-  double* gg = sn + (ctx->max_krylov + 2);
-  double* yy = gg + (ctx->max_krylov + 2);
-  double* st = ctx->d_stat;
   const long long sweeps0 = ctx->sweeps;
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_giv, 0, 4LL * (ctx->max_krylov + 2) * sizeof(double), ctx->stream));
-  // beta = ||b||, v_0 = b / beta
-  AAC_TRY(norm2_update(ctx, nullptr, 0, nullptr, 1.0, b, nullptr, nr));
-  LAUNCH(ctx, KID_SCALAR, 0, k_beta<<<1, 1, 0, ctx->stream>>>(nr, st, gg));
-  LAUNCH(ctx, KID_AXPY, 16.0 * L, k_scale<<<grid1d(L, 256), 256, 0, ctx->stream>>>(b, st + ST_INV, ctx->d_V, L));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, st, ST_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  const double beta = ctx->h_stat[ST_BETA];
-  int m = 0, converged = 0;
-  double relres = 1.0;
-  if (beta == 0.0) {
-    CUDA_TRY(ctx, cudaMemsetAsync(x, 0, L * sizeof(double), ctx->stream));
-    converged = 1;
-    relres = 0.0;
-  }
-  long long paper_mv = 0;
+  if (method == AAC_SP) AAC_TRY(sp_prepare(ctx, k));
+  // init: V_0 = b (raw), state, Givens/Gram workspaces
+  IterState init{};
+  init.maxit = maxit;
+  init.rtol = rtol;
+  *ctx->h_st = init;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_st, ctx->h_st, sizeof(IterState), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_V, b, L * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_giv, 0, 6LL * ldh * sizeof(double), ctx->stream));
   int alloc_sum = 0;
   {
     int al[AAC_MAX_ELL];
     allocation(ctx, method, k, al);
     for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
   }
-  for (int j = 0; j < maxit && !converged; ++j) {
-    const double* vj = ctx->d_V + (long long)j * L;
-    double* zj = ctx->d_Z + (long long)j * L;
-    AAC_TRY(aac_precond_apply(ctx, method, k, vj, zj));
-    AAC_TRY(matvec_impl(ctx, zj, ctx->d_W));
-    paper_mv += ctx->ell + (method == AAC_SP ? sp_paper_matvecs(ctx, k) : alloc_sum);
-    // CGS2 pass 1: h1 = V^T w
-    LAUNCH(ctx, KID_DOT, 8.0 * L * (j + 2),
-           k_mdot<<<nctas, KRY_THREADS, red_smem(j + 1), ctx->stream>>>(ctx->d_V, L, j + 1, ctx->d_W, L, ctx->d_part));
-    AAC_TRY(reduce_to(ctx, nctas, j + 1, h1));
-    // pass 2: w -= V h1 ; h2 = V^T w
-    LAUNCH(ctx, KID_UPD, 8.0 * L * (j + 3),
-           k_update<MODE_DOTS><<<nctas, KRY_THREADS, red_smem(j + 1), ctx->stream>>>(
-               ctx->d_V, L, j + 1, h1, 1.0, ctx->d_W, ctx->d_W, L, ctx->d_part));
-    AAC_TRY(reduce_to(ctx, nctas, j + 1, h2));
-    // pass 3: w -= V h2 ; ||w||^2
-    AAC_TRY(norm2_update(ctx, ctx->d_V, j + 1, h2, 1.0, ctx->d_W, ctx->d_W, nr));
-    LAUNCH(ctx, KID_SCALAR, 0, k_arnoldi<<<1, 1, 0, ctx->stream>>>(j, ldh, h1, h2, nr, ctx->d_H, cs, sn, gg, st));
-    LAUNCH(ctx, KID_AXPY, 16.0 * L,
-           k_scale<<<grid1d(L, 256), 256, 0, ctx->stream>>>(ctx->d_W, st + ST_INV, ctx->d_V + (long long)(j + 1) * L, L));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, st, ST_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    m = j + 1;
-    relres = ctx->h_stat[ST_RELRES];
-    if (ctx->h_stat[ST_HNORM] == 0.0 || relres <= rtol) converged = 1;
+  GraphEntry* ge = nullptr;
+  const bool graphs = ctx->use_graphs && !ctx->prof;
+  if (graphs) AAC_TRY(get_graph(ctx, method, k, &ge));
+  // Arnoldi steps. Graph path: replay one captured step per iteration and poll the state of
+  // the PREVIOUS step (speculative: a step launched after convergence returns at once).
+  int it = 0;
+  for (; it < maxit; ++it) {
+    if (graphs) {
+      CUDA_TRY(ctx, cudaGraphLaunch(ge->exec, ctx->stream));
+      ctx->launches += ge->nodes;
+      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_it[it & 1], ctx->stream));
+      if (it >= 1) {
+        CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_it[(it - 1) & 1]));
+        if (ctx->h_st->done) break;
+      }
+    } else {
+      AAC_TRY(arnoldi_step(ctx, method, k, it));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      if (ctx->h_st->done) break;
+    }
   }
-  if (m > 0) {
-    LAUNCH(ctx, KID_SCALAR, 0, k_backsub<<<1, 1, 0, ctx->stream>>>(m, ldh, ctx->d_H, gg, yy));
+  // finalise the last column (no-op when already done) and form x = sum y_i Z_i
+  if (method == AAC_SP) {
+    AAC_TRY(sp_gmres_finalize(ctx));
+  } else {
+    // finalise the last Arnoldi column (same kernel; its transform output is unused)
+    AAC_TRY(launch_fwd_upd(ctx, 0));
+    if (ctx->nranks > 1) {
+      AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
+      LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+    }
+  }
+  double* yy = ctx->d_giv + 3 * ldh;
+  LAUNCH(ctx, KID_SCALAR, 0,
+         k_backsub<<<1, 1, 0, ctx->stream>>>(ctx->d_st, ldh, ctx->d_H, ctx->d_giv + 2 * ldh, ctx->d_giv + 4 * ldh, yy));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const IterState fin = *ctx->h_st;
+  const int m = fin.m;
+  if (m > 0)
     LAUNCH(ctx, KID_AXPY, 8.0 * L * (m + 1),
-           k_lincomb<<<grid1d(L, 256), 256, 0, ctx->stream>>>(ctx->d_Z, L, m, yy, x, L));
-  }
+           k_lincomb<<<grid1d((L + 1) / 2, 256), 256, 0, ctx->stream>>>(ctx->d_Z, L, ctx->d_st, yy, x, L));
+  else
+    CUDA_TRY(ctx, cudaMemsetAsync(x, 0, L * sizeof(double), ctx->stream));
+  const bool converged = fin.relres <= rtol || fin.hn == 0.0 || fin.beta == 0.0;
   double rtrue = 0.0;
-  if (info && beta > 0.0) {
-    // true residual ||b - calA x|| / ||b|| (one extra apply, not counted as an iteration)
+  if (info && fin.beta > 0.0) {
+    // true residual ||b - calA x|| / ||b|| (one extra apply, not an Arnoldi step)
     AAC_TRY(matvec_impl(ctx, x, ctx->d_tmp));
-    AAC_TRY(norm2_update(ctx, ctx->d_tmp, 1, st + ST_ONE, 1.0, b, nullptr, nr));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat + ST_NRM2, nr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    const int nb = std::min<int>(ctx->num_sms * 4, (int)grid1d(L, 256));
+    LAUNCH(ctx, KID_AXPY, 16.0 * L, k_diffnorm<<<nb, 256, 0, ctx->stream>>>(b, ctx->d_tmp, L, ctx->d_part));
+    LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
+    AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    rtrue = sqrt(ctx->h_stat[ST_NRM2]) / beta;
+    rtrue = sqrt(ctx->h_stat[0]) / fin.beta;
   }
   if (info) {
     info->iters = m;
-    info->converged = converged;
-    info->relres_est = relres;
+    info->converged = converged ? 1 : 0;
+    info->relres_est = fin.relres;
     info->relres_true = rtrue;
-    info->matvecs_paper_units = paper_mv;
+    info->matvecs_paper_units = (long long)m * (ctx->ell + (method == AAC_SP ? sp_paper_matvecs(ctx, k) : alloc_sum));
     info->stencil_sweeps = ctx->sweeps - sweeps0;
   }
   return converged ? AAC_OK : AAC_ENOCONV;
@@ -604,6 +820,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
 extern "C" int aac_gmres(aac_ctx* ctx, int method, int k, const double* b, double* x, double rtol,
                          int maxit, aac_gmres_info* info) {
   if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_gmres: bad pointers");
+  StreamScope ss(ctx);
   return gmres_impl(ctx, method, k, b, x, rtol, maxit, info);
 }
 
@@ -613,8 +830,10 @@ extern "C" int aac_gmres_host(aac_ctx* ctx, int method, int k, const double* b_h
   const long long L = (long long)ctx->ell * ctx->geo.N;
   if (!ctx->d_bx && cudaMalloc((void**)&ctx->d_bx, 2 * L * sizeof(double)) != cudaSuccess) {
     ctx->d_bx = nullptr;
+    cudaGetLastError();
     return aac_fail(ctx, AAC_ENOMEM, "staging allocation failed");
   }
+  StreamScope ss(ctx);
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_bx, b_host, L * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   const int rc = gmres_impl(ctx, method, k, ctx->d_bx, ctx->d_bx + L, rtol, maxit, info);
   if (rc < 0) return rc;

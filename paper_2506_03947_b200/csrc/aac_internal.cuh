@@ -64,7 +64,14 @@ struct NcPlan {            // inner Chebyshev plan for (method, k)
   std::vector<double> a_re, a_im, b_re, b_im;   // [blk][s] s = 1..p-1, row stride pmax
 };
 
-struct SpPlan;             // saddle-point plan (aac_sp.cuh)
+struct SpPlan;             // saddle-point plan (sp.cuh)
+struct IterState;          // GMRES device state (krylov.cuh)
+
+struct GraphEntry {        // one captured Arnoldi step per (method, k)
+  int method, k;
+  cudaGraphExec_t exec;
+  int nodes;
+};
 
 struct aac_ctx {
   // problem
@@ -75,8 +82,12 @@ struct aac_ctx {
   double mu_min = 1.0, mu_max = 1.0;
   Geo geo{};
   int max_krylov = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t user_stream = nullptr;  // caller's stream (entry / exit ordering)
+  cudaStream_t stream = nullptr;       // library-owned non-blocking stream (graph capture)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_it[2] = {nullptr, nullptr};
   int device = 0;
+  int num_sms = 148;
+  int ka_grid = 0;                     // persistent grid of k_arnoldi
   // device memory (library-owned)
   double* d_w = nullptr;               // wx | wy | wz
   double* d_what = nullptr;            // [ell][N] packed half-complex DFT of the input
@@ -87,13 +98,18 @@ struct aac_ctx {
   double* d_W = nullptr;               // [ell][N] Arnoldi work vector
   double* d_bx = nullptr;              // [2][ell][N] staging for aac_gmres_host
   double* d_halo = nullptr;            // [2][ell][S]  lo | hi
-  double* d_part = nullptr;            // partial sums [max_ctas][max_krylov+2]
-  double* d_red = nullptr;             // reduced sums  (several vectors of max_krylov+2)
-  double* d_H = nullptr;               // Hessenberg (max_krylov+1) x max_krylov, col-major
-  double* d_giv = nullptr;             // cs | sn | g | y
+  double* d_part = nullptr;            // per-CTA partial sums
+  long long part_len = 0;
+  double* d_red = nullptr;             // reduced sums / scratch (3 * ldh)
+  double* d_H = nullptr;               // Hessenberg ldh x max_krylov, col-major
+  double* d_G = nullptr;               // Gram matrix ldh x ldh
+  double* d_giv = nullptr;             // cs | sn | g | y | sigma | c   (ldh each)
   double* d_stat = nullptr;            // small scalars (device)
   double* h_stat = nullptr;            // pinned mirror
-  int part_ctas = 0;
+  IterState* d_st = nullptr;
+  IterState* h_st = nullptr;           // pinned mirror (graph memcpy node target)
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
   // plans
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;
@@ -123,9 +139,9 @@ int aac_fail(aac_ctx* ctx, int code, const char* fmt, ...);
                       cudaGetErrorString(e_));                                              \
   } while (0)
 
-#define AAC_TRY(call)        \
+#define AAC_TRY(...)         \
   do {                       \
-    int r_ = (call);         \
+    int r_ = (__VA_ARGS__);  \
     if (r_ < 0) return r_;   \
   } while (0)
 
@@ -144,6 +160,10 @@ struct LaunchScope {
     __VA_ARGS__;                                                                            \
     AAC_TRY(ls_.end());                                                                     \
   } while (0)
+
+// Loop over the ell planes of a point with compile-time indices (register-resident arrays).
+// ELLC is the compile-time plane capacity of the kernel (10 or 16; ell <= ELLC).
+#define FOR_PL(pl) _Pragma("unroll") for (int pl = 0; pl < ELLC; ++pl) if (pl < ell)
 
 inline unsigned grid1d(long long n, int threads) {
   long long g = (n + threads - 1) / threads;

@@ -1,0 +1,165 @@
+// arnoldi.cuh -- CGS2 pass 1 fused with the calA apply (see krylov.cuh for the scheme).
+//
+//   w = calA Z_j (raw), s_i = <V_i, w>, gg_i = <V_i, V_j>, i <= j,
+// one read of the basis for both the projections and the new Gram column. Persistent
+// grid-stride CTAs accumulate per-warp partial sums in shared memory; the last CTA sums
+// the per-CTA partials in a fixed order and runs the CGS2 scalar algebra.
+#pragma once
+
+#include "krylov.cuh"
+#include "stencil.cuh"
+#include "tma.cuh"
+
+struct KAParams {
+  const double* Z;            // raw preconditioned basis, stride L
+  const double* V;            // raw Krylov basis, stride L
+  double* W;                  // w = calA Z_j (raw)
+  long long L;
+  double* part;               // [gridDim.x][2*(j+1)]
+  const double* hlo;
+  const double* hhi;
+  ArnoldiCtx ac;
+};
+
+constexpr int AT = 256;          // tile points per CTA iteration (one per thread)
+constexpr int AS = 3;            // bulk-copy pipeline stages for the basis tiles
+
+// Dynamic shared memory layout: [AS][ELLC][AT] basis ring | [nw][2*(ldh)] acc | [2*ldh] tot
+template <int ELLC>
+__host__ __device__ constexpr size_t arnoldi_ring_doubles() { return (size_t)AS * ELLC * AT; }
+
+template <int DIM, int ELLC, bool TMA>
+__global__ void __launch_bounds__(AT, 2) k_arnoldi(Geo g, int ell, KAParams P) {
+  IterState* st = P.ac.st;
+  if (st->done) return;
+  const int j = st->j;
+  const int nv = j + 1, nv2 = 2 * nv;
+  extern __shared__ __align__(16) double smem[];
+  double* ring = smem;
+  double* acc = smem + arnoldi_ring_doubles<ELLC>();
+  __shared__ __align__(8) uint64_t bar[AS];
+  __shared__ bool last;
+  const int nw = AT / 32, t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int k = t; k < nw * nv2; k += AT) acc[k] = 0.0;
+  const long long N = g.N;
+  const long long ntile = (N + AT - 1) / AT;
+  const long long my_tiles = blockIdx.x < ntile ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long long nitems = my_tiles * nv;       // item k -> (tile r = k / nv, basis vector i = k % nv)
+  auto tile_base = [&](long long r) { return (blockIdx.x + r * gridDim.x) * (long long)AT; };
+  auto issue = [&](long long k) {
+    const long long r = k / nv;
+    const int i = (int)(k % nv);
+    const long long b = tile_base(r);
+    const int len = (int)((N - b) < AT ? (N - b) : AT);
+    const int s = (int)(k % AS);
+    bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + b, N, ell, len, &bar[s]);
+  };
+  if constexpr (TMA) {
+    if (t == 0) {
+      for (int s = 0; s < AS; ++s) mbar_init(&bar[s], 1);
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if constexpr (TMA) {
+    if (t == 0)
+      for (long long k = 0; k < nitems && k < AS; ++k) issue(k);
+  }
+  const double* z = P.Z + (long long)j * P.L;
+  const double* vj = P.V + (long long)j * P.L;
+  for (long long r = 0; r < my_tiles; ++r) {
+    const long long b = tile_base(r);
+    const int len = (int)((N - b) < AT ? (N - b) : AT);
+    const int lb = len & ~1;
+    const bool valid = t < len;
+    const long long p = b + t;
+    double w[ELLC], u[ELLC];
+    if (valid) {
+      PtV<DIM, 1> q;
+      load_ptv<DIM, 1>(g, p, q);
+      // planes in pairs: all loads of a pair are issued before its stores
+#pragma unroll
+      for (int g0 = 0; g0 < ELLC; g0 += 2) {
+        SV<1> sv[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int pl = g0 + k;
+          if (pl < ell) {
+            load_sv<DIM, 1>(g, q, z + (long long)pl * N, P.hlo + pl * g.S, P.hhi + pl * g.S, sv[k]);
+            u[pl] = vj[(long long)pl * N + p];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int pl = g0 + k;
+          if (pl < ell) {
+            double a[1];
+            stencil_sv<DIM, 1>(q, sv[k], a);
+            w[pl] = a[0];
+            if (pl > 0) w[pl] -= (k > 0) ? sv[0].c[0] : z[(long long)(pl - 1) * N + p];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int pl = g0 + k;
+          if (pl < ell) P.W[(long long)pl * N + p] = w[pl];
+        }
+      }
+    }
+    for (int i = 0; i < nv; ++i) {
+      const long long k = r * nv + i;
+      const int s = (int)(k % AS);
+      if constexpr (TMA) mbar_wait(&bar[s], (uint32_t)((k / AS) & 1));
+      double sa = 0.0, ga = 0.0;
+      if (valid) {
+        const double* vi = P.V + (long long)i * P.L + b;
+        FOR_PL(pl) {
+          const double v = (TMA && t < lb) ? ring[((long long)s * ELLC + pl) * AT + t] : vi[(long long)pl * N + t];
+          sa = fma(v, w[pl], sa);
+          ga = fma(v, u[pl], ga);
+        }
+      }
+      sa = warp_sum(sa);
+      ga = warp_sum(ga);
+      if (lane == 0) {
+        acc[warp * nv2 + i] += sa;
+        acc[warp * nv2 + nv + i] += ga;
+      }
+      if constexpr (TMA) {
+        __syncthreads();                          // stage s consumed by every warp
+        if (t == 0 && k + AS < nitems) issue(k + AS);
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = t; k < nv2; k += AT) {
+    double sum = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) sum += acc[w2 * nv2 + k];
+    P.part[(long long)blockIdx.x * nv2 + k] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    const unsigned tk = atomicAdd(&st->tick, 1u);
+    last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double* tot = acc + nw * nv2;
+  for (int k = warp; k < nv2; k += nw) {       // fixed order: lane-strided, then warp tree
+    double sum = 0.0;
+    for (int c = lane; c < (int)gridDim.x; c += 32) sum += __ldcg(P.part + (long long)c * nv2 + k);
+    sum = warp_sum(sum);
+    if (lane == 0) tot[k] = sum;
+  }
+  __syncthreads();
+  if (t == 0) {
+    st->tick = 0;
+    if (P.ac.local_only) {
+      for (int k = 0; k < nv2; ++k) P.ac.red[k] = tot[k];
+    } else {
+      arnoldi_cgs2_step(P.ac, j, tot, tot + nv);
+    }
+  }
+}

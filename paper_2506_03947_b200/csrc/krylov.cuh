@@ -1,19 +1,47 @@
 // krylov.cuh -- flexible GMRES building blocks (BASELINE.json north_star; not in the paper).
 //
-// CGS2 (reading R14) as three streaming passes over the Krylov basis:
-//   pass 1  h  = V^T w                         (k_mdot)
-//   pass 2  w -= V h ;  h' = V^T w             (k_update<MODE_DOTS>, one read of V)
-//   pass 3  w -= V h';  ||w||^2                (k_update<MODE_NORM>)
-// Every pass writes per-CTA partial sums; k_reduce sums them in a FIXED order (the result
-// is bitwise reproducible run to run). Scalars (Givens rotations, residual estimate, the
-// triangular solve) stay on the device (single-thread kernels).
+// Arnoldi with CGS2 (reading R14) organised for HBM traffic:
+//   * the basis is stored UNNORMALISED (V_i raw, sigma_i = 1/||V_i||), so the update that
+//     forms the next vector u = w - V c can be fused into the next preconditioner's forward
+//     transform (k_forward<UPD>) without waiting for ||u||;
+//   * pass 1 (k_arnoldi, fused with the calA apply): s = V^T w and the new Gram column
+//     V^T v_j in ONE read of the basis; the second CGS pass is formed algebraically,
+//     h2 = V^T (w - V h1) = h1 - G h1 with G = V^T V the (normalised) Gram matrix, which is
+//     identical to classical CGS2 in exact arithmetic; c = h1 + h2 is column j of H;
+//   * every reduction is per-CTA partials + a fixed-order sum in the LAST CTA (bitwise
+//     reproducible), followed by the scalar algebra (Givens, residual estimate, flags) on
+//     the device: no host round trip inside an Arnoldi step.
+// Multi-rank: the last CTA only reduces locally; an NCCL all-reduce and k_scalar_* follow.
 #pragma once
 
 #include "aac_internal.cuh"
 
-constexpr int KRY_THREADS = 256;
-constexpr int KRY_E = 8;                        // elements per thread per CTA chunk
-constexpr long long KRY_CHUNK = (long long)KRY_THREADS * KRY_E;
+struct IterState {
+  int j;            // column under construction
+  int done;         // 1: converged / breakdown / maxit -> every iteration kernel returns
+  int m;            // completed Arnoldi columns
+  int maxit;
+  unsigned tick;    // last-CTA ticket (reset by the last CTA)
+  unsigned pad;
+  double beta;      // ||b||
+  double relres;    // |g_m| / beta
+  double rtol;
+  double hn;        // last H[j+1, j]
+};
+
+struct ArnoldiCtx {
+  IterState* st;
+  double* H;        // (ldh x max_krylov) column-major, ldh = max_krylov + 1
+  int ldh;
+  double* cs;       // Givens cosines
+  double* sn;       // Givens sines
+  double* g;        // rotated rhs
+  double* sigma;    // 1/||V_i raw||
+  double* c;        // CGS2 coefficients of the pending column (normalised basis)
+  double* G;        // Gram matrix (ldh x ldh)
+  double* red;      // multi-rank: locally reduced raw sums before the all-reduce
+  int local_only;   // 1 when nranks > 1
+};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -21,194 +49,148 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-reduce one value per thread into red[warp][i]; caller syncs and combines.
-__device__ __forceinline__ void stash(double* red, int nv, int i, double v) {
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * nv + i] = v;
-}
-
-__device__ __forceinline__ void flush_partials(const double* red, int nv, double* part) {
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += red[w * nv + i];
-    part[(long long)blockIdx.x * nv + i] = s;
-  }
-}
-
-// part[cta][i] = sum over the CTA's chunk of V_i . w, i < nv
-__global__ void __launch_bounds__(KRY_THREADS) k_mdot(const double* __restrict__ V, long long ldv,
-                                                      int nv, const double* __restrict__ w,
-                                                      long long n, double* __restrict__ part) {
-  extern __shared__ double red[];
-  const long long base = (long long)blockIdx.x * KRY_CHUNK + threadIdx.x;
-  double wr[KRY_E];
-#pragma unroll
-  for (int e = 0; e < KRY_E; ++e) {
-    const long long idx = base + (long long)e * KRY_THREADS;
-    wr[e] = idx < n ? w[idx] : 0.0;
-  }
-  for (int i = 0; i < nv; ++i) {
-    const double* v = V + (long long)i * ldv;
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < KRY_E; ++e) {
-      const long long idx = base + (long long)e * KRY_THREADS;
-      if (idx < n) acc = fma(v[idx], wr[e], acc);
-    }
-    stash(red, nv, i, acc);
-  }
-  flush_partials(red, nv, part);
-}
-
-enum { MODE_DOTS = 0, MODE_NORM = 1 };
-
-// w_out = w_in - sum_i coef[i] V_i, then per-CTA partials of V^T w_out (MODE_DOTS) or of
-// ||w_out||^2 (MODE_NORM, partial slot 0). w_out may be NULL (no store), nv may be 0.
-template <int MODE>
-__global__ void __launch_bounds__(KRY_THREADS) k_update(const double* __restrict__ V, long long ldv,
-                                                        int nv, const double* __restrict__ coef,
-                                                        double coef_sign,
-                                                        const double* __restrict__ w_in,
-                                                        double* __restrict__ w_out, long long n,
-                                                        double* __restrict__ part) {
-  extern __shared__ double red[];
-  const long long base = (long long)blockIdx.x * KRY_CHUNK + threadIdx.x;
-  double wr[KRY_E];
-#pragma unroll
-  for (int e = 0; e < KRY_E; ++e) {
-    const long long idx = base + (long long)e * KRY_THREADS;
-    wr[e] = idx < n ? w_in[idx] : 0.0;
-  }
-  for (int i = 0; i < nv; ++i) {
-    const double* v = V + (long long)i * ldv;
-    const double c = coef_sign * coef[i];
-#pragma unroll
-    for (int e = 0; e < KRY_E; ++e) {
-      const long long idx = base + (long long)e * KRY_THREADS;
-      if (idx < n) wr[e] = fma(-c, v[idx], wr[e]);
-    }
-  }
-  if (w_out) {
-#pragma unroll
-    for (int e = 0; e < KRY_E; ++e) {
-      const long long idx = base + (long long)e * KRY_THREADS;
-      if (idx < n) w_out[idx] = wr[e];
-    }
-  }
-  if (MODE == MODE_DOTS) {
-    for (int i = 0; i < nv; ++i) {
-      const double* v = V + (long long)i * ldv;
-      double acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < KRY_E; ++e) {
-        const long long idx = base + (long long)e * KRY_THREADS;
-        if (idx < n) acc = fma(v[idx], wr[e], acc);
-      }
-      stash(red, nv, i, acc);
-    }
-    flush_partials(red, nv, part);
-  } else {
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < KRY_E; ++e) acc = fma(wr[e], wr[e], acc);
-    stash(red, 1, 0, acc);
-    flush_partials(red, 1, part);
-  }
-}
-
-// out[i] = sum_c part[c][i] in a fixed order (one CTA per i).
-__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ part, int nctas, int nv,
-                                                double* __restrict__ out) {
-  __shared__ double red[8];
-  const int i = blockIdx.x;
+// Fixed-order sum of n values by one CTA (lane-strided, warp tree, warps in order).
+__device__ double block_sum_fixed(const double* v, int n) {
+  __shared__ double wsum[32];
   double s = 0.0;
-  for (int c = threadIdx.x; c < nctas; c += blockDim.x) s += part[(long long)c * nv + i];
+  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < n; i += blockDim.x * blockDim.y)
+    s += __ldcg(v + i);                      // written by other CTAs: bypass L1
+  s = warp_sum(s);
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  if ((tid & 31) == 0) wsum[tid >> 5] = s;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += wsum[w];
+  __syncthreads();
+  return t;
+}
+
+// ||u||^2 of the vector just formed: j == 0 -> beta; else H[j, j-1] and Givens of column j-1.
+__device__ void arnoldi_norm_step(const ArnoldiCtx& ac, int j, double nrm2) {
+  IterState* st = ac.st;
+  const double nu = sqrt(nrm2);
+  ac.sigma[j] = nu > 0.0 ? 1.0 / nu : 0.0;
+  if (j == 0) {
+    st->beta = nu;
+    ac.g[0] = nu;
+    st->relres = 1.0;
+    st->m = 0;
+    if (nu == 0.0) {
+      st->relres = 0.0;
+      st->done = 1;
+    }
+    return;
+  }
+  const int col = j - 1;
+  double* h = ac.H + (long long)col * ac.ldh;
+  for (int i = 0; i < j; ++i) h[i] = ac.c[i];
+  h[j] = nu;
+  for (int i = 0; i < col; ++i) {
+    const double t = ac.cs[i] * h[i] + ac.sn[i] * h[i + 1];
+    h[i + 1] = -ac.sn[i] * h[i] + ac.cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double r = hypot(h[col], h[col + 1]);
+  ac.cs[col] = h[col] / r;
+  ac.sn[col] = h[col + 1] / r;
+  h[col] = r;
+  h[col + 1] = 0.0;
+  ac.g[col + 1] = -ac.sn[col] * ac.g[col];
+  ac.g[col] = ac.cs[col] * ac.g[col];
+  st->hn = nu;
+  st->m = j;
+  st->relres = fabs(ac.g[col + 1]) / st->beta;
+  if (st->relres <= st->rtol || nu == 0.0 || j >= st->maxit) st->done = 1;
+}
+
+// CGS2 coefficients of column j from the raw sums s_i = <V_i, W>, gg_i = <V_i, V_j>.
+__device__ void arnoldi_cgs2_step(const ArnoldiCtx& ac, int j, const double* s, const double* gg) {
+  const int ld = ac.ldh;
+  const double sj = ac.sigma[j];
+  double* h1 = ac.red + 2 * ld;              // scratch
+  for (int i = 0; i <= j; ++i) {
+    h1[i] = ac.sigma[i] * sj * s[i];
+    const double gij = ac.sigma[i] * sj * gg[i];
+    ac.G[(long long)j * ld + i] = gij;
+    ac.G[(long long)i * ld + j] = gij;
+  }
+  for (int i = 0; i <= j; ++i) {             // h2 = h1 - G h1 ;  c = h1 + h2
+    double t = 0.0;
+    for (int k = 0; k <= j; ++k) t = fma(ac.G[(long long)k * ld + i], h1[k], t);
+    ac.c[i] = h1[i] + (h1[i] - t);
+  }
+  ac.st->j = j + 1;
+}
+
+// Multi-rank scalar kernels (after the NCCL all-reduce of the local sums).
+__global__ void k_scalar_norm(ArnoldiCtx ac) {
+  if (ac.st->done) return;
+  arnoldi_norm_step(ac, ac.st->j, ac.red[0]);
+}
+__global__ void k_scalar_cgs2(ArnoldiCtx ac) {
+  if (ac.st->done) return;
+  const int j = ac.st->j;
+  arnoldi_cgs2_step(ac, j, ac.red, ac.red + (j + 1));
+}
+
+// y = R^{-1} g for the m x m upper-triangular rotated Hessenberg; y_i *= sigma_i so that
+// x = sum_i y_i Z_i with the RAW preconditioned vectors Z_i = P^{-1} V_i(raw).
+__global__ void k_backsub(const IterState* st, int ldh, const double* __restrict__ H,
+                          const double* __restrict__ g, const double* __restrict__ sigma,
+                          double* __restrict__ y) {
+  const int m = st->m;
+  for (int i = m - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int k = i + 1; k < m; ++k) s -= H[(long long)k * ldh + i] * y[k];
+    y[i] = s / H[(long long)i * ldh + i];
+  }
+  for (int i = 0; i < m; ++i) y[i] *= sigma[i];
+}
+
+// x = sum_{i<m} y[i] Z_i
+__global__ void __launch_bounds__(256) k_lincomb(const double* __restrict__ Z, long long ldz,
+                                                 const IterState* st, const double* __restrict__ y,
+                                                 double* __restrict__ x, long long n) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (i >= n) return;
+  const int m = st->m;
+  double s0 = 0.0, s1 = 0.0;
+  const bool two = i + 1 < n;
+  for (int k = 0; k < m; ++k) {
+    const double yk = y[k];
+    const double* z = Z + (long long)k * ldz + i;
+    s0 = fma(yk, z[0], s0);
+    if (two) s1 = fma(yk, z[1], s1);
+  }
+  x[i] = s0;
+  if (two) x[i + 1] = s1;
+}
+
+// part[cta] = sum over the CTA's elements of (a - b)^2   (b may be NULL)
+__global__ void __launch_bounds__(256) k_diffnorm(const double* __restrict__ a,
+                                                  const double* __restrict__ b, long long n,
+                                                  double* __restrict__ part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double d = a[i] - (b ? b[i] : 0.0);
+    s = fma(d, d, s);
+  }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    out[i] = t;
+    part[blockIdx.x] = t;
   }
 }
 
-// Status block layout (device d_stat, mirrored to pinned host):
-enum {
-  ST_RELRES = 0,   // |g_{j+1}| / beta
-  ST_HNORM,        // H[j+1, j]
-  ST_INV,          // 1 / H[j+1, j] (scale for v_{j+1}); 1/beta for v_0
-  ST_BETA,         // ||b||
-  ST_ONE,          // constant 1.0
-  ST_NRM2,         // scratch: reduced squared norm
-  ST_COUNT
-};
-
-// beta = sqrt(nrm2); g = (beta, 0, ...); inv = 1/beta.
-__global__ void k_beta(const double* __restrict__ nrm2, double* __restrict__ stat,
-                       double* __restrict__ g) {
-  const double beta = sqrt(nrm2[0]);
-  stat[ST_BETA] = beta;
-  stat[ST_INV] = beta > 0.0 ? 1.0 / beta : 0.0;
-  stat[ST_RELRES] = 1.0;
-  stat[ST_ONE] = 1.0;
-  g[0] = beta;
-}
-
-// Arnoldi column j: H[0..j, j] = h1 + h2, H[j+1, j] = ||w||; apply old rotations, form the
-// new one (r = hypot, c = h_jj/r, s = h_{j+1,j}/r; reading R14) and update g.
-__global__ void k_arnoldi(int j, int ldh, const double* __restrict__ h1,
-                          const double* __restrict__ h2, const double* __restrict__ nrm2,
-                          double* __restrict__ H, double* __restrict__ cs, double* __restrict__ sn,
-                          double* __restrict__ g, double* __restrict__ stat) {
-  double* col = H + (long long)j * ldh;
-  for (int i = 0; i <= j; ++i) col[i] = h1[i] + h2[i];
-  const double hn = sqrt(nrm2[0]);
-  col[j + 1] = hn;
-  for (int i = 0; i < j; ++i) {
-    const double t = cs[i] * col[i] + sn[i] * col[i + 1];
-    col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
-    col[i] = t;
-  }
-  const double r = hypot(col[j], col[j + 1]);
-  cs[j] = col[j] / r;
-  sn[j] = col[j + 1] / r;
-  col[j] = r;
-  col[j + 1] = 0.0;
-  g[j + 1] = -sn[j] * g[j];
-  g[j] = cs[j] * g[j];
-  stat[ST_HNORM] = hn;
-  stat[ST_INV] = hn > 0.0 ? 1.0 / hn : 0.0;
-  stat[ST_RELRES] = fabs(g[j + 1]) / stat[ST_BETA];
-}
-
-// y = R^{-1} g for the m x m upper-triangular rotated Hessenberg.
-__global__ void k_backsub(int m, int ldh, const double* __restrict__ H, const double* __restrict__ g,
-                          double* __restrict__ y) {
-  for (int i = m - 1; i >= 0; --i) {
-    double s = g[i];
-    for (int k = i + 1; k < m; ++k) s -= H[(long long)k * ldh + i] * y[k];
-    y[i] = s / H[(long long)i * ldh + i];
-  }
-}
-
-// out = scale[0] * w
-__global__ void __launch_bounds__(256) k_scale(const double* __restrict__ w,
-                                               const double* __restrict__ scale,
-                                               double* __restrict__ out, long long n) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = scale[0] * w[i];
-}
-
-// x = sum_i y[i] Z_i
-__global__ void __launch_bounds__(256) k_lincomb(const double* __restrict__ Z, long long ldz, int m,
-                                                 const double* __restrict__ y,
-                                                 double* __restrict__ x, long long n) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double s = 0.0;
-  for (int k = 0; k < m; ++k) s = fma(y[k], Z[(long long)k * ldz + i], s);
-  x[i] = s;
+// out[0] = sum_c part[c] (fixed order, one CTA)
+__global__ void __launch_bounds__(256) k_sum(const double* __restrict__ part, int n,
+                                             double* __restrict__ out) {
+  const double t = block_sum_fixed(part, n);
+  if (threadIdx.x == 0) out[0] = t;
 }

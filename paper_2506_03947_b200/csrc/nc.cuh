@@ -3,17 +3,28 @@
 // P_alpha^{-1} r = (Gamma^{-1} U (x) I)(I (x) A - Lambda (x) I)^{-1}(U^* Gamma (x) I) r
 // (PAPER.md:252-254 Eq. eq:Paform, pairing of reading R6), block problems
 // (A - Lambda_k) y_k = w_k (Eq. eq:blockproblem) solved by p_k Chebyshev iterations
-// (recurrence of reading R8).
+// (recurrence of reading R8):
+//   x_0 = 0, x_1 = w/theta, x_{s+1} = x_s + a_s (x_s - x_{s-1}) + b_s (w - (A - Lambda) x_s).
 //
-// Packed half-complex layout: for real input the ell Fourier
-// blocks satisfy w_{ell-k} = conj(w_k), so only k = 0..ell/2 are solved:
+// Packed half-complex layout: for real input the ell Fourier blocks satisfy
+// w_{ell-k} = conj(w_k), so only k = 0..ell/2 are solved:
 //   plane 0            = block 0 (real, Lambda_0 = alpha^{1/ell})
 //   planes 2k-1, 2k    = Re, Im of block k, k = 1..ell/2-1
 //   plane ell-1        = block ell/2 (real, Lambda = -alpha^{1/ell})
 // i.e. ell real planes, the same bytes as the real block vector.
+//
+// Kernels (one GMRES iteration = k_forward, P_max-2 x k_sweep, k_sweep<LAST>):
+//   k_forward   (optional fused Arnoldi update u = s_w W - sum_i c_i s_i V_i, its squared
+//                norm and the new basis vector) + gamma-scale + real->half-complex DFT
+//   k_sweep     one Chebyshev step for every block active at this sweep (aligned ends:
+//                block k starts at sweep P_max - p_k), threadIdx.y = block
+//   k_sweep<LAST> the final step of every block fused with the inverse DFT and
+//                gamma^{-1} scaling: x_{p_k} never goes to HBM
 #pragma once
 
+#include "krylov.cuh"
 #include "stencil.cuh"
+#include "tma.cuh"
 
 struct Dft {
   int ell;
@@ -24,154 +35,331 @@ struct Dft {
   double scale;              // ell^{-1/2}
 };
 
-// hat w = U^* Gamma r, packed. One thread per point, ell loads / ell stores.
-__global__ void __launch_bounds__(256) k_forward(long long N, Dft D, const double* __restrict__ r,
-                                                 double* __restrict__ what) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= N) return;
+__device__ __forceinline__ int plane_of(int ell, int kb) {
+  const int h = ell / 2;
+  return kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1);
+}
+
+// Arnoldi update fused into the forward transform (GMRES mode, see krylov.cuh):
+//   u = sigma_{j-1} W - sum_{i<j} c_i sigma_i V_i   written to V_j (unnormalised), ||u||^2 reduced.
+struct FwdUpd {
+  const double* W;           // calA Z_{j-1} (raw)
+  double* V;                 // raw basis base pointer, stride L (V_0 = b on entry)
+  long long L;
+  double* part;              // per-CTA partials of ||u||^2
+  ArnoldiCtx ac;             // st, sigma, c (CGS2 coefficients of column j-1), Givens state
+};
+
+// gamma-scale + real -> packed half-complex DFT of the ell values w[] of one point.
+template <int ELLC>
+__device__ __forceinline__ void dft_store(const Dft& D, long long N, long long p, double* w,
+                                          double* __restrict__ what) {
   const int ell = D.ell, h = ell / 2;
-  double w[AAC_MAX_ELL];
-#pragma unroll
-  for (int j = 0; j < AAC_MAX_ELL; ++j)
-    if (j < ell) w[j] = D.g[j] * r[(long long)j * N + p];
-  // k = 0 and k = ell/2 (real)
+  FOR_PL(pl) w[pl] *= D.g[pl];
   double s0 = 0.0, sh = 0.0;
-#pragma unroll
-  for (int j = 0; j < AAC_MAX_ELL; ++j)
-    if (j < ell) {
-      s0 += w[j];
-      sh += (j & 1) ? -w[j] : w[j];
-    }
+  FOR_PL(pl) {
+    s0 += w[pl];
+    sh += (pl & 1) ? -w[pl] : w[pl];
+  }
   what[p] = D.scale * s0;
   what[(long long)(ell - 1) * N + p] = D.scale * sh;
   for (int k = 1; k < h; ++k) {
     double re = 0.0, im = 0.0;
     int m = 0;
-#pragma unroll
-    for (int j = 0; j < AAC_MAX_ELL; ++j)
-      if (j < ell) {
-        re = fma(w[j], D.c[m], re);
-        im = fma(-w[j], D.s[m], im);
-        m += k;
-        if (m >= ell) m -= ell;
-      }
+    FOR_PL(pl) {
+      re = fma(w[pl], D.c[m], re);
+      im = fma(-w[pl], D.s[m], im);
+      m += k;
+      if (m >= ell) m -= ell;
+    }
     what[(long long)(2 * k - 1) * N + p] = D.scale * re;
     what[(long long)(2 * k) * N + p] = D.scale * im;
   }
 }
 
-// One Chebyshev step for every ACTIVE packed block at this global sweep.
-struct NcBlk {
-  int kind;                  // 0 inactive, 1 real (1 plane), 2 complex (2 planes)
-  int q;                     // first plane of the block
-  int first;                 // local step s == 1: x_1 = w/theta (virtual), x_0 = 0
-  const double* xs;          // x_s, plane q (ignored when first)
-  const double* xm;          // x_{s-1}, plane q (NULL when s <= 2: x_1 = w/theta is virtual)
-  double* xo;                // x_{s+1}, plane q
-  double ar, ai, br, bi;     // a_s = rho_s rho_{s-1}, b_s = 2 rho_s / delta (complex)
-  double lr, li;             // Lambda_k
-  double tr, ti;             // 1/theta_k
-};
-struct NcSweep {
-  NcBlk b[AAC_MAX_BLK];
-  int nblk;
-};
-
-template <int DIM>
-__global__ void __launch_bounds__(256) k_sweep(Geo g, NcSweep P, const double* __restrict__ what,
-                                               const double* __restrict__ hlo,
-                                               const double* __restrict__ hhi) {
+// Standalone forward transform: hat w = U^* Gamma r.
+template <int ELLC>
+__global__ void __launch_bounds__(256) k_forward(long long N, Dft D, const double* __restrict__ r,
+                                                 double* __restrict__ what) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= g.N) return;
-  Pt<DIM> q;
-  load_pt<DIM>(g, p, q);
-  const long long N = g.N;
-  for (int kb = 0; kb < P.nblk; ++kb) {
-    const NcBlk& B = P.b[kb];
-    if (B.kind == 0) continue;
-    const double* wr = what + (long long)B.q * N;
-    const double* hl = hlo + B.q * g.S;
-    const double* hh = hhi + B.q * g.S;
-    if (B.kind == 1) {
-      double xs, Axs, xm;
-      if (B.first) {
-        xs = wr[p] * B.tr;
-        Axs = apply_A<DIM>(g, q, wr, hl, hh) * B.tr;
-        xm = 0.0;
-      } else {
-        xs = B.xs[p];
-        Axs = apply_A<DIM>(g, q, B.xs, hl, hh);
-        xm = B.xm ? B.xm[p] : wr[p] * B.tr;
+  if (p >= N) return;
+  const int ell = D.ell;
+  double w[ELLC];
+  FOR_PL(pl) w[pl] = __ldg(r + (long long)pl * N + p);
+  dft_store<ELLC>(D, N, p, w, what);
+}
+
+constexpr int FT = 256;        // tile points per CTA (one per thread)
+constexpr int FS = 3;          // bulk-copy pipeline stages
+
+// GMRES mode: form u from W and V_0..V_{j-1} (streamed through a TMA bulk-copy ring), store
+// V_j, reduce ||u||^2 (last CTA: Arnoldi norm step), and transform u.
+template <int ELLC, bool TMA>
+__global__ void __launch_bounds__(FT) k_fwd_upd(long long N, Dft D, double* __restrict__ what,
+                                                FwdUpd U) {
+  extern __shared__ __align__(16) double sm[];      // [FS][ELLC][FT]
+  __shared__ __align__(8) uint64_t bar[FS];
+  __shared__ double red[FT / 32];
+  __shared__ bool last;
+  IterState* st = U.ac.st;
+  if (st->done) return;
+  const int j = st->j;
+  const int ell = D.ell;
+  const int t = threadIdx.x;
+  const long long base = (long long)blockIdx.x * FT;
+  const int len = (int)((N - base) < FT ? (N - base) : FT);
+  const int lb = len & ~1;
+  const bool valid = t < len;
+  const long long L = U.L;
+  const int nitems = j == 0 ? 1 : j + 1;   // item 0: W (or V_0 when j == 0); item k: V_{k-1}
+  auto src_of = [&](int k) -> const double* {
+    return k == 0 ? (j == 0 ? U.V : U.W) : U.V + (long long)(k - 1) * L;
+  };
+  if constexpr (TMA) {
+    if (t == 0) {
+      for (int s = 0; s < FS; ++s) mbar_init(&bar[s], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (t == 0)
+      for (int k = 0; k < nitems && k < FS; ++k)
+        bulk_planes(sm + (long long)k * ELLC * FT, FT, src_of(k) + base, N, ell, len, &bar[k]);
+  }
+  double w[ELLC];
+  FOR_PL(pl) w[pl] = 0.0;
+  for (int k = 0; k < nitems; ++k) {
+    const int s = k % FS;
+    const double coef = k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1];
+    const double* src = src_of(k) + base;
+    if constexpr (TMA) mbar_wait(&bar[s], (uint32_t)((k / FS) & 1));
+    if (valid) {
+      FOR_PL(pl) {
+        const double v = (TMA && t < lb) ? sm[((long long)s * ELLC + pl) * FT + t] : src[(long long)pl * N + t];
+        w[pl] = fma(coef, v, w[pl]);
       }
-      const double res = wr[p] - (Axs - B.lr * xs);
-      B.xo[p] = xs + B.ar * (xs - xm) + B.br * res;
-    } else {
-      const double* wi = wr + N;
-      double ur, ui, Aur, Aui, mr, mi;
-      if (B.first) {
-        const double w0 = wr[p], w1 = wi[p];
-        const double Aw0 = apply_A<DIM>(g, q, wr, hl, hh);
-        const double Aw1 = apply_A<DIM>(g, q, wi, hl + g.S, hh + g.S);
-        ur = w0 * B.tr - w1 * B.ti;
-        ui = w0 * B.ti + w1 * B.tr;
-        Aur = Aw0 * B.tr - Aw1 * B.ti;
-        Aui = Aw0 * B.ti + Aw1 * B.tr;
-        mr = mi = 0.0;
-      } else {
-        ur = B.xs[p];
-        ui = B.xs[N + p];
-        Aur = apply_A<DIM>(g, q, B.xs, hl, hh);
-        Aui = apply_A<DIM>(g, q, B.xs + N, hl + g.S, hh + g.S);
-        if (B.xm) {
-          mr = B.xm[p];
-          mi = B.xm[N + p];
-        } else {                               // x_1 = w / theta
-          const double w0 = wr[p], w1 = wi[p];
-          mr = w0 * B.tr - w1 * B.ti;
-          mi = w0 * B.ti + w1 * B.tr;
-        }
-      }
-      // residual w - (A - Lambda) x
-      const double rr = wr[p] - (Aur - (B.lr * ur - B.li * ui));
-      const double ri = wi[p] - (Aui - (B.lr * ui + B.li * ur));
-      const double dr = ur - mr, di = ui - mi;
-      B.xo[p] = ur + (B.ar * dr - B.ai * di) + (B.br * rr - B.bi * ri);
-      B.xo[N + p] = ui + (B.ar * di + B.ai * dr) + (B.br * ri + B.bi * rr);
+    }
+    if constexpr (TMA) {
+      __syncthreads();                              // stage s fully consumed
+      if (t == 0 && k + FS < nitems)
+        bulk_planes(sm + (long long)s * ELLC * FT, FT, src_of(k + FS) + base, N, ell, len, &bar[s]);
+    }
+  }
+  double nrm = 0.0;
+  if (valid) {
+    const long long p = base + t;
+    if (j > 0) {
+      double* vj = U.V + (long long)j * L;
+      FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
+    }
+    FOR_PL(pl) nrm = fma(w[pl], w[pl], nrm);
+    dft_store<ELLC>(D, N, p, w, what);
+  }
+  // ||u||^2: CTA partial, then the last CTA reduces in a fixed order and finalises Arnoldi
+  // column j-1 (or beta when j == 0).
+  nrm = warp_sum(nrm);
+  if ((t & 31) == 0) red[t >> 5] = nrm;
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+    for (int w2 = 0; w2 < FT / 32; ++w2) tot += red[w2];
+    U.part[blockIdx.x] = tot;
+    __threadfence();
+    const unsigned tk = atomicAdd(&st->tick, 1u);
+    last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    const double tot = block_sum_fixed(U.part, gridDim.x);
+    if (t == 0) {
+      st->tick = 0;
+      if (U.ac.local_only) U.ac.red[0] = tot;
+      else arnoldi_norm_step(U.ac, j, tot);
     }
   }
 }
 
-// Final iterates y_k -> z = Gamma^{-1} U y (real by construction of the packing).
-struct NcFinal {
-  const double* y[AAC_MAX_BLK];   // x_{p_k} (plane q of the block) or NULL when p_k == 1
-  double tr[AAC_MAX_BLK], ti[AAC_MAX_BLK];
+// ------------------------------------------------------------------------------------------
+struct NcBlk {
+  int kb;                    // packed block index (0..ell/2)
+  int cplx;                  // 1: Re/Im plane pair
+  int q;                     // first plane of the block
+  // x_s = scs * (*ps), x_{s-1} = scm * (*pm): the virtual iterates x_1 = w/theta and x_0 = 0
+  // become a pointer to hat w with a complex scale (theta^{-1}, or 0), so every block runs
+  // the same branch-free code path.
+  const double* ps;
+  const double* pm;
+  double* xo;                // x_{s+1}, plane q (unused in the LAST sweep)
+  double sr, si;             // scs
+  double mr, mi;             // scm
+  double ar, ai, br, bi;     // a_s = rho_s rho_{s-1}, b_s = 2 rho_s / delta (complex)
+  double lr, li;             // Lambda_k
+};
+struct NcSweep {
+  NcBlk b[AAC_MAX_BLK];      // the active blocks of this sweep, compacted (threadIdx.y)
+  int nact;
+  // LAST sweep: every packed block, active or passive (p_k == 1: y_k = w_k / theta_k)
+  int passive[AAC_MAX_BLK];
+  double ptr[AAC_MAX_BLK], pti[AAC_MAX_BLK];
   int nblk;
+};
+
+constexpr int SW_TX = 64;                 // point groups per CTA along x
+
+template <int DIM, int VEC, bool LAST>
+__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P, Dft D,
+                                                                 const double* __restrict__ what,
+                                                                 const double* __restrict__ hlo,
+                                                                 const double* __restrict__ hhi,
+                                                                 double* __restrict__ zbase,
+                                                                 long long zjs,
+                                                                 const IterState* st) {
+  if (st && st->done) return;
+  // output: z (standalone) or Z_j = zbase + j * zjs (GMRES mode, j on the device)
+  double* zout = zbase + (st ? (long long)st->j * zjs : 0LL);
+  // LAST: final iterates of all blocks at this CTA's points, then the inverse DFT
+  extern __shared__ double ysh[];         // [ell planes][SW_TX*VEC]
+  const long long N = g.N;
+  const long long p = ((long long)blockIdx.x * SW_TX + threadIdx.x) * VEC;
+  const NcBlk& B = P.b[threadIdx.y];
+  double out_r[VEC], out_i[VEC];
+  if (p < N) {
+    PtV<DIM, VEC> q;
+    load_ptv<DIM, VEC>(g, p, q);
+    const double* wr = what + (long long)B.q * N;
+    const double* hl = hlo + B.q * g.S;
+    const double* hh = hhi + B.q * g.S;
+    if (!B.cplx) {
+      double a[VEC], c[VEC], m[VEC], w0[VEC];
+      apply_Av<DIM, VEC>(g, q, B.ps, hl, hh, a, c);
+      ldc<VEC>(B.pm, p, m);
+      ldv<VEC>(wr, p, w0);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const double xs = B.sr * c[e], Axs = B.sr * a[e], xm = B.mr * m[e];
+        const double res = w0[e] - (Axs - B.lr * xs);
+        out_r[e] = xs + B.ar * (xs - xm) + B.br * res;
+      }
+      if (!LAST) stv<VEC>(B.xo, p, out_r);
+    } else {
+      double a0[VEC], a1[VEC], c0[VEC], c1[VEC], m0[VEC], m1[VEC], w0[VEC], w1[VEC];
+      apply_Av<DIM, VEC>(g, q, B.ps, hl, hh, a0, c0);
+      apply_Av<DIM, VEC>(g, q, B.ps + N, hl + g.S, hh + g.S, a1, c1);
+      ldc<VEC>(B.pm, p, m0);
+      ldc<VEC>(B.pm + N, p, m1);
+      ldv<VEC>(wr, p, w0);
+      ldv<VEC>(wr + N, p, w1);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const double ur = B.sr * c0[e] - B.si * c1[e], ui = B.sr * c1[e] + B.si * c0[e];
+        const double Aur = B.sr * a0[e] - B.si * a1[e], Aui = B.sr * a1[e] + B.si * a0[e];
+        const double mr = B.mr * m0[e] - B.mi * m1[e], mi = B.mr * m1[e] + B.mi * m0[e];
+        // residual w - (A - Lambda) x
+        const double rr = w0[e] - (Aur - (B.lr * ur - B.li * ui));
+        const double ri = w1[e] - (Aui - (B.lr * ui + B.li * ur));
+        const double dr = ur - mr, di = ui - mi;
+        out_r[e] = ur + (B.ar * dr - B.ai * di) + (B.br * rr - B.bi * ri);
+        out_i[e] = ui + (B.ar * di + B.ai * dr) + (B.br * ri + B.bi * rr);
+      }
+      if (!LAST) {
+        stv<VEC>(B.xo, p, out_r);
+        stv<VEC>(B.xo + N, p, out_i);
+      }
+    }
+    if (LAST) {
+      const int tp = threadIdx.x * VEC;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        ysh[B.q * (SW_TX * VEC) + tp + e] = out_r[e];
+        if (B.cplx) ysh[(B.q + 1) * (SW_TX * VEC) + tp + e] = out_i[e];
+      }
+    }
+  }
+  if constexpr (LAST) {
+    __syncthreads();
+    // passive blocks (p_k == 1): y = w / theta straight from hat w
+    const int ell = D.ell, h = ell / 2;
+    const int npts = SW_TX * VEC;
+    const long long p0 = (long long)blockIdx.x * npts;
+    const int nthr = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int kb = 0; kb <= h; ++kb) {
+      if (!P.passive[kb]) continue;
+      const int qq = plane_of(ell, kb);
+      const bool cp = (kb != 0 && kb != h);
+      for (int t = tid; t < npts; t += nthr) {
+        if (p0 + t >= N) continue;
+        const double a = what[(long long)qq * N + p0 + t];
+        const double b = cp ? what[(long long)(qq + 1) * N + p0 + t] : 0.0;
+        ysh[qq * npts + t] = a * P.ptr[kb] - b * P.pti[kb];
+        if (cp) ysh[(qq + 1) * npts + t] = a * P.pti[kb] + b * P.ptr[kb];
+      }
+    }
+    __syncthreads();
+    // z_j = ell^{-1/2} gamma_j^{-1} (y_0 + (-1)^j y_{ell/2} + 2 sum_{k=1}^{ell/2-1} Re(y_k e^{2 pi i jk/ell}))
+    // thread (x, y) -> its VEC points, output planes j = y, y + nact, ...
+    const int tp = threadIdx.x * VEC;
+    if (p0 + tp < N) {
+      for (int jj = threadIdx.y; jj < ell; jj += blockDim.y) {
+        double acc[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+        int m = jj;
+        for (int kb = 1; kb < h; ++kb) {
+          double yr[VEC], yi[VEC];
+          ldc<VEC>(ysh, (2 * kb - 1) * npts + tp, yr);
+          ldc<VEC>(ysh, (2 * kb) * npts + tp, yi);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            acc[e] = fma(yr[e], D.c[m], acc[e]);
+            acc[e] = fma(-yi[e], D.s[m], acc[e]);
+          }
+          m += jj;
+          if (m >= ell) m -= ell;
+        }
+        double y0[VEC], yh[VEC], o[VEC];
+        ldc<VEC>(ysh, tp, y0);
+        ldc<VEC>(ysh, (ell - 1) * npts + tp, yh);
+        const double f = D.scale * D.gi[jj];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) o[e] = f * (y0[e] + ((jj & 1) ? -yh[e] : yh[e]) + 2.0 * acc[e]);
+        stv<VEC>(zout, (long long)jj * N + p0 + tp, o);
+      }
+    }
+  }
+}
+
+// P_max == 1 (every block exact at p = 1, e.g. c = 0, or k = 1): z = Gamma^{-1} U (w / theta).
+struct NcFinal {
+  double tr[AAC_MAX_BLK], ti[AAC_MAX_BLK];
 };
 
 __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
                                                  const double* __restrict__ what,
-                                                 double* __restrict__ z) {
+                                                 double* __restrict__ zbase, long long zjs,
+                                                 const IterState* st) {
+  if (st && st->done) return;
+  double* z = zbase + (st ? (long long)st->j * zjs : 0LL);
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= N) return;
   const int ell = D.ell, h = ell / 2;
   double yr[AAC_MAX_BLK], yi[AAC_MAX_BLK];
-  for (int kb = 0; kb <= h; ++kb) {
-    const int q = (kb == 0) ? 0 : (kb == h ? ell - 1 : 2 * kb - 1);
+#pragma unroll
+  for (int kb = 0; kb < AAC_MAX_BLK; ++kb) {
+    if (kb > h) break;
+    const int q = plane_of(ell, kb);
     const bool cplx = (kb != 0 && kb != h);
-    if (F.y[kb]) {
-      yr[kb] = F.y[kb][p];
-      yi[kb] = cplx ? F.y[kb][N + p] : 0.0;
-    } else {
-      const double w0 = what[(long long)q * N + p];
-      const double w1 = cplx ? what[(long long)(q + 1) * N + p] : 0.0;
-      yr[kb] = w0 * F.tr[kb] - w1 * F.ti[kb];
-      yi[kb] = cplx ? (w0 * F.ti[kb] + w1 * F.tr[kb]) : 0.0;
-    }
+    const double w0 = what[(long long)q * N + p];
+    const double w1 = cplx ? what[(long long)(q + 1) * N + p] : 0.0;
+    yr[kb] = w0 * F.tr[kb] - w1 * F.ti[kb];
+    yi[kb] = cplx ? (w0 * F.ti[kb] + w1 * F.tr[kb]) : 0.0;
   }
   for (int j = 0; j < ell; ++j) {
     double acc = 0.0;
-    int m = j;                                    // m = j*k mod ell
-    for (int kb = 1; kb < h; ++kb) {
+    int m = j;
+#pragma unroll
+    for (int kb = 1; kb < AAC_MAX_BLK; ++kb) {
+      if (kb >= h) break;
       acc = fma(yr[kb], D.c[m], acc);
       acc = fma(-yi[kb], D.s[m], acc);
       m += j;

@@ -5,90 +5,190 @@
 // w_f = 0, so a boundary neighbour is replaced by u_P itself (contribution exactly 0, no
 // out-of-range load). Across the slab axis the neighbour comes from the halo layer of the
 // adjacent rank.
+//
+// Every thread owns VEC consecutive points along x (VEC = 2 when nx is even: 16-byte
+// loads of the centre / north / south values and of the face weights).
 #pragma once
 
 #include "aac_internal.cuh"
 
-template <int DIM>
-struct Pt {
-  long long p;
-  int x, y, z;
-  long long li;                      // index inside the slab layer (for halo reads)
-  double wxm, wxp, wym, wyp, wzm, wzp;
-};
-
-template <int DIM>
-__device__ __forceinline__ void load_pt(const Geo& g, long long p, Pt<DIM>& q) {
-  q.p = p;
-  q.x = (int)(p % g.nx);
-  long long r = p / g.nx;
-  q.y = (int)(r % g.ny);
-  q.z = (int)(r / g.ny);
-  q.li = p % g.S;
-  q.wxm = __ldg(g.wx + p);
-  q.wxp = __ldg(g.wx + p + 1);
-  if (DIM >= 2) {
-    q.wym = __ldg(g.wy + p);
-    q.wyp = __ldg(g.wy + p + g.nx);
+template <int VEC>
+__device__ __forceinline__ void ldv(const double* __restrict__ u, long long p, double* out) {
+  if constexpr (VEC == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(u + p));
+    out[0] = t.x;
+    out[1] = t.y;
   } else {
-    q.wym = q.wyp = 0.0;
-  }
-  if (DIM >= 3) {
-    q.wzm = __ldg(g.wz + p);
-    q.wzp = __ldg(g.wz + p + g.S);
-  } else {
-    q.wzm = q.wzp = 0.0;
+    out[0] = __ldg(u + p);
   }
 }
 
-// (A u)_p for one plane u (base pointer of the plane); hlo / hhi = this plane's halo layers.
-template <int DIM>
-__device__ __forceinline__ double apply_A(const Geo& g, const Pt<DIM>& q,
-                                          const double* __restrict__ u,
-                                          const double* __restrict__ hlo,
-                                          const double* __restrict__ hhi) {
-  const double u0 = u[q.p];
-  const double xm = (q.x > 0) ? u[q.p - 1] : u0;
-  const double xp = (q.x < g.nx - 1) ? u[q.p + 1] : u0;
-  double acc = u0;
-  acc = fma(q.wxm, u0 - xm, acc);
-  acc = fma(q.wxp, u0 - xp, acc);
-  if (DIM == 2) {                    // y is the slab axis
-    const double ym = (q.y > 0) ? u[q.p - g.nx] : (g.has_lo ? hlo[q.li] : u0);
-    const double yp = (q.y < g.ny - 1) ? u[q.p + g.nx] : (g.has_hi ? hhi[q.li] : u0);
-    acc = fma(q.wym, u0 - ym, acc);
-    acc = fma(q.wyp, u0 - yp, acc);
+// Plain (coherent) load: for buffers written earlier in the same kernel sequence.
+template <int VEC>
+__device__ __forceinline__ void ldc(const double* u, long long p, double* out) {
+  if constexpr (VEC == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(u + p);
+    out[0] = t.x;
+    out[1] = t.y;
+  } else {
+    out[0] = u[p];
   }
-  if (DIM == 3) {                    // z is the slab axis
-    const double ym = (q.y > 0) ? u[q.p - g.nx] : u0;
-    const double yp = (q.y < g.ny - 1) ? u[q.p + g.nx] : u0;
-    const double zm = (q.z > 0) ? u[q.p - g.S] : (g.has_lo ? hlo[q.li] : u0);
-    const double zp = (q.z < g.nz - 1) ? u[q.p + g.S] : (g.has_hi ? hhi[q.li] : u0);
-    acc = fma(q.wym, u0 - ym, acc);
-    acc = fma(q.wyp, u0 - yp, acc);
-    acc = fma(q.wzm, u0 - zm, acc);
-    acc = fma(q.wzp, u0 - zp, acc);
+}
+
+template <int VEC>
+__device__ __forceinline__ void stv(double* u, long long p, const double* v) {
+  if constexpr (VEC == 2) {
+    *reinterpret_cast<double2*>(u + p) = make_double2(v[0], v[1]);
+  } else {
+    u[p] = v[0];
   }
-  return acc;
+}
+
+// Geometry + face weights of the VEC points p .. p+VEC-1 (same row).
+template <int DIM, int VEC>
+struct PtV {
+  long long p, li;
+  int x, y, z;
+  double wx[VEC + 1];             // lower x-faces of the VEC points, then the last upper face
+  double wym[VEC], wyp[VEC], wzm[VEC], wzp[VEC];
+};
+
+template <int DIM, int VEC>
+__device__ __forceinline__ void load_ptv(const Geo& g, long long p, PtV<DIM, VEC>& q) {
+  q.p = p;
+  q.x = (int)(p % g.nx);
+  const long long r = p / g.nx;
+  q.y = (int)(r % g.ny);
+  q.z = (int)(r / g.ny);
+  q.li = p % g.S;
+  ldv<VEC>(g.wx, p, q.wx);
+  q.wx[VEC] = __ldg(g.wx + p + VEC);
+  if constexpr (DIM >= 2) {
+    ldv<VEC>(g.wy, p, q.wym);
+    ldv<VEC>(g.wy, p + g.nx, q.wyp);
+  }
+  if constexpr (DIM >= 3) {
+    ldv<VEC>(g.wz, p, q.wzm);
+    ldv<VEC>(g.wz, p + g.S, q.wzp);
+  }
+}
+
+// Neighbour pointers of the VEC-point group for one plane (branch-free: boundary neighbours
+// alias the centre, slab neighbours point into the halo layer). All loads of a stencil are
+// then independent and issue back to back.
+struct Nbr {
+  const double* c;   // centre (VEC values)
+  const double* w;   // west of the first point
+  const double* e;   // east of the last point
+  const double* n;   // y - 1   (VEC values)
+  const double* s;   // y + 1
+  const double* d;   // z - 1
+  const double* u;   // z + 1
+};
+
+template <int DIM, int VEC>
+__device__ __forceinline__ Nbr nbr(const Geo& g, const PtV<DIM, VEC>& q, const double* u,
+                                   const double* hlo, const double* hhi) {
+  Nbr b;
+  b.c = u + q.p;
+  b.w = (q.x > 0) ? b.c - 1 : b.c;
+  b.e = (q.x + VEC < g.nx) ? b.c + VEC : b.c + (VEC - 1);
+  b.n = b.s = b.d = b.u = b.c;
+  if constexpr (DIM == 2) {
+    b.n = (q.y > 0) ? b.c - g.nx : (g.has_lo ? hlo + q.li : b.c);
+    b.s = (q.y < g.ny - 1) ? b.c + g.nx : (g.has_hi ? hhi + q.li : b.c);
+  }
+  if constexpr (DIM == 3) {
+    b.n = (q.y > 0) ? b.c - g.nx : b.c;
+    b.s = (q.y < g.ny - 1) ? b.c + g.nx : b.c;
+    b.d = (q.z > 0) ? b.c - g.S : (g.has_lo ? hlo + q.li : b.c);
+    b.u = (q.z < g.nz - 1) ? b.c + g.S : (g.has_hi ? hhi + q.li : b.c);
+  }
+  return b;
+}
+
+// Stencil operands of one plane at the VEC-point group (loads only: lets a kernel issue the
+// loads of several planes before any arithmetic or store).
+template <int VEC>
+struct SV {
+  double c[VEC], n[VEC], s[VEC], d[VEC], u[VEC];
+  double w, e;
+};
+
+template <int DIM, int VEC>
+__device__ __forceinline__ void load_sv(const Geo& g, const PtV<DIM, VEC>& q, const double* u,
+                                        const double* hlo, const double* hhi, SV<VEC>& v) {
+  const Nbr b = nbr<DIM, VEC>(g, q, u, hlo, hhi);
+  ldc<VEC>(b.c, 0, v.c);
+  v.w = *b.w;
+  v.e = *b.e;
+  if constexpr (DIM >= 2) {
+    ldc<VEC>(b.n, 0, v.n);
+    ldc<VEC>(b.s, 0, v.s);
+  }
+  if constexpr (DIM >= 3) {
+    ldc<VEC>(b.d, 0, v.d);
+    ldc<VEC>(b.u, 0, v.u);
+  }
+}
+
+// out[e] = (A u)_{p+e} from loaded operands
+template <int DIM, int VEC>
+__device__ __forceinline__ void stencil_sv(const PtV<DIM, VEC>& q, const SV<VEC>& v, double* out) {
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    const double l = e == 0 ? v.w : v.c[e - 1];
+    const double r = e == VEC - 1 ? v.e : v.c[e + 1];
+    const double c = v.c[e];
+    double acc = c;
+    acc = fma(q.wx[e], c - l, acc);
+    acc = fma(q.wx[e + 1], c - r, acc);
+    if constexpr (DIM >= 2) {
+      acc = fma(q.wym[e], c - v.n[e], acc);
+      acc = fma(q.wyp[e], c - v.s[e], acc);
+    }
+    if constexpr (DIM >= 3) {
+      acc = fma(q.wzm[e], c - v.d[e], acc);
+      acc = fma(q.wzp[e], c - v.u[e], acc);
+    }
+    out[e] = acc;
+  }
+}
+
+// out[e] = (A u)_{p+e}, centre[e] = u_{p+e}, e < VEC.
+template <int DIM, int VEC>
+__device__ __forceinline__ void apply_Av(const Geo& g, const PtV<DIM, VEC>& q, const double* u,
+                                         const double* hlo, const double* hhi, double* out,
+                                         double* centre) {
+  SV<VEC> v;
+  load_sv<DIM, VEC>(g, q, u, hlo, hhi, v);
+  stencil_sv<DIM, VEC>(q, v, out);
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) centre[e] = v.c[e];
 }
 
 // ------------------------------------------------------------------------------------------
 // y = calA x over all ell planes: y_0 = A x_0, y_j = A x_j - x_{j-1}.
-// One thread per spatial point; the face weights are loaded once and reused for all planes.
-template <int DIM>
+template <int DIM, int VEC>
 __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __restrict__ x,
                                                 double* __restrict__ y,
                                                 const double* __restrict__ hlo,
                                                 const double* __restrict__ hhi) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (p >= g.N) return;
-  Pt<DIM> q;
-  load_pt<DIM>(g, p, q);
-  double prev = 0.0;
+  PtV<DIM, VEC> q;
+  load_ptv<DIM, VEC>(g, p, q);
+  double prev[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) prev[e] = 0.0;
   for (int j = 0; j < ell; ++j) {
-    const double* u = x + (long long)j * g.N;
-    const double ax = apply_A<DIM>(g, q, u, hlo + j * g.S, hhi + j * g.S);
-    y[(long long)j * g.N + p] = ax - prev;
-    prev = u[p];
+    double ax[VEC], c[VEC];
+    apply_Av<DIM, VEC>(g, q, x + (long long)j * g.N, hlo + j * g.S, hhi + j * g.S, ax, c);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      ax[e] -= prev[e];
+      prev[e] = c[e];
+    }
+    stv<VEC>(y + (long long)j * g.N, p, ax);
   }
 }
