@@ -14,8 +14,13 @@
 #include "comm.cuh"
 #include "krylov.cuh"
 #include "nc.cuh"
-#include "sp.cuh"
 #include "stencil.cuh"
+
+// saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
+static int sp_prepare(aac_ctx* ctx, int k);
+static int sp_solve(aac_ctx* ctx, int k, double* zbase, long long zjs, const IterState* st);
+static void sp_destroy(aac_ctx* ctx);
+static long long sp_paper_matvecs(const aac_ctx* ctx, int k);
 
 static thread_local std::string g_last_err;
 
@@ -475,6 +480,8 @@ static Dft make_dft(const aac_ctx* ctx) {
   return D;
 }
 
+#include "sp.cuh"
+
 static inline int plane_of_block(int ell, int kb) {
   const int h = ell / 2;
   return kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1);
@@ -635,7 +642,17 @@ extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* 
   if (k < 1) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
   StreamScope ss(ctx);
   if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z, false);
-  if (method == AAC_SP) return sp_apply(ctx, k, r, z);
+  if (method == AAC_SP) {
+    AAC_TRY(sp_prepare(ctx, k));
+    const long long N = ctx->geo.N;
+    const Dft D = make_dft(ctx);
+    const double V = 8.0 * ctx->ell * N;
+    if (ctx->ell <= 10)
+      LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+    else
+      LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+    return sp_solve(ctx, k, z, 0, nullptr);
+  }
   return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
 }
 
@@ -682,7 +699,10 @@ static int arnoldi_impl(aac_ctx* ctx) {
 // forms V_j), then w = calA Z_j with the CGS2 projections and Gram column.
 static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   if (method == AAC_SP) {
-    AAC_TRY(sp_gmres_precond(ctx, k));
+    const double V = 8.0 * ctx->ell * ctx->geo.N;
+    AAC_TRY(launch_fwd_upd(ctx, 3 * V));
+    if (ctx->nranks > 1) return aac_fail(ctx, AAC_EINVAL, "AAC_SP runs on one rank");
+    AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
   } else {
     AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true));
   }
@@ -771,9 +791,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
     }
   }
   // finalise the last column (no-op when already done) and form x = sum y_i Z_i
-  if (method == AAC_SP) {
-    AAC_TRY(sp_gmres_finalize(ctx));
-  } else {
+  {
     // finalise the last Arnoldi column (same kernel; its transform output is unused)
     AAC_TRY(launch_fwd_upd(ctx, 0));
     if (ctx->nranks > 1) {

@@ -1,16 +1,730 @@
-// sp.cuh -- saddle-point inner solver (placeholder until the SP kernels land).
+// sp.cuh -- saddle-point inner solver P_SP (§4; §5.1, 694-697).
+//
+// Per packed Fourier block (after the same gamma-scale + DFT as NC):
+//   complex block k (1 <= k < ell/2): lambda = conj(Lambda_k) (Im lambda > 0), b = conj(w_k);
+//     MINRES (k_in iterations from 0) on the real saddle system Eq. (eq:saddlesystem)
+//       S [u; v] = [Im lam u + Psi v; Psi u - Im lam v] = [-Im b; Re b] = [Im w_k; Re w_k],
+//       Psi = A - Re lam, preconditioned by P_D = diag(M, M) (Eq. eq:minresprecond),
+//       M ~ (A + (Im lam - Re lam) I)^{-1} = one V-cycle;  y_k = conj(u - i v) = u + i v.
+//   real blocks k = 0, ell/2: PCG (k_in iterations) on (A - Lambda_k) y = w_k, M = one V-cycle
+//     of A - Lambda_k.
+// then the inverse DFT + gamma^{-1}. Reading R16: V(1,1) cycle, damped Jacobi
+// omega = 0.8, aggregation by 2 per axis with Galerkin coarse operators (a coarse face weight is
+// the sum of the fine faces between the two aggregates; the identity becomes the child count),
+// dense solve once every axis <= 8. The oracle (oracle/saddle.py) follows the same algorithm
+// with scipy sparse products; it shares no code with this file.
+//
+// All blocks advance in lock step; every kernel is batched over the ell packed planes
+// (blockIdx.y = plane or block); the Krylov scalars live on the device and are updated by the
+// last CTA of the kernel that produces the dot products (fixed-order sums).
 #pragma once
-#include "aac_internal.cuh"
 
-static int sp_apply(aac_ctx* ctx, int k, const double* r, double* z) {
-  (void)k; (void)r; (void)z;
-  return aac_fail(ctx, AAC_EINVAL, "AAC_SP inner solver not built yet");
+#include <algorithm>
+#include <vector>
+
+#include "krylov.cuh"
+#include "nc.cuh"
+#include "stencil.cuh"
+
+constexpr double SP_OMEGA = 0.8;
+constexpr int SP_COARSE_MAX_AXIS = 8;
+constexpr int SP_T = 256;
+
+struct SpBlk {                 // device scalars of one packed block
+  // MINRES (Elman-Silvester-Wathen form, as oracle/saddle.py::minres)
+  double gamma, gamma_prev, eta, s_prev, s_cur, c_prev, c_cur, delta;
+  double a1, a2, a3, xcoef, dcoef, vcoef;
+  // PCG (as oracle/saddle.py::pcg)
+  double rho, alpha, beta;
+  int stop;                    // 1: the oracle's loop has broken out; 2: break after this update
+  int pad;
+};
+
+struct SpConst {               // per-block constants, passed by value
+  double lre[AAC_MAX_BLK], lim[AAC_MAX_BLK];   // lambda (complex blocks: conj Lambda_k)
+  double s[AAC_MAX_ELL];                        // MG shift per plane: A + s I
+  int ell;
+};
+
+struct SpLevel {               // one multigrid level (device arrays)
+  Geo g;                       // extents + face weights (lower-face convention), no halos
+  double* cnt;                 // Galerkin image of I: fine cells per aggregate
+  double* b;                   // [ell][N] right-hand sides (levels >= 1)
+  double* x;                   // [ell][N] pre-smoothed iterate
+  double* x2;                  // [ell][N] post-smoothed iterate (the level's result, levels >= 1)
+};
+
+struct SpPlan {
+  int ell = 0, h = 0;
+  std::vector<SpLevel> lev;
+  std::vector<void*> owned;    // device allocations
+  double* minv = nullptr;      // [h+1][nc][nc] dense inverses of the coarsest operator
+  int nc = 0;
+  SpConst K;
+  double* X = nullptr;
+  double* Vb[3] = {nullptr, nullptr, nullptr};
+  double* Zb[2] = {nullptr, nullptr};
+  double* Wb[3] = {nullptr, nullptr, nullptr};
+  double *SZ = nullptr, *R = nullptr, *P = nullptr, *Zr = nullptr;
+  SpBlk* blk = nullptr;        // [h+1]
+  double* part = nullptr;      // partials [planes or blocks][tiles]
+  unsigned* tick = nullptr;
+};
+
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ int sp_block_of(int ell, int pl) {
+  const int h = ell / 2;
+  return pl == 0 ? 0 : (pl == ell - 1 ? h : (pl + 1) / 2);
 }
+
+// A_l(s) u at the point: m u_p + sum_f w_f (u_p - u_nb), m = (1 + s) cnt_p
+template <int DIM>
+__device__ __forceinline__ double mg_apply(const Geo& g, const PtV<DIM, 1>& q, const double* u, double m) {
+  double a[1], c[1];
+  apply_Av<DIM, 1>(g, q, u, nullptr, nullptr, a, c);
+  return a[0] + (m - 1.0) * c[0];
+}
+
+template <int DIM>
+__device__ __forceinline__ double diag_of(const PtV<DIM, 1>& q, double m) {
+  double d = m + q.wx[0] + q.wx[1];
+  if constexpr (DIM >= 2) d += q.wym[0] + q.wyp[0];
+  if constexpr (DIM >= 3) d += q.wzm[0] + q.wzp[0];
+  return d;
+}
+
+struct MgIo {                  // per-plane fine-level pointers
+  const double* in[AAC_MAX_ELL];
+  double* out[AAC_MAX_ELL];
+};
+
+struct SpStepCtx {
+  SpBlk* blk;
+  double* part;
+  unsigned* tick;
+  SpConst K;
+  int phase;                   // step B: 0 = initial (gamma / rho), 1 = iteration
+  const IterState* st;
+};
+
+// ---- scalar steps (thread 0 of the last CTA) ---------------------------------------------
+// A: after K1. tot[kb] = <S z, z> (complex) or <p, A' p> (real).
+__device__ void sp_scalar_A(const SpStepCtx& S, const double* tot) {
+  const int h = S.K.ell / 2;
+  for (int kb = 0; kb <= h; ++kb) {
+    SpBlk& b = S.blk[kb];
+    if (b.stop == 2) b.stop = 1;
+    if (kb == 0 || kb == h) {
+      if (!b.stop) b.alpha = b.rho / tot[kb];
+    } else {
+      b.delta = tot[kb];
+      b.dcoef = b.delta / b.gamma;
+      b.vcoef = b.gamma / b.gamma_prev;
+    }
+  }
+}
+
+// B: after the V-cycle. tot[plane] = <M v, v> per plane (complex blocks: two planes).
+__device__ void sp_scalar_B(const SpStepCtx& S, const double* tot) {
+  const int ell = S.K.ell, h = ell / 2;
+  for (int kb = 0; kb <= h; ++kb) {
+    SpBlk& b = S.blk[kb];
+    if (kb == 0 || kb == h) {
+      const double rho_new = tot[kb == 0 ? 0 : ell - 1];
+      if (S.phase == 0) {
+        b.rho = rho_new;
+        b.stop = (rho_new == 0.0) ? 1 : 0;
+      } else if (!b.stop) {
+        b.beta = rho_new / b.rho;
+        b.rho = rho_new;
+        if (rho_new == 0.0) b.stop = 1;
+      }
+      continue;
+    }
+    const double d = tot[2 * kb - 1] + tot[2 * kb];
+    const double gn = sqrt(d > 0.0 ? d : 0.0);
+    if (S.phase == 0) {
+      b.gamma = gn;
+      b.gamma_prev = 1.0;
+      b.eta = gn;
+      b.s_prev = b.s_cur = 0.0;
+      b.c_prev = b.c_cur = 1.0;
+      b.stop = (gn == 0.0) ? 1 : 0;
+      continue;
+    }
+    if (b.stop) continue;
+    const double a0 = b.c_cur * b.delta - b.c_prev * b.s_cur * b.gamma;
+    const double a1 = sqrt(a0 * a0 + gn * gn);
+    const double a2 = b.s_cur * b.delta + b.c_prev * b.c_cur * b.gamma;
+    const double a3 = b.s_prev * b.gamma;
+    const double c_next = a0 / a1, s_next = gn / a1;
+    b.a1 = a1;
+    b.a2 = a2;
+    b.a3 = a3;
+    b.xcoef = c_next * b.eta;
+    b.eta = -s_next * b.eta;
+    b.gamma_prev = b.gamma;            // K6 scales z by 1/gamma_prev (= the old gamma)
+    b.gamma = gn;
+    b.s_prev = b.s_cur;
+    b.s_cur = s_next;
+    b.c_prev = b.c_cur;
+    b.c_cur = c_next;
+    if (gn == 0.0) b.stop = 2;
+  }
+}
+
+// Per-(plane or block, CTA) partials; the last CTA sums in a fixed order and runs a step.
+__device__ __forceinline__ void sp_reduce(const SpStepCtx& S, double v, bool stepB) {
+  __shared__ double red[SP_T / 32];
+  __shared__ bool last;
+  __shared__ double tot[AAC_MAX_ELL];
+  v = warp_sum(v);
+  const int t = threadIdx.x;
+  if ((t & 31) == 0) red[t >> 5] = v;
+  __syncthreads();
+  const int ntile = gridDim.x;
+  if (t == 0) {
+    double s = 0.0;
+    for (int w = 0; w < SP_T / 32; ++w) s += red[w];
+    S.part[(long long)blockIdx.y * ntile + blockIdx.x] = s;
+    __threadfence();
+    const unsigned tk = atomicAdd(S.tick, 1u);
+    last = (tk == gridDim.x * gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int q = 0; q < (int)gridDim.y; ++q) {
+    const double s = block_sum_fixed(S.part + (long long)q * ntile, ntile);
+    if (t == 0) tot[q] = s;
+  }
+  if (t == 0) {
+    *S.tick = 0;
+    if (stepB) sp_scalar_B(S, tot);
+    else sp_scalar_A(S, tot);
+  }
+}
+
+// ---- multigrid kernels (grid: tiles x planes) ----------------------------------------------
+// x = omega b / D (pre-smoothing from zero)
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_smooth0(Geo g, const double* __restrict__ cnt, SpConst K,
+                                                     MgIo io, const double* bl, double* xl,
+                                                     const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y;
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (p >= g.N) return;
+  PtV<DIM, 1> q;
+  load_ptv<DIM, 1>(g, p, q);
+  const double m = (1.0 + K.s[pl]) * cnt[p];
+  const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
+  xl[(long long)pl * g.N + p] = SP_OMEGA * b[p] / diag_of<DIM>(q, m);
+}
+
+// b_{l+1} = P^T (b - A_l x): one thread per COARSE point sums its children
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_restrict(Geo g, const double* __restrict__ cnt, Geo gc,
+                                                      SpConst K, MgIo io, const double* bl,
+                                                      const double* xl, double* bc,
+                                                      const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y;
+  const long long pc = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (pc >= gc.N) return;
+  const int X = (int)(pc % gc.nx);
+  const long long rr = pc / gc.nx;
+  const int Y = (int)(rr % gc.ny), Z = (int)(rr / gc.ny);
+  const double s = K.s[pl];
+  const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
+  const double* x = xl + (long long)pl * g.N;
+  double acc = 0.0;
+  for (int dz = 0; dz < (DIM >= 3 ? 2 : 1); ++dz)
+    for (int dy = 0; dy < (DIM >= 2 ? 2 : 1); ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int fx = 2 * X + dx, fy = DIM >= 2 ? 2 * Y + dy : 0, fz = DIM >= 3 ? 2 * Z + dz : 0;
+        if (fx >= g.nx || fy >= g.ny || fz >= g.nz) continue;
+        const long long p = ((long long)fz * g.ny + fy) * g.nx + fx;
+        PtV<DIM, 1> q;
+        load_ptv<DIM, 1>(g, p, q);
+        acc += b[p] - mg_apply<DIM>(g, q, x, (1.0 + s) * cnt[p]);
+      }
+  bc[(long long)pl * gc.N + pc] = acc;
+}
+
+// x_c = A_c(s)^{-1} b_c with the precomputed dense inverse of the plane's block (CTA per plane)
+__global__ void __launch_bounds__(SP_T) k_mg_coarse(int nc, const double* __restrict__ minv, int ell,
+                                                    const double* bc, double* xc, const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.x;
+  const double* M = minv + (long long)sp_block_of(ell, pl) * nc * nc;
+  const double* b = bc + (long long)pl * nc;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nc; ++k) s = fma(M[(long long)i * nc + k], b[k], s);
+    xc[(long long)pl * nc + i] = s;
+  }
+}
+
+// x_l += P x_c (injection from the aggregate)
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_prolong(Geo g, Geo gc, double* xl, const double* xc,
+                                                     const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y;
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (p >= g.N) return;
+  const int x = (int)(p % g.nx);
+  const long long r = p / g.nx;
+  const int y = (int)(r % g.ny), z = (int)(r / g.ny);
+  const long long pc = ((long long)(z / 2) * gc.ny + y / 2) * gc.nx + x / 2;
+  xl[(long long)pl * g.N + p] += xc[(long long)pl * gc.N + pc];
+}
+
+// x2 = x + omega (b - A x)/D. Level 0: written to io.out[pl], dot partial <x2, b> per plane,
+// last CTA: scalar step B.
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restrict__ cnt, MgIo io,
+                                                  const double* bl, const double* xl, double* x2l,
+                                                  SpStepCtx S, int level0) {
+  if (S.st && S.st->done) return;
+  const int pl = blockIdx.y;
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  double dotp = 0.0;
+  if (p < g.N) {
+    PtV<DIM, 1> q;
+    load_ptv<DIM, 1>(g, p, q);
+    const double m = (1.0 + S.K.s[pl]) * cnt[p];
+    const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
+    const double* x = xl + (long long)pl * g.N;
+    const double xn = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m)) / diag_of<DIM>(q, m);
+    if (level0) {
+      io.out[pl][p] = xn;
+      dotp = xn * b[p];
+    } else {
+      x2l[(long long)pl * g.N + p] = xn;
+    }
+  }
+  if (level0) sp_reduce(S, dotp, true);
+}
+
+// ---- Krylov kernels -------------------------------------------------------------------------
+struct SpVec {
+  double* X;
+  double *Vp, *Vc, *Vn, *Zc, *Wp, *Wc, *Wn, *SZ;
+  double *R, *P, *Zr;
+  const double* what;
+};
+
+// complex planes: Vc = [Im w; Re w] (u-plane <- Im w, v-plane <- Re w), Vp = Wp = Wc = X = 0;
+// real planes: R = w, X = 0.
+__global__ void __launch_bounds__(SP_T) k_sp_init(long long N, int ell, SpVec v, const IterState* st) {
+  if (st && st->done) return;
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (p >= N) return;
+  const int h = ell / 2;
+  for (int pl = 0; pl < ell; ++pl) {
+    const long long o = (long long)pl * N + p;
+    v.X[o] = 0.0;
+    const int kb = sp_block_of(ell, pl);
+    if (kb == 0 || kb == h) {
+      v.R[o] = v.what[o];
+    } else {
+      v.Vc[o] = (pl & 1) ? v.what[o + N] : v.what[o - N];   // 2k-1 is the u (Re) plane
+      v.Vp[o] = 0.0;
+      v.Wp[o] = 0.0;
+      v.Wc[o] = 0.0;
+    }
+  }
+}
+
+// K1 (grid: tiles x blocks): complex: SZ = S (z / gamma), partial <S z, z> / gamma^2-scaled;
+// real: Q = SZ = (A - Lambda) P, partial <P, Q>. Last CTA: scalar step A.
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) {
+  if (S.st && S.st->done) return;
+  const int kb = blockIdx.y, ell = S.K.ell, h = ell / 2;
+  const long long N = g.N;
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  const SpBlk& b = S.blk[kb];
+  double dotp = 0.0;
+  if (p < N && !b.stop) {
+    PtV<DIM, 1> q;
+    load_ptv<DIM, 1>(g, p, q);
+    if (kb == 0 || kb == h) {
+      const int pl = kb == 0 ? 0 : ell - 1;
+      const double* pp = v.P + (long long)pl * N;
+      const double a = mg_apply<DIM>(g, q, pp, 1.0 + S.K.s[pl]);   // (A - Lambda) p
+      v.SZ[(long long)pl * N + p] = a;
+      dotp = pp[p] * a;
+    } else {
+      const int qu = 2 * kb - 1, qv = qu + 1;
+      const double invg = 1.0 / b.gamma;
+      double azu[1], azv[1], zu[1], zv[1];
+      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qu * N, nullptr, nullptr, azu, zu);
+      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qv * N, nullptr, nullptr, azv, zv);
+      const double us = zu[0] * invg, vs = zv[0] * invg;
+      const double Au = azu[0] * invg, Av = azv[0] * invg;
+      const double lr = S.K.lre[kb], li = S.K.lim[kb];
+      const double Su = li * us + (Av - lr * vs);
+      const double Sv = (Au - lr * us) - li * vs;
+      v.SZ[(long long)qu * N + p] = Su;
+      v.SZ[(long long)qv * N + p] = Sv;
+      dotp = Su * us + Sv * vs;
+    }
+  }
+  sp_reduce(S, dotp, false);
+}
+
+// K3 (grid: tiles x planes): complex: Vn = SZ - (delta/gamma) Vc - (gamma/gamma_prev) Vp;
+// real: X += alpha P, R -= alpha Q.
+__global__ void __launch_bounds__(SP_T) k_sp_upd1(long long N, int ell, SpVec v, const SpBlk* blk,
+                                                  const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y, h = ell / 2, kb = sp_block_of(ell, pl);
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (p >= N) return;
+  const long long o = (long long)pl * N + p;
+  const SpBlk& b = blk[kb];
+  if (b.stop == 1) return;
+  if (kb == 0 || kb == h) {
+    v.X[o] = fma(b.alpha, v.P[o], v.X[o]);
+    v.R[o] = fma(-b.alpha, v.SZ[o], v.R[o]);
+  } else {
+    v.Vn[o] = v.SZ[o] - b.dcoef * v.Vc[o] - b.vcoef * v.Vp[o];
+  }
+}
+
+// K6 (grid: tiles x planes): complex: Wn = (z/gamma_old - a3 Wp - a2 Wc) / a1, X += xcoef Wn;
+// real: P = Zr + beta P.
+__global__ void __launch_bounds__(SP_T) k_sp_upd2(long long N, int ell, SpVec v, const SpBlk* blk,
+                                                  const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y, h = ell / 2, kb = sp_block_of(ell, pl);
+  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (p >= N) return;
+  const long long o = (long long)pl * N + p;
+  const SpBlk& b = blk[kb];
+  if (b.stop == 1) return;
+  if (kb == 0 || kb == h) {
+    v.P[o] = fma(b.beta, v.P[o], v.Zr[o]);
+  } else {
+    const double zs = v.Zc[o] / b.gamma_prev;
+    const double wn = (zs - b.a3 * v.Wp[o] - b.a2 * v.Wc[o]) / b.a1;
+    v.Wn[o] = wn;
+    v.X[o] = fma(b.xcoef, wn, v.X[o]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+static int sp_alloc(aac_ctx* ctx, SpPlan* P, double** p, long long n) {
+  if (cudaMalloc((void**)p, (size_t)std::max<long long>(n, 1) * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return aac_fail(ctx, AAC_ENOMEM, "SP workspace allocation failed");
+  }
+  P->owned.push_back(*p);
+  return AAC_OK;
+}
+
+static void sp_destroy(aac_ctx* ctx) {
+  if (!ctx->sp) return;
+  for (void* p : ctx->sp->owned) cudaFree(p);
+  delete ctx->sp;
+  ctx->sp = nullptr;
+}
+
+struct HostLevel {
+  int nx, ny, nz;
+  std::vector<double> wx, wy, wz, cnt;      // lower-face layout, padded like aac_setup
+};
+
+static inline long long pad4l(long long v) { return (v + 3) / 4 * 4; }
+
+static HostLevel coarsen(const HostLevel& f, int dim) {
+  HostLevel c;
+  c.nx = f.nx > 1 ? (f.nx + 1) / 2 : 1;
+  c.ny = f.ny > 1 ? (f.ny + 1) / 2 : 1;
+  c.nz = f.nz > 1 ? (f.nz + 1) / 2 : 1;
+  const long long Nc = (long long)c.nx * c.ny * c.nz, Nf = (long long)f.nx * f.ny * f.nz;
+  const long long Sc = dim == 3 ? (long long)c.nx * c.ny : c.nx;
+  c.wx.assign(pad4l(Nc + 1), 0.0);
+  c.wy.assign(pad4l(Nc + c.nx), 0.0);
+  c.wz.assign(pad4l(Nc + Sc), 0.0);
+  c.cnt.assign(Nc, 0.0);
+  auto fi = [&](long long x, long long y, long long z) { return (z * f.ny + y) * f.nx + x; };
+  auto ci = [&](long long x, long long y, long long z) { return (z * c.ny + y) * c.nx + x; };
+  (void)Nf;
+  for (long long z = 0; z < f.nz; ++z)
+    for (long long y = 0; y < f.ny; ++y)
+      for (long long x = 0; x < f.nx; ++x) {
+        const long long pf = fi(x, y, z);
+        const long long X = x / 2, Y = f.ny > 1 ? y / 2 : 0, Z = f.nz > 1 ? z / 2 : 0;
+        const long long pc = ci(X, Y, Z);
+        c.cnt[pc] += f.cnt[pf];
+        // a fine lower face between two different aggregates adds to the coarse lower face
+        if (x > 0 && (x & 1) == 0) c.wx[pc] += f.wx[pf];
+        if (dim >= 2 && y > 0 && (y & 1) == 0) c.wy[pc] += f.wy[pf];
+        if (dim >= 3 && z > 0 && (z & 1) == 0) c.wz[pc] += f.wz[pf];
+      }
+  return c;
+}
+
+// dense A_c(s) = diag((1+s) cnt + sum w) - W, inverted by Cholesky (SPD)
+static bool dense_inverse(const HostLevel& c, int dim, double s, std::vector<double>& inv) {
+  const int n = c.nx * c.ny * c.nz;
+  std::vector<double> A((size_t)n * n, 0.0);
+  const long long S = dim == 3 ? (long long)c.nx * c.ny : c.nx;
+  for (int z = 0; z < c.nz; ++z)
+    for (int y = 0; y < c.ny; ++y)
+      for (int x = 0; x < c.nx; ++x) {
+        const int p = (z * c.ny + y) * c.nx + x;
+        A[(size_t)p * n + p] += (1.0 + s) * c.cnt[p];
+        auto edge = [&](int q, double w) {
+          A[(size_t)p * n + p] += w;
+          A[(size_t)q * n + q] += w;
+          A[(size_t)p * n + q] -= w;
+          A[(size_t)q * n + p] -= w;
+        };
+        if (x > 0) edge(p - 1, c.wx[p]);
+        if (dim >= 2 && y > 0) edge(p - c.nx, c.wy[p]);
+        if (dim >= 3 && z > 0) edge((int)(p - S), c.wz[p]);
+      }
+  // Cholesky A = L L^T (lower, in place)
+  for (int j = 0; j < n; ++j) {
+    double d = A[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= A[(size_t)j * n + k] * A[(size_t)j * n + k];
+    if (!(d > 0.0)) return false;
+    d = sqrt(d);
+    A[(size_t)j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double v = A[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) v -= A[(size_t)i * n + k] * A[(size_t)j * n + k];
+      A[(size_t)i * n + j] = v / d;
+    }
+  }
+  inv.assign((size_t)n * n, 0.0);
+  std::vector<double> col(n);
+  for (int e = 0; e < n; ++e) {          // solve L L^T x = e_e
+    for (int i = 0; i < n; ++i) {
+      double v = (i == e) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) v -= A[(size_t)i * n + k] * col[k];
+      col[i] = v / A[(size_t)i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double v = col[i];
+      for (int k = i + 1; k < n; ++k) v -= A[(size_t)k * n + i] * col[k];
+      col[i] = v / A[(size_t)i * n + i];
+    }
+    for (int i = 0; i < n; ++i) inv[(size_t)i * n + e] = col[i];
+  }
+  return true;
+}
+
+static void shift_of_block(const aac_ctx* ctx, int kb, double* lr, double* li);
+
 static int sp_prepare(aac_ctx* ctx, int k) {
   (void)k;
-  return aac_fail(ctx, AAC_EINVAL, "AAC_SP inner solver not built yet");
+  if (ctx->sp) return AAC_OK;
+  if (ctx->nranks > 1)
+    return aac_fail(ctx, AAC_EINVAL, "AAC_SP runs on one rank (multigrid across slabs not built)");
+  SpPlan* P = new SpPlan();
+  ctx->sp = P;
+  const int ell = ctx->ell, h = ell / 2, dim = ctx->dim;
+  P->ell = ell;
+  P->h = h;
+  const Geo& g0 = ctx->geo;
+  const long long N = g0.N, L = (long long)ell * N;
+  // block shifts
+  P->K.ell = ell;
+  for (int kb = 0; kb <= h; ++kb) {
+    double lr, li;
+    shift_of_block(ctx, kb, &lr, &li);
+    if (kb == 0 || kb == h) {
+      P->K.lre[kb] = lr;
+      P->K.lim[kb] = 0.0;
+    } else {                                    // lambda = conj(Lambda_k): Im lambda > 0
+      P->K.lre[kb] = lr;
+      P->K.lim[kb] = -li;
+    }
+  }
+  for (int pl = 0; pl < ell; ++pl) {
+    const int kb = pl == 0 ? 0 : (pl == ell - 1 ? h : (pl + 1) / 2);
+    P->K.s[pl] = (kb == 0 || kb == h) ? -P->K.lre[kb] : P->K.lim[kb] - P->K.lre[kb];
+  }
+  // level 0 from the device face weights
+  HostLevel f;
+  f.nx = g0.nx;
+  f.ny = g0.ny;
+  f.nz = g0.nz;
+  const long long lenx = pad4l(N + 1), leny = pad4l(N + g0.nx), lenz = pad4l(N + g0.S);
+  f.wx.resize(lenx);
+  f.wy.resize(leny);
+  f.wz.resize(lenz);
+  CUDA_TRY(ctx, cudaMemcpy(f.wx.data(), g0.wx, lenx * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(f.wy.data(), g0.wy, leny * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(f.wz.data(), g0.wz, lenz * sizeof(double), cudaMemcpyDeviceToHost));
+  f.cnt.assign(N, 1.0);
+  std::vector<HostLevel> hl{f};
+  while (std::max(hl.back().nx, std::max(hl.back().ny, hl.back().nz)) > SP_COARSE_MAX_AXIS)
+    hl.push_back(coarsen(hl.back(), dim));
+  // device levels
+  for (size_t l = 0; l < hl.size(); ++l) {
+    const HostLevel& H = hl[l];
+    SpLevel lv{};
+    Geo& g = lv.g;
+    g.nx = H.nx;
+    g.ny = H.ny;
+    g.nz = H.nz;
+    g.N = (long long)H.nx * H.ny * H.nz;
+    g.S = dim == 3 ? (long long)H.nx * H.ny : H.nx;
+    g.has_lo = g.has_hi = 0;
+    double* w = nullptr;
+    const size_t nw = H.wx.size() + H.wy.size() + H.wz.size();
+    AAC_TRY(sp_alloc(ctx, P, &w, nw));
+    CUDA_TRY(ctx, cudaMemcpy(w, H.wx.data(), H.wx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(w + H.wx.size(), H.wy.data(), H.wy.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(w + H.wx.size() + H.wy.size(), H.wz.data(), H.wz.size() * sizeof(double),
+                             cudaMemcpyHostToDevice));
+    g.wx = w;
+    g.wy = w + H.wx.size();
+    g.wz = w + H.wx.size() + H.wy.size();
+    AAC_TRY(sp_alloc(ctx, P, &lv.cnt, g.N));
+    CUDA_TRY(ctx, cudaMemcpy(lv.cnt, H.cnt.data(), g.N * sizeof(double), cudaMemcpyHostToDevice));
+    if (l > 0) AAC_TRY(sp_alloc(ctx, P, &lv.b, (long long)ell * g.N));
+    AAC_TRY(sp_alloc(ctx, P, &lv.x, (long long)ell * g.N));
+    if (l > 0) AAC_TRY(sp_alloc(ctx, P, &lv.x2, (long long)ell * g.N));
+    P->lev.push_back(lv);
+  }
+  // coarsest dense inverses, one per block shift
+  const HostLevel& Hc = hl.back();
+  P->nc = Hc.nx * Hc.ny * Hc.nz;
+  std::vector<double> allinv((size_t)(h + 1) * P->nc * P->nc);
+  for (int kb = 0; kb <= h; ++kb) {
+    const int pl = kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1);
+    std::vector<double> inv;
+    if (!dense_inverse(Hc, dim, P->K.s[pl], inv))
+      return aac_fail(ctx, AAC_EINVAL, "coarsest multigrid operator not SPD");
+    std::copy(inv.begin(), inv.end(), allinv.begin() + (size_t)kb * P->nc * P->nc);
+  }
+  AAC_TRY(sp_alloc(ctx, P, &P->minv, (long long)allinv.size()));
+  CUDA_TRY(ctx, cudaMemcpy(P->minv, allinv.data(), allinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  // Krylov workspaces
+  double** bufs[] = {&P->X, &P->Vb[0], &P->Vb[1], &P->Vb[2], &P->Zb[0], &P->Zb[1], &P->Wb[0],
+                     &P->Wb[1], &P->Wb[2], &P->SZ, &P->R, &P->P, &P->Zr};
+  for (double** b : bufs) AAC_TRY(sp_alloc(ctx, P, b, L));
+  double* blk = nullptr;
+  AAC_TRY(sp_alloc(ctx, P, &blk, (long long)(h + 1) * (sizeof(SpBlk) / sizeof(double) + 1)));
+  P->blk = reinterpret_cast<SpBlk*>(blk);
+  CUDA_TRY(ctx, cudaMemset(P->blk, 0, (h + 1) * sizeof(SpBlk)));
+  const long long ntile = (N + SP_T - 1) / SP_T;
+  AAC_TRY(sp_alloc(ctx, P, &P->part, ntile * ell + 8));
+  double* tk = nullptr;
+  AAC_TRY(sp_alloc(ctx, P, &tk, 1));
+  P->tick = reinterpret_cast<unsigned*>(tk);
+  CUDA_TRY(ctx, cudaMemset(P->tick, 0, sizeof(double)));
+  return AAC_OK;
 }
-static int sp_gmres_precond(aac_ctx* ctx, int k) { return sp_prepare(ctx, k); }
-static int sp_gmres_finalize(aac_ctx* ctx) { return sp_prepare(ctx, 0); }
+
+template <int DIM>
+static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
+  SpPlan* P = ctx->sp;
+  const int ell = P->ell;
+  const int nl = (int)P->lev.size();
+  const IterState* st = S.st;
+  for (int l = 0; l < nl - 1; ++l) {                       // down
+    SpLevel& a = P->lev[l];
+    SpLevel& c = P->lev[l + 1];
+    const double* bl = l == 0 ? nullptr : a.b;
+    const dim3 gf(grid1d(a.g.N, SP_T), ell), gc(grid1d(c.g.N, SP_T), ell);
+    LAUNCH(ctx, KID_SP_MG, 16.0 * ell * a.g.N,
+           k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, P->K, io, bl, a.x, st));
+    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+           k_mg_restrict<DIM><<<gc, SP_T, 0, ctx->stream>>>(a.g, a.cnt, c.g, P->K, io, bl, a.x, c.b, st));
+  }
+  SpLevel& cl = P->lev[nl - 1];
+  if (nl == 1) return aac_fail(ctx, AAC_EINVAL, "SP needs at least one coarsening (grid too small)");
+  LAUNCH(ctx, KID_SP_MG, 8.0 * ell * P->nc * P->nc,
+         k_mg_coarse<<<ell, SP_T, 0, ctx->stream>>>(P->nc, P->minv, ell, cl.b, cl.x2, st));
+  for (int l = nl - 2; l >= 0; --l) {                      // up
+    SpLevel& a = P->lev[l];
+    SpLevel& c = P->lev[l + 1];
+    const double* bl = l == 0 ? nullptr : a.b;
+    const dim3 gf(grid1d(a.g.N, SP_T), ell);
+    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+           k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, c.g, a.x, c.x2, st));
+    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+           k_mg_post<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0));
+  }
+  return AAC_OK;
+}
+
+// Inner solve on hat w (ctx->d_what) -> packed y in P->X -> inverse DFT -> z (zbase + j*zjs).
+template <int DIM>
+static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const IterState* st) {
+  SpPlan* P = ctx->sp;
+  const int ell = P->ell, h = P->h;
+  const long long N = ctx->geo.N;
+  const double V = 8.0 * ell * N;
+  double *Vp = P->Vb[0], *Vc = P->Vb[1], *Vn = P->Vb[2];
+  double *Zc = P->Zb[0], *Zn = P->Zb[1];
+  double *Wp = P->Wb[0], *Wc = P->Wb[1], *Wn = P->Wb[2];
+  auto vecs = [&]() {
+    SpVec v{P->X, Vp, Vc, Vn, Zc, Wp, Wc, Wn, P->SZ, P->R, P->P, P->Zr, ctx->d_what};
+    return v;
+  };
+  auto io_for = [&](bool init) {
+    MgIo io{};
+    for (int pl = 0; pl < ell; ++pl) {
+      const int kb = pl == 0 ? 0 : (pl == ell - 1 ? h : (pl + 1) / 2);
+      const long long o = (long long)pl * N;
+      if (kb == 0 || kb == h) {
+        io.in[pl] = P->R + o;
+        io.out[pl] = (init ? P->P : P->Zr) + o;
+      } else {
+        io.in[pl] = (init ? Vc : Vn) + o;
+        io.out[pl] = (init ? Zc : Zn) + o;
+      }
+    }
+    return io;
+  };
+  SpStepCtx S{P->blk, P->part, P->tick, P->K, 0, st};
+  const unsigned gt = grid1d(N, SP_T);
+  LAUNCH(ctx, KID_SP_VEC, 2.0 * V, k_sp_init<<<gt, SP_T, 0, ctx->stream>>>(N, ell, vecs(), st));
+  S.phase = 0;
+  AAC_TRY(sp_vcycle<DIM>(ctx, io_for(true), S));          // z_1 = M v_1 ; p_0 = M r_0
+  S.phase = 1;
+  for (int it = 0; it < k; ++it) {
+    LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+           k_sp_apply<DIM><<<dim3(gt, h + 1), SP_T, 0, ctx->stream>>>(ctx->geo, vecs(), S));
+    LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
+           k_sp_upd1<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
+    AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
+    LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
+           k_sp_upd2<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
+    // rotate: v_prev <- v <- v_next, z <- z_next, w_prev <- w <- w_next
+    double* t = Vp; Vp = Vc; Vc = Vn; Vn = t;
+    t = Zc; Zc = Zn; Zn = t;
+    t = Wp; Wp = Wc; Wc = Wn; Wn = t;
+  }
+  // z = Gamma^{-1} U y (y packed in X): the same inverse transform with unit block scales
+  NcFinal F{};
+  for (int kb = 0; kb <= h; ++kb) {
+    F.tr[kb] = 1.0;
+    F.ti[kb] = 0.0;
+  }
+  const Dft D = make_dft(ctx);
+  LAUNCH(ctx, KID_INV, 2.0 * V,
+         k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, P->X, zbase, zjs, st));
+  return AAC_OK;
+}
+
+static int sp_solve(aac_ctx* ctx, int k, double* zbase, long long zjs, const IterState* st) {
+  switch (ctx->dim) {
+    case 1: return sp_solve_t<1>(ctx, k, zbase, zjs, st);
+    case 2: return sp_solve_t<2>(ctx, k, zbase, zjs, st);
+    default: return sp_solve_t<3>(ctx, k, zbase, zjs, st);
+  }
+}
+
 static long long sp_paper_matvecs(const aac_ctx* ctx, int k) { return 2LL * (ctx->ell - 1) * k; }
-static void sp_destroy(aac_ctx* ctx) { (void)ctx; }

@@ -219,3 +219,42 @@ def test_headline_full_size_gmres_vs_stored_oracle():
     assert np.linalg.norm(xs[idx] - ref) <= 1e-9 * np.linalg.norm(ref)
     assert np.linalg.norm(xs) == pytest.approx(g["x_norm"], rel=1e-9)
     s.close()
+
+
+# ---------------------------------------------------------------- saddle-point inner solver (SP)
+SP_CASES = [
+    ("saddle", dict(shape=(1, 40, 36)), 8),
+    ("saddle", dict(shape=(1, 37, 53), ell=4, alpha=1e-2), 3),
+    ("2d256", dict(shape=(1, 24, 20), ell=12, alpha=0.3), 5),
+    ("1d", {}, 4),
+    ("3d", dict(shape=(12, 10, 9), ell=6), 3),
+]
+
+
+@pytest.mark.parametrize("name,kw,k", SP_CASES)
+def test_sp_precond_parity(name, kw, k):
+    from oracle import saddle
+    p = synth.make_problem(name, **kw)
+    s = _solver(p)
+    w = op.weights(p)
+    r = np.random.default_rng(5).standard_normal((p.ell,) + p.shape)
+    z = s.precond_apply("sp", k, _dev(r, p.ell)).cpu().numpy()
+    zo = saddle.sp_apply(w, r, p.ell, p.alpha, k)
+    assert _rel(z, zo) <= 1e-12
+    s.close()
+
+
+def test_sp_gmres_parity():
+    from oracle import saddle
+    p = synth.make_problem("saddle", shape=(1, 64, 48))
+    s = _solver(p, max_krylov=40)
+    x, info = s.gmres("sp", p.k, _dev(p.b, p.ell), rtol=p.rtol, maxit=40)
+    w = op.weights(p)
+    lev = saddle.hierarchy(w)
+    ro = og.fgmres(lambda v: op.apply_allatonce(w, v),
+                   lambda v: saddle.sp_apply(w, v, p.ell, p.alpha, p.k, lev), p.b, p.rtol, 40)
+    assert info["converged"] == 1 and ro.converged
+    assert abs(info["iters"] - ro.iters) <= 1
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    assert info["matvecs_paper_units"] == info["iters"] * (p.ell + 2 * (p.ell - 1) * p.k)
+    s.close()
