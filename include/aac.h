@@ -66,6 +66,16 @@ typedef struct {
  * Returns AAC_EINVAL on nranks < 1, rank out of range or n < nranks.             */
 int aac_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi);
 
+/* Host-only (no GPU needed): this rank's face weights w_f = c kappa_f n_a^2 in the device
+ * layout used by the kernels -- three "lower face" arrays wx | wy | wz, concatenated, lengths
+ * lens[0..2] (each padded to a multiple of 4 doubles): w?[p] is the face between point p and
+ * its lower neighbour along the axis (0 on physical boundaries), and w?[p + stride] is p's
+ * upper face, so the slab's top face sits in the extra layer at the end of the slab axis.
+ * Call with w_out == NULL to get the lengths; gershgorin (may be NULL) receives the local
+ * max_P (1 + 2 sum_f w_f). Same inputs and errors as aac_setup.                             */
+int aac_slab_weights(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+                     double c, double* w_out, int64_t* lens, double* gershgorin);
+
 /* Create a solver context on the current CUDA device.
  *  kx, ky, kz : HOST pointers to the GLOBAL interior-face diffusivities kappa_f
  *               (anisotropy already applied), natural layouts

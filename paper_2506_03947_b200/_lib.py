@@ -18,7 +18,7 @@ AAC_NC1, AAC_NC2, AAC_SP = 1, 2, 3
 METHODS = {"nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
-SYMBOLS = ["aac_slab_range", "aac_setup", "aac_matvec", "aac_precond_apply", "aac_gmres",
+SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_matvec", "aac_precond_apply", "aac_gmres",
            "aac_gmres_host", "aac_query", "aac_profile_enable", "aac_profile_count",
            "aac_profile_read", "aac_profile_reset", "aac_launch_count", "aac_last_error",
            "aac_destroy"]
@@ -54,6 +54,8 @@ def _load():
     sig = {
         "aac_slab_range": (I, [ctypes.c_int64, I, I, ctypes.POINTER(ctypes.c_int64),
                                ctypes.POINTER(ctypes.c_int64)]),
+        "aac_slab_weights": (I, [ctypes.POINTER(aac_grid), dp, dp, dp, D, dp,
+                                 ctypes.POINTER(ctypes.c_int64), dp]),
         "aac_setup": (I, [ctypes.POINTER(aac_grid), dp, dp, dp, D, I, D, I, P, P,
                           ctypes.POINTER(P)]),
         "aac_matvec": (I, [P, P, P]),

@@ -99,6 +99,90 @@ extern "C" int aac_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int6
 
 static bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
+// Local face weights of slab [lo, hi) in the lower-face layout (see Geo), each sub-array
+// padded to 4 doubles: wx | wy | wz. Returns false on a non-positive / non-finite kappa.
+static bool slab_weights(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+                         double c, long long lo, long long hi, std::vector<double>& hw,
+                         long long lens[3], double* gershgorin) {
+  const long long nx = g->n[0], ny = g->dim >= 2 ? g->n[1] : 1, nz = g->dim >= 3 ? g->n[2] : 1;
+  const long long lny = g->dim == 2 ? hi - lo : ny, lnz = g->dim == 3 ? hi - lo : 1;
+  const long long N = nx * lny * lnz, S = g->dim == 3 ? nx * lny : nx;
+  auto pad4 = [](long long v) { return (v + 3) / 4 * 4; };
+  lens[0] = pad4(N + 1);
+  lens[1] = pad4(N + nx);
+  lens[2] = pad4(N + S);
+  hw.assign(lens[0] + lens[1] + lens[2], 0.0);
+  double* wx = hw.data();
+  double* wy = wx + lens[0];
+  double* wz = wy + lens[1];
+  const double sx = c * (double)nx * (double)nx, sy = c * (double)ny * (double)ny,
+               sz = c * (double)nz * (double)nz;
+  bool bad = false;
+  const long long z0 = g->dim == 3 ? lo : 0, y0 = g->dim == 2 ? lo : 0;
+  for (long long zl = 0; zl < lnz; ++zl)
+    for (long long yl = 0; yl < lny; ++yl)
+      for (long long x = 0; x < nx; ++x) {
+        const long long p = (zl * lny + yl) * nx + x;
+        const long long zg = z0 + zl, yg = y0 + yl;
+        if (x > 0) {
+          const double k = kx[(zg * ny + yg) * (nx - 1) + (x - 1)];
+          bad |= !finite_pos(k);
+          wx[p] = sx * k;
+        }
+        if (g->dim >= 2 && yg > 0) {
+          const double k = ky[(zg * (ny - 1) + (yg - 1)) * nx + x];
+          bad |= !finite_pos(k);
+          wy[p] = sy * k;
+        }
+        if (g->dim == 3 && zg > 0) {
+          const double k = kz[((zg - 1) * ny + yg) * nx + x];
+          bad |= !finite_pos(k);
+          wz[p] = sz * k;
+        }
+      }
+  // the slab's top face (layer index = local extent) along the slab axis
+  if (g->dim == 2 && hi < ny)
+    for (long long x = 0; x < nx; ++x) {
+      const double k = ky[(hi - 1) * nx + x];
+      bad |= !finite_pos(k);
+      wy[N + x] = sy * k;
+    }
+  if (g->dim == 3 && hi < nz)
+    for (long long yx = 0; yx < S; ++yx) {
+      const double k = kz[(hi - 1) * S + yx];
+      bad |= !finite_pos(k);
+      wz[N + yx] = sz * k;
+    }
+  // Gershgorin bound mu_max = max_P (1 + 2 sum_f w_f) (reading R5); mu_min = 1 exactly.
+  double gmax = 1.0;
+  for (long long p = 0; p < N; ++p) {
+    double sum = wx[p] + wx[p + 1];
+    if (g->dim >= 2) sum += wy[p] + wy[p + nx];
+    if (g->dim >= 3) sum += wz[p] + wz[p + S];
+    gmax = fmax(gmax, 1.0 + 2.0 * sum);
+  }
+  *gershgorin = gmax;
+  return !bad;
+}
+
+extern "C" int aac_slab_weights(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+                                double c, double* w_out, int64_t* lens_out, double* gershgorin) {
+  if (!g || !kx || !lens_out || g->dim < 1 || g->dim > 3 || g->nranks < 1)
+    return aac_fail(nullptr, AAC_EINVAL, "aac_slab_weights: bad arguments");
+  const long long nslab = g->dim == 2 ? g->n[1] : (g->dim == 3 ? g->n[2] : 1);
+  int64_t lo = 0, hi = nslab;
+  if (g->dim > 1 && aac_slab_range(nslab, g->nranks, g->rank, &lo, &hi) != AAC_OK) return AAC_EINVAL;
+  if (g->dim == 1 && g->nranks != 1) return aac_fail(nullptr, AAC_EINVAL, "1D problems run on one rank");
+  std::vector<double> hw;
+  long long lens[3];
+  double gm = 1.0;
+  const bool ok = slab_weights(g, kx, ky, kz, c, lo, hi, hw, lens, &gm);
+  for (int a = 0; a < 3; ++a) lens_out[a] = lens[a];
+  if (gershgorin) *gershgorin = gm;
+  if (w_out) std::copy(hw.begin(), hw.end(), w_out);
+  return ok ? AAC_OK : aac_fail(nullptr, AAC_EINVAL, "kappa must be finite and > 0 on every interior face");
+}
+
 extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, const double* kz,
                          double c, int ell, double alpha, int max_krylov, void* cuda_stream,
                          const void* nccl_id, aac_ctx** out) {
@@ -150,64 +234,15 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   G.has_hi = (g->nranks > 1 && g->rank < g->nranks - 1);
   const long long N = G.N;
 
-  // Face weights w_f = c kappa_f n_a^2, lower-face layout with one padding layer (host build).
-  // sub-array lengths padded to 4 doubles: 16-byte vector loads stay aligned in every array
-  auto pad4 = [](long long v) { return (v + 3) / 4 * 4; };
-  const long long lenx = pad4(N + 1), leny = pad4(N + G.nx), lenz = pad4(N + G.S);
-  std::vector<double> hw(lenx + leny + lenz, 0.0);
-  double* wx = hw.data();
-  double* wy = wx + lenx;
-  double* wz = wy + leny;
-  const double sx = c * (double)nx * (double)nx, sy = c * (double)ny * (double)ny,
-               sz = c * (double)nz * (double)nz;
-  bool bad = false;
-  const long long z0 = g->dim == 3 ? lo : 0, y0 = g->dim == 2 ? lo : 0;
-  for (long long zl = 0; zl < G.nz; ++zl)
-    for (long long yl = 0; yl < G.ny; ++yl)
-      for (long long x = 0; x < nx; ++x) {
-        const long long p = (zl * G.ny + yl) * nx + x;
-        const long long zg = z0 + zl, yg = y0 + yl;
-        if (x > 0) {
-          const double k = kx[(zg * ny + yg) * (nx - 1) + (x - 1)];
-          bad |= !finite_pos(k);
-          wx[p] = sx * k;
-        }
-        if (g->dim >= 2 && yg > 0) {
-          const double k = ky[(zg * (ny - 1) + (yg - 1)) * nx + x];
-          bad |= !finite_pos(k);
-          wy[p] = sy * k;
-        }
-        if (g->dim == 3 && zg > 0) {
-          const double k = kz[((zg - 1) * ny + yg) * nx + x];
-          bad |= !finite_pos(k);
-          wz[p] = sz * k;
-        }
-      }
-  // the slab's top face (layer index = local extent) along the slab axis
-  if (g->dim == 2 && hi < ny)
-    for (long long x = 0; x < nx; ++x) {
-      const double k = ky[(hi - 1) * nx + x];
-      bad |= !finite_pos(k);
-      wy[N + x] = sy * k;
-    }
-  if (g->dim == 3 && hi < nz)
-    for (long long yx = 0; yx < G.S; ++yx) {
-      const double k = kz[(hi - 1) * G.S + yx];
-      bad |= !finite_pos(k);
-      wz[N + yx] = sz * k;
-    }
-  if (bad) {
+  // Face weights w_f = c kappa_f n_a^2 of this slab (host build) + local Gershgorin max.
+  std::vector<double> hw;
+  long long lens[3];
+  double gmax = 1.0;
+  if (!slab_weights(g, kx, ky, kz, c, lo, hi, hw, lens, &gmax)) {
     delete ctx;
     return aac_fail(nullptr, AAC_EINVAL, "kappa must be finite and > 0 on every interior face");
   }
-  // Gershgorin bound mu_max = max_P (1 + 2 sum_f w_f) (reading R5); mu_min = 1 exactly.
-  double gmax = 1.0;
-  for (long long p = 0; p < N; ++p) {
-    double s = wx[p] + wx[p + 1];
-    if (g->dim >= 2) s += wy[p] + wy[p + G.nx];
-    if (g->dim >= 3) s += wz[p] + wz[p + G.S];
-    gmax = fmax(gmax, 1.0 + 2.0 * s);
-  }
+  const long long lenx = lens[0], leny = lens[1];
 
   int rc = comm_init(ctx, nccl_id);
   if (rc != AAC_OK) {
