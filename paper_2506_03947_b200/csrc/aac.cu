@@ -37,7 +37,7 @@ int aac_fail(aac_ctx* ctx, int code, const char* fmt, ...) {
 
 static const char* kKernelNames[KID_COUNT] = {
     "matvec", "forward_dft", "cheb_sweep", "inverse_dft", "multidot", "cgs_update",
-    "reduce", "scalar", "axpy", "sp_stencil", "sp_multigrid", "sp_vector", "halo"};
+    "reduce", "scalar", "axpy", "sp_stencil", "sp_multigrid", "sp_vector", "halo", "arnoldi"};
 
 LaunchScope::LaunchScope(aac_ctx* c, int kid, double bytes) : ctx(c), id(kid) {
   ctx->launches++;
@@ -556,7 +556,7 @@ static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
   const size_t smem = TMA ? (size_t)FS * ELLC * FT * sizeof(double) : 0;
   AAC_TRY(smem_optin(ctx, k_fwd_upd<ELLC, TMA>, smem));
   LAUNCH(ctx, KID_FWD, bytes,
-         (k_fwd_upd<ELLC, TMA><<<grid1d(N, FT), FT, smem, ctx->stream>>>(N, D, ctx->d_what, U)));
+         (k_fwd_upd<ELLC, TMA><<<grid1d(N, FT), FT + 32, smem, ctx->stream>>>(N, D, ctx->d_what, U)));
   return AAC_OK;
 }
 
@@ -571,7 +571,7 @@ static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
 // last sweep fused with the inverse DFT. gmres_mode: input is the Arnoldi update (W, V, c),
 // output Z_j with j read on the device; otherwise r -> z.
 template <int DIM, int VEC>
-static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zbase, bool gmres_mode) {
+static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zbase, bool gmres_mode, int host_j) {
   const Geo& g = ctx->geo;
   const int ell = ctx->ell, h = ell / 2;
   const long long N = g.N, L = (long long)ell * N;
@@ -579,8 +579,8 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   const Dft D = make_dft(ctx);
   const IterState* st = gmres_mode ? ctx->d_st : nullptr;
   if (gmres_mode) {
-    // model bytes: read W + V_0..V_{j-1}, write V_j and hat w (j averaged out: counted as 3V)
-    AAC_TRY(launch_fwd_upd(ctx, 3 * V));
+    // algorithmic bytes: W + V_0..V_{j-1} in, V_j and hat w out
+    AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
     if (ctx->nranks > 1) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
@@ -662,13 +662,13 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   return AAC_OK;
 }
 
-static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z, bool gmres_mode) {
+static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z, bool gmres_mode, int host_j = 0) {
   const NcPlan& P = nc_plan(ctx, method, k);
   const bool v2 = vec2(ctx);
   switch (ctx->dim) {
-    case 1: return v2 ? nc_apply_t<1, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<1, 1>(ctx, P, r, z, gmres_mode);
-    case 2: return v2 ? nc_apply_t<2, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<2, 1>(ctx, P, r, z, gmres_mode);
-    default: return v2 ? nc_apply_t<3, 2>(ctx, P, r, z, gmres_mode) : nc_apply_t<3, 1>(ctx, P, r, z, gmres_mode);
+    case 1: return v2 ? nc_apply_t<1, 2>(ctx, P, r, z, gmres_mode, host_j) : nc_apply_t<1, 1>(ctx, P, r, z, gmres_mode, host_j);
+    case 2: return v2 ? nc_apply_t<2, 2>(ctx, P, r, z, gmres_mode, host_j) : nc_apply_t<2, 1>(ctx, P, r, z, gmres_mode, host_j);
+    default: return v2 ? nc_apply_t<3, 2>(ctx, P, r, z, gmres_mode, host_j) : nc_apply_t<3, 1>(ctx, P, r, z, gmres_mode, host_j);
   }
 }
 
@@ -694,39 +694,40 @@ extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* 
 // ------------------------------------------------------------------------------------------
 // GMRES
 template <int DIM, int ELLC, bool TMA>
-static int launch_arnoldi(aac_ctx* ctx) {
+static int launch_arnoldi(aac_ctx* ctx, int host_j) {
   const Geo& g = ctx->geo;
   const int ldh = ctx->max_krylov + 1;
   KAParams P{ctx->d_Z, ctx->d_V, ctx->d_W, (long long)ctx->ell * g.N, ctx->d_part,
              ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, arnoldi_ctx(ctx)};
-  const size_t smem = (arnoldi_ring_doubles<ELLC>() + (size_t)(AT / 32 + 1) * 2 * ldh) * sizeof(double);
+  const size_t smem = (arnoldi_ring_doubles<ELLC>() + (size_t)(AW + 1) * 2 * ldh) * sizeof(double);
   // persistent grid: exactly the resident capacity (no partial second wave)
   static thread_local int occ_cache[2][4][2] = {};
   int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0];
   if (!occ) {
     AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA>, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA>, AT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA>, AT + 32, smem);
     if (occ < 1) occ = 1;
   }
   const long long ntile = (g.N + AT - 1) / AT;
   const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ntile);
   const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
-  LAUNCH(ctx, KID_MATVEC, 2 * V + C, (k_arnoldi<DIM, ELLC, TMA><<<grid, AT, smem, ctx->stream>>>(g, ctx->ell, P)));
+  // algorithmic bytes: Z_j + C in, W out, basis V_0..V_j in
+  LAUNCH(ctx, KID_ARNOLDI, (host_j + 3) * V + C, (k_arnoldi<DIM, ELLC, TMA><<<grid, AT + 32, smem, ctx->stream>>>(g, ctx->ell, P)));
   return AAC_OK;
 }
 
 template <int DIM>
-static int arnoldi_dim(aac_ctx* ctx) {
+static int arnoldi_dim(aac_ctx* ctx, int host_j) {
   const bool tma = (ctx->geo.N % 2) == 0;
-  if (ctx->ell <= 10) return tma ? launch_arnoldi<DIM, 10, true>(ctx) : launch_arnoldi<DIM, 10, false>(ctx);
-  return tma ? launch_arnoldi<DIM, 16, true>(ctx) : launch_arnoldi<DIM, 16, false>(ctx);
+  if (ctx->ell <= 10) return tma ? launch_arnoldi<DIM, 10, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false>(ctx, host_j);
+  return tma ? launch_arnoldi<DIM, 16, true>(ctx, host_j) : launch_arnoldi<DIM, 16, false>(ctx, host_j);
 }
 
-static int arnoldi_impl(aac_ctx* ctx) {
+static int arnoldi_impl(aac_ctx* ctx, int host_j) {
   switch (ctx->dim) {
-    case 1: return arnoldi_dim<1>(ctx);
-    case 2: return arnoldi_dim<2>(ctx);
-    default: return arnoldi_dim<3>(ctx);
+    case 1: return arnoldi_dim<1>(ctx, host_j);
+    case 2: return arnoldi_dim<2>(ctx, host_j);
+    default: return arnoldi_dim<3>(ctx, host_j);
   }
 }
 
@@ -735,14 +736,14 @@ static int arnoldi_impl(aac_ctx* ctx) {
 static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
-    AAC_TRY(launch_fwd_upd(ctx, 3 * V));
+    AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
     if (ctx->nranks > 1) return aac_fail(ctx, AAC_EINVAL, "AAC_SP runs on one rank");
     AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
   } else {
-    AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true));
+    AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j));
   }
   if (ctx->nranks > 1) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
-  AAC_TRY(arnoldi_impl(ctx));
+  AAC_TRY(arnoldi_impl(ctx, host_j));
   if (ctx->nranks > 1) {
     AAC_TRY(comm_allreduce(ctx, ctx->d_red, 2 * (host_j + 1), ncclSum));
     LAUNCH(ctx, KID_SCALAR, 0, k_scalar_cgs2<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));

@@ -51,6 +51,7 @@ enum KernelId {
   KID_SP_MG,           // SP: multigrid smoother / transfer / coarse solve
   KID_SP_VEC,          // SP: Krylov vector updates and dots
   KID_HALO,            // halo pack/copy
+  KID_ARNOLDI,         // calA apply fused with the CGS2 projections + Gram column
   KID_COUNT
 };
 

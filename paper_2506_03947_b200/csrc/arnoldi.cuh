@@ -21,15 +21,18 @@ struct KAParams {
   ArnoldiCtx ac;
 };
 
-constexpr int AT = 256;          // tile points per CTA iteration (one per thread)
-constexpr int AS = 3;            // bulk-copy pipeline stages for the basis tiles
+constexpr int AT = 256;          // tile points per CTA iteration (one per consumer thread)
+constexpr int AS = 4;            // bulk-copy pipeline stages for the basis tiles
+constexpr int AW = AT / 32;      // consumer warps; warp AW is the TMA producer
 
-// Dynamic shared memory layout: [AS][ELLC][AT] basis ring | [nw][2*(ldh)] acc | [2*ldh] tot
+// Dynamic shared memory layout: [AS][ELLC][AT] basis ring | [AW][2*ldh] acc | [2*ldh] tot
 template <int ELLC>
 __host__ __device__ constexpr size_t arnoldi_ring_doubles() { return (size_t)AS * ELLC * AT; }
 
+// Warp-specialised: warps 0..AW-1 compute (stencil, dots), warp AW streams the basis tiles
+// V_i (i <= j) of every tile through the bulk-copy ring (full / empty mbarriers per stage).
 template <int DIM, int ELLC, bool TMA>
-__global__ void __launch_bounds__(AT, 2) k_arnoldi(Geo g, int ell, KAParams P) {
+__global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams P) {
   IterState* st = P.ac.st;
   if (st->done) return;
   const int j = st->j;
@@ -37,104 +40,107 @@ __global__ void __launch_bounds__(AT, 2) k_arnoldi(Geo g, int ell, KAParams P) {
   extern __shared__ __align__(16) double smem[];
   double* ring = smem;
   double* acc = smem + arnoldi_ring_doubles<ELLC>();
-  __shared__ __align__(8) uint64_t bar[AS];
+  __shared__ __align__(8) uint64_t full[AS], empty[AS];
   __shared__ bool last;
-  const int nw = AT / 32, t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  for (int k = t; k < nw * nv2; k += AT) acc[k] = 0.0;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int k = t; k < AW * nv2; k += blockDim.x) acc[k] = 0.0;
   const long long N = g.N;
   const long long ntile = (N + AT - 1) / AT;
   const long long my_tiles = blockIdx.x < ntile ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const long long nitems = my_tiles * nv;       // item k -> (tile r = k / nv, basis vector i = k % nv)
   auto tile_base = [&](long long r) { return (blockIdx.x + r * gridDim.x) * (long long)AT; };
-  auto issue = [&](long long k) {
-    const long long r = k / nv;
-    const int i = (int)(k % nv);
-    const long long b = tile_base(r);
-    const int len = (int)((N - b) < AT ? (N - b) : AT);
-    const int s = (int)(k % AS);
-    bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + b, N, ell, len, &bar[s]);
-  };
-  if constexpr (TMA) {
-    if (t == 0) {
-      for (int s = 0; s < AS; ++s) mbar_init(&bar[s], 1);
-      fence_mbar_init();
+  if (TMA && t == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], AW);
     }
+    fence_mbar_init();
   }
   __syncthreads();
-  if constexpr (TMA) {
-    if (t == 0)
-      for (long long k = 0; k < nitems && k < AS; ++k) issue(k);
-  }
-  const double* z = P.Z + (long long)j * P.L;
-  const double* vj = P.V + (long long)j * P.L;
-  for (long long r = 0; r < my_tiles; ++r) {
-    const long long b = tile_base(r);
-    const int len = (int)((N - b) < AT ? (N - b) : AT);
-    const int lb = len & ~1;
-    const bool valid = t < len;
-    const long long p = b + t;
-    double w[ELLC], u[ELLC];
-    if (valid) {
-      PtV<DIM, 1> q;
-      load_ptv<DIM, 1>(g, p, q);
-      // planes in pairs: all loads of a pair are issued before its stores
-#pragma unroll
-      for (int g0 = 0; g0 < ELLC; g0 += 2) {
-        SV<1> sv[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int pl = g0 + k;
-          if (pl < ell) {
-            load_sv<DIM, 1>(g, q, z + (long long)pl * N, P.hlo + pl * g.S, P.hhi + pl * g.S, sv[k]);
-            u[pl] = vj[(long long)pl * N + p];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int pl = g0 + k;
-          if (pl < ell) {
-            double a[1];
-            stencil_sv<DIM, 1>(q, sv[k], a);
-            w[pl] = a[0];
-            if (pl > 0) w[pl] -= (k > 0) ? sv[0].c[0] : z[(long long)(pl - 1) * N + p];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int pl = g0 + k;
-          if (pl < ell) P.W[(long long)pl * N + p] = w[pl];
-        }
+  if (warp == AW) {                             // ---- producer warp
+    if (TMA && lane == 0) {
+      for (long long k = 0; k < nitems; ++k) {
+        const int s = (int)(k % AS);
+        if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
+        const long long r = k / nv;
+        const int i = (int)(k % nv);
+        const long long b = tile_base(r);
+        const int len = (int)((N - b) < AT ? (N - b) : AT);
+        bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + b, N, ell, len, &full[s]);
       }
     }
-    for (int i = 0; i < nv; ++i) {
-      const long long k = r * nv + i;
-      const int s = (int)(k % AS);
-      if constexpr (TMA) mbar_wait(&bar[s], (uint32_t)((k / AS) & 1));
-      double sa = 0.0, ga = 0.0;
+  } else {                                      // ---- consumer warps
+    const double* z = P.Z + (long long)j * P.L;
+    const double* vj = P.V + (long long)j * P.L;
+    for (long long r = 0; r < my_tiles; ++r) {
+      const long long b = tile_base(r);
+      const int len = (int)((N - b) < AT ? (N - b) : AT);
+      const int lb = len & ~1;
+      const bool valid = t < len;
+      const long long p = b + t;
+      double w[ELLC], u[ELLC];
       if (valid) {
-        const double* vi = P.V + (long long)i * P.L + b;
-        FOR_PL(pl) {
-          const double v = (TMA && t < lb) ? ring[((long long)s * ELLC + pl) * AT + t] : vi[(long long)pl * N + t];
-          sa = fma(v, w[pl], sa);
-          ga = fma(v, u[pl], ga);
+        PtV<DIM, 1> q;
+        load_ptv<DIM, 1>(g, p, q);
+        // planes in pairs: all loads of a pair are issued before its stores
+#pragma unroll
+        for (int g0 = 0; g0 < ELLC; g0 += 2) {
+          SV<1> sv[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int pl = g0 + k;
+            if (pl < ell) {
+              load_sv<DIM, 1>(g, q, z + (long long)pl * N, P.hlo + pl * g.S, P.hhi + pl * g.S, sv[k]);
+              u[pl] = vj[(long long)pl * N + p];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int pl = g0 + k;
+            if (pl < ell) {
+              double a[1];
+              stencil_sv<DIM, 1>(q, sv[k], a);
+              w[pl] = a[0];
+              if (pl > 0) w[pl] -= (k > 0) ? sv[0].c[0] : z[(long long)(pl - 1) * N + p];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int pl = g0 + k;
+            if (pl < ell) P.W[(long long)pl * N + p] = w[pl];
+          }
         }
       }
-      sa = warp_sum(sa);
-      ga = warp_sum(ga);
-      if (lane == 0) {
-        acc[warp * nv2 + i] += sa;
-        acc[warp * nv2 + nv + i] += ga;
-      }
-      if constexpr (TMA) {
-        __syncthreads();                          // stage s consumed by every warp
-        if (t == 0 && k + AS < nitems) issue(k + AS);
+      for (int i = 0; i < nv; ++i) {
+        const long long k = r * nv + i;
+        const int s = (int)(k % AS);
+        if constexpr (TMA) mbar_wait(&full[s], (uint32_t)((k / AS) & 1));
+        double sa = 0.0, ga = 0.0;
+        if (valid) {
+          const double* vi = P.V + (long long)i * P.L + b;
+          FOR_PL(pl) {
+            const double v = (TMA && t < lb) ? ring[((long long)s * ELLC + pl) * AT + t] : vi[(long long)pl * N + t];
+            sa = fma(v, w[pl], sa);
+            ga = fma(v, u[pl], ga);
+          }
+        }
+        if constexpr (TMA) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+        }
+        sa = warp_sum(sa);
+        ga = warp_sum(ga);
+        if (lane == 0) {
+          acc[warp * nv2 + i] += sa;
+          acc[warp * nv2 + nv + i] += ga;
+        }
       }
     }
   }
   __syncthreads();
-  for (int k = t; k < nv2; k += AT) {
+  for (int k = t; k < nv2; k += blockDim.x) {
     double sum = 0.0;
-    for (int w2 = 0; w2 < nw; ++w2) sum += acc[w2 * nv2 + k];
+    for (int w2 = 0; w2 < AW; ++w2) sum += acc[w2 * nv2 + k];
     P.part[(long long)blockIdx.x * nv2 + k] = sum;
   }
   __threadfence();
@@ -146,8 +152,9 @@ __global__ void __launch_bounds__(AT, 2) k_arnoldi(Geo g, int ell, KAParams P) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double* tot = acc + nw * nv2;
-  for (int k = warp; k < nv2; k += nw) {       // fixed order: lane-strided, then warp tree
+  double* tot = acc + AW * nv2;
+  const int nwarps = blockDim.x >> 5;
+  for (int k = warp; k < nv2; k += nwarps) {   // fixed order: lane-strided, then warp tree
     double sum = 0.0;
     for (int c = lane; c < (int)gridDim.x; c += 32) sum += __ldcg(P.part + (long long)c * nv2 + k);
     sum = warp_sum(sum);

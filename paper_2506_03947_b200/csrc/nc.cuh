@@ -89,79 +89,87 @@ __global__ void __launch_bounds__(256) k_forward(long long N, Dft D, const doubl
   dft_store<ELLC>(D, N, p, w, what);
 }
 
-constexpr int FT = 256;        // tile points per CTA (one per thread)
+constexpr int FT = 256;        // tile points per CTA (one per consumer thread)
 constexpr int FS = 3;          // bulk-copy pipeline stages
+constexpr int FW = FT / 32;    // consumer warps; warp FW is the TMA producer
 
-// GMRES mode: form u from W and V_0..V_{j-1} (streamed through a TMA bulk-copy ring), store
-// V_j, reduce ||u||^2 (last CTA: Arnoldi norm step), and transform u.
+// GMRES mode: form u from W and V_0..V_{j-1} (streamed through a TMA bulk-copy ring fed by
+// a producer warp), store V_j, reduce ||u||^2 (last CTA: Arnoldi norm step), transform u.
 template <int ELLC, bool TMA>
-__global__ void __launch_bounds__(FT) k_fwd_upd(long long N, Dft D, double* __restrict__ what,
-                                                FwdUpd U) {
+__global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double* __restrict__ what,
+                                                     FwdUpd U) {
   extern __shared__ __align__(16) double sm[];      // [FS][ELLC][FT]
-  __shared__ __align__(8) uint64_t bar[FS];
-  __shared__ double red[FT / 32];
+  __shared__ __align__(8) uint64_t full[FS], empty[FS];
+  __shared__ double red[FW];
   __shared__ bool last;
   IterState* st = U.ac.st;
   if (st->done) return;
   const int j = st->j;
   const int ell = D.ell;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const long long base = (long long)blockIdx.x * FT;
   const int len = (int)((N - base) < FT ? (N - base) : FT);
   const int lb = len & ~1;
-  const bool valid = t < len;
   const long long L = U.L;
   const int nitems = j == 0 ? 1 : j + 1;   // item 0: W (or V_0 when j == 0); item k: V_{k-1}
   auto src_of = [&](int k) -> const double* {
     return k == 0 ? (j == 0 ? U.V : U.W) : U.V + (long long)(k - 1) * L;
   };
-  if constexpr (TMA) {
-    if (t == 0) {
-      for (int s = 0; s < FS; ++s) mbar_init(&bar[s], 1);
-      fence_mbar_init();
+  if (TMA && t == 0) {
+    for (int s = 0; s < FS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], FW);
     }
-    __syncthreads();
-    if (t == 0)
-      for (int k = 0; k < nitems && k < FS; ++k)
-        bulk_planes(sm + (long long)k * ELLC * FT, FT, src_of(k) + base, N, ell, len, &bar[k]);
+    fence_mbar_init();
   }
-  double w[ELLC];
-  FOR_PL(pl) w[pl] = 0.0;
-  for (int k = 0; k < nitems; ++k) {
-    const int s = k % FS;
-    const double coef = k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1];
-    const double* src = src_of(k) + base;
-    if constexpr (TMA) mbar_wait(&bar[s], (uint32_t)((k / FS) & 1));
-    if (valid) {
-      FOR_PL(pl) {
-        const double v = (TMA && t < lb) ? sm[((long long)s * ELLC + pl) * FT + t] : src[(long long)pl * N + t];
-        w[pl] = fma(coef, v, w[pl]);
+  __syncthreads();
+  double nrm = 0.0;
+  if (warp == FW) {                                 // ---- producer warp
+    if (TMA && lane == 0) {
+      for (int k = 0; k < nitems; ++k) {
+        const int s = k % FS;
+        if (k >= FS) mbar_wait(&empty[s], (uint32_t)(((k / FS) - 1) & 1));
+        bulk_planes(sm + (long long)s * ELLC * FT, FT, src_of(k) + base, N, ell, len, &full[s]);
       }
     }
-    if constexpr (TMA) {
-      __syncthreads();                              // stage s fully consumed
-      if (t == 0 && k + FS < nitems)
-        bulk_planes(sm + (long long)s * ELLC * FT, FT, src_of(k + FS) + base, N, ell, len, &bar[s]);
+  } else {                                          // ---- consumer warps
+    const bool valid = t < len;
+    double w[ELLC];
+    FOR_PL(pl) w[pl] = 0.0;
+    for (int k = 0; k < nitems; ++k) {
+      const int s = k % FS;
+      const double coef = k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1];
+      const double* src = src_of(k) + base;
+      if constexpr (TMA) mbar_wait(&full[s], (uint32_t)((k / FS) & 1));
+      if (valid) {
+        FOR_PL(pl) {
+          const double v = (TMA && t < lb) ? sm[((long long)s * ELLC + pl) * FT + t] : src[(long long)pl * N + t];
+          w[pl] = fma(coef, v, w[pl]);
+        }
+      }
+      if constexpr (TMA) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
     }
-  }
-  double nrm = 0.0;
-  if (valid) {
-    const long long p = base + t;
-    if (j > 0) {
-      double* vj = U.V + (long long)j * L;
-      FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
+    if (valid) {
+      const long long p = base + t;
+      if (j > 0) {
+        double* vj = U.V + (long long)j * L;
+        FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
+      }
+      FOR_PL(pl) nrm = fma(w[pl], w[pl], nrm);
+      dft_store<ELLC>(D, N, p, w, what);
     }
-    FOR_PL(pl) nrm = fma(w[pl], w[pl], nrm);
-    dft_store<ELLC>(D, N, p, w, what);
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[warp] = nrm;
   }
   // ||u||^2: CTA partial, then the last CTA reduces in a fixed order and finalises Arnoldi
   // column j-1 (or beta when j == 0).
-  nrm = warp_sum(nrm);
-  if ((t & 31) == 0) red[t >> 5] = nrm;
   __syncthreads();
   if (t == 0) {
     double tot = 0.0;
-    for (int w2 = 0; w2 < FT / 32; ++w2) tot += red[w2];
+    for (int w2 = 0; w2 < FW; ++w2) tot += red[w2];
     U.part[blockIdx.x] = tot;
     __threadfence();
     const unsigned tk = atomicAdd(&st->tick, 1u);
