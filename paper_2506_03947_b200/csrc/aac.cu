@@ -15,6 +15,7 @@
 #include "krylov.cuh"
 #include "nc.cuh"
 #include "stencil.cuh"
+#include "tsweep.cuh"
 
 // saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
 static int sp_prepare(aac_ctx* ctx, int k);
@@ -264,6 +265,8 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (getenv("AAC_NO_GRAPH")) ctx->use_graphs = false;
+  // temporally blocked sweeps: opt-in (AAC_TSWEEP=1) until they beat the per-step kernel
+  ctx->use_tsweep = getenv("AAC_TSWEEP") != nullptr;
   if (ctx->nranks > 1) ctx->use_graphs = false;
 
   // device allocations
@@ -276,7 +279,7 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   const long long fwd_ctas = (N + 255) / 256 + 1;
   ctx->part_len = std::max<long long>((long long)ctx->ka_grid * 2 * ldh, fwd_ctas);
   ctx->part_len = std::max<long long>(ctx->part_len, 4096);
-  bool ok = alloc(&ctx->d_w, hw.size()) && alloc(&ctx->d_what, L) && alloc(&ctx->d_X, 3 * L) &&
+  bool ok = alloc(&ctx->d_w, hw.size()) && alloc(&ctx->d_what, L) && alloc(&ctx->d_X, 4 * L) &&
             alloc(&ctx->d_tmp, L) && alloc(&ctx->d_V, (long long)(max_krylov + 1) * L) &&
             alloc(&ctx->d_Z, (long long)max_krylov * L) && alloc(&ctx->d_W, L) &&
             alloc(&ctx->d_halo, 2LL * ell * G.S) && alloc(&ctx->d_part, ctx->part_len) &&
@@ -375,8 +378,9 @@ static int launch_matvec(aac_ctx* ctx, const double* x, double* y, double bytes)
   const Geo& g = ctx->geo;
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
+  const dim3 grid(grid1d(g.nx / VEC, 256), g.ny, g.nz);
   LAUNCH(ctx, KID_MATVEC, bytes,
-         k_matvec<DIM, VEC><<<grid1d(g.N / VEC, 256), 256, 0, ctx->stream>>>(g, ctx->ell, x, y, hlo, hhi));
+         k_matvec<DIM, VEC><<<grid, 256, 0, ctx->stream>>>(g, ctx->ell, x, y, hlo, hhi));
   return AAC_OK;
 }
 
@@ -570,6 +574,99 @@ static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
 // Preconditioner: forward DFT (optionally fused with the Arnoldi update), Chebyshev sweeps,
 // last sweep fused with the inverse DFT. gmres_mode: input is the Arnoldi update (W, V, c),
 // output Z_j with j read on the device; otherwise r -> z.
+// Temporally blocked sweeps (tsweep.cuh): passes of up to TS_S global sweeps; every active
+// block advances its steps of the pass inside one CTA tile; the final iterates feed the
+// inverse transform. Slot sets ping-pong between passes: set k = d_X + (2k, 2k+1) * L.
+constexpr int TS_S = 4, TS_TX = 32, TS_TY = 16;
+
+static int tsweep_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long zjs, const IterState* st) {
+  const Geo& g = ctx->geo;
+  const int ell = ctx->ell, h = ell / 2;
+  const long long N = g.N, L = (long long)ell * N;
+  const double V = 8.0 * L, C = 8.0 * ctx->dim * N;
+  const Dft D = make_dft(ctx);
+  struct Src { const double* p; double r, i; };
+  Src cur[AAC_MAX_BLK], prv[AAC_MAX_BLK];
+  for (int kb = 0; kb <= h; ++kb) {
+    const double* wq = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
+    double tr, ti;
+    inv_theta(ctx, kb, &tr, &ti);
+    cur[kb] = {wq, tr, ti};                       // x_1 = w / theta
+    prv[kb] = {wq, 0.0, 0.0};                     // x_0 = 0
+  }
+  using TG = TGeom<TS_S, TS_TX, TS_TY>;
+  const size_t smem = (size_t)TG::NDBL * sizeof(double);
+  AAC_TRY(smem_optin(ctx, k_tsweep<TS_S, TS_TX, TS_TY>, smem));
+  const unsigned ntiles = (unsigned)(((g.nx + TS_TX - 1) / TS_TX) * ((g.ny + TS_TY - 1) / TS_TY));
+  const int pm = P.pmax;
+  int set = 0;
+  for (int t0 = 1; t0 <= pm - 1; t0 += TS_S) {
+    const int t1 = std::min(t0 + TS_S - 1, pm - 1);
+    const bool final_pass = (t1 == pm - 1);
+    TSweep T{};
+    int nb = 0, nplanes = 0, steps = 0;
+    double* outA = ctx->d_X + (long long)(2 * set) * L;
+    double* outB = ctx->d_X + (long long)(2 * set + 1) * L;
+    Src ncur[AAC_MAX_BLK], nprv[AAC_MAX_BLK];
+    for (int kb = 0; kb <= h; ++kb) {
+      ncur[kb] = cur[kb];
+      nprv[kb] = prv[kb];
+      const int off = pm - P.p[kb];
+      const int s_begin = std::max(1, t0 - off), s_end = t1 - off;
+      if (s_end < 1) continue;                     // block not started yet
+      const int ns = s_end - s_begin + 1;
+      const int q = plane_of_block(ell, kb);
+      const bool cplx = (kb != 0 && kb != h);
+      TBlk& B = T.b[nb++];
+      B.cplx = cplx ? 1 : 0;
+      B.q = q;
+      B.ns = ns;
+      B.s0 = s_begin;
+      B.ps = cur[kb].p; B.sr = cur[kb].r; B.si = cur[kb].i;
+      B.pm = prv[kb].p; B.mr = prv[kb].r; B.mi = prv[kb].i;
+      for (int l = 0; l < ns; ++l) {
+        const int s = s_begin + l;
+        B.ar[l] = P.a_re[kb * pm + s]; B.ai[l] = P.a_im[kb * pm + s];
+        B.br[l] = P.b_re[kb * pm + s]; B.bi[l] = P.b_im[kb * pm + s];
+      }
+      shift_of_block(ctx, kb, &B.lr, &B.li);
+      B.out_last = outA + (long long)q * N;
+      ncur[kb] = {B.out_last, 1.0, 0.0};
+      if (final_pass) {
+        B.out_prev = nullptr;
+      } else if (ns == 1 && s_begin == 1) {       // x_{s_end} = x_1 stays virtual
+        B.out_prev = nullptr;
+        nprv[kb] = cur[kb];
+      } else {
+        B.out_prev = outB + (long long)q * N;
+        nprv[kb] = {B.out_prev, 1.0, 0.0};
+      }
+      nplanes += cplx ? 2 : 1;
+      steps += ns * (cplx ? 2 : 1);
+    }
+    if (nb > 0) {
+      // algorithmic bytes: x_s, x_{s-1}, hat w in + up to two iterates out per active plane
+      const double bytes = 8.0 * N * nplanes * (final_pass ? 4.0 : 5.0) + C * nb;
+      LAUNCH(ctx, KID_SWEEP, bytes,
+             (k_tsweep<TS_S, TS_TX, TS_TY><<<dim3(ntiles, nb), 256, smem, ctx->stream>>>(g, T, ctx->d_what, st)));
+      ctx->sweeps += steps;
+    }
+    for (int kb = 0; kb <= h; ++kb) {
+      cur[kb] = ncur[kb];
+      prv[kb] = nprv[kb];
+    }
+    set ^= 1;
+  }
+  NcFinal F{};
+  for (int kb = 0; kb <= h; ++kb) {
+    F.src[kb] = cur[kb].p;
+    F.tr[kb] = cur[kb].r;
+    F.ti[kb] = cur[kb].i;
+  }
+  LAUNCH(ctx, KID_INV, 2 * V, k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  return AAC_OK;
+}
+
 template <int DIM, int VEC>
 static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zbase, bool gmres_mode, int host_j) {
   const Geo& g = ctx->geo;
@@ -594,16 +691,21 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   const long long zjs = gmres_mode ? L : 0;
   if (P.pmax == 1) {
     NcFinal F{};
-    for (int kb = 0; kb <= h; ++kb) inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
+    for (int kb = 0; kb <= h; ++kb) {
+      inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
+      F.src[kb] = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
+    }
     LAUNCH(ctx, KID_INV, 2 * V,
-           k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, ctx->d_what, zbase, zjs, st));
+           k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
     return AAC_OK;
   }
+  if (DIM == 2 && ctx->nranks == 1 && ctx->use_tsweep && (g.nx % 2) == 0)
+    return tsweep_passes(ctx, P, zbase, zjs, st);
   double* X = ctx->d_X;
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * g.S;
-  const unsigned gsw = grid1d(N / VEC, SW_TX);
+  const dim3 gsw(grid1d(g.nx / VEC, SW_TX), g.ny, g.nz);
   for (int t = 1; t < P.pmax; ++t) {
     const bool last = (t == P.pmax - 1);
     NcSweep S{};
@@ -708,7 +810,7 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA>, AT + 32, smem);
     if (occ < 1) occ = 1;
   }
-  const long long ntile = (g.N + AT - 1) / AT;
+  const long long ntile = (long long)((g.nx + AT - 1) / AT) * g.ny * g.nz;
   const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ntile);
   const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
   // algorithmic bytes: Z_j + C in, W out, basis V_0..V_j in
@@ -718,7 +820,7 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
 
 template <int DIM>
 static int arnoldi_dim(aac_ctx* ctx, int host_j) {
-  const bool tma = (ctx->geo.N % 2) == 0;
+  const bool tma = (ctx->geo.nx % 2) == 0;          // row-aligned tiles start at row * nx
   if (ctx->ell <= 10) return tma ? launch_arnoldi<DIM, 10, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false>(ctx, host_j);
   return tma ? launch_arnoldi<DIM, 16, true>(ctx, host_j) : launch_arnoldi<DIM, 16, false>(ctx, host_j);
 }

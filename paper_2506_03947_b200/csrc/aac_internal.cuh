@@ -111,6 +111,7 @@ struct aac_ctx {
   IterState* h_st = nullptr;           // pinned mirror (graph memcpy node target)
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  bool use_tsweep = true;             // temporally blocked sweeps (2D, one rank)
   // plans
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;

@@ -45,10 +45,23 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   for (int k = t; k < AW * nv2; k += blockDim.x) acc[k] = 0.0;
   const long long N = g.N;
-  const long long ntile = (N + AT - 1) / AT;
+  // row-aligned tiles: (row, chunk of AT points within the row) -> no per-point index division
+  const unsigned cpr = (unsigned)((g.nx + AT - 1) / AT), nrow = (unsigned)g.ny * (unsigned)g.nz;
+  const long long ntile = (long long)cpr * nrow;
   const long long my_tiles = blockIdx.x < ntile ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const long long nitems = my_tiles * nv;       // item k -> (tile r = k / nv, basis vector i = k % nv)
-  auto tile_base = [&](long long r) { return (blockIdx.x + r * gridDim.x) * (long long)AT; };
+  struct Tile { long long base; int x0, y, z, len; };
+  auto tile_of = [&](long long r) {
+    const unsigned tix = (unsigned)(blockIdx.x + r * gridDim.x);
+    const unsigned row = tix / cpr, ch = tix - row * cpr;
+    Tile T;
+    T.x0 = (int)(ch * AT);
+    T.y = (int)(row % (unsigned)g.ny);
+    T.z = (int)(row / (unsigned)g.ny);
+    T.base = (long long)row * g.nx + T.x0;
+    T.len = g.nx - T.x0 < AT ? g.nx - T.x0 : AT;
+    return T;
+  };
   if (TMA && t == 0) {
     for (int s = 0; s < AS; ++s) {
       mbar_init(&full[s], 1);
@@ -62,26 +75,25 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
       for (long long k = 0; k < nitems; ++k) {
         const int s = (int)(k % AS);
         if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
-        const long long r = k / nv;
+        const Tile T = tile_of(k / nv);
         const int i = (int)(k % nv);
-        const long long b = tile_base(r);
-        const int len = (int)((N - b) < AT ? (N - b) : AT);
-        bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + b, N, ell, len, &full[s]);
+        bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s]);
       }
     }
   } else {                                      // ---- consumer warps
     const double* z = P.Z + (long long)j * P.L;
     const double* vj = P.V + (long long)j * P.L;
     for (long long r = 0; r < my_tiles; ++r) {
-      const long long b = tile_base(r);
-      const int len = (int)((N - b) < AT ? (N - b) : AT);
+      const Tile T = tile_of(r);
+      const long long b = T.base;
+      const int len = T.len;
       const int lb = len & ~1;
       const bool valid = t < len;
       const long long p = b + t;
       double w[ELLC], u[ELLC];
       if (valid) {
         PtV<DIM, 1> q;
-        load_ptv<DIM, 1>(g, p, q);
+        load_ptv_xyz<DIM, 1>(g, T.x0 + t, T.y, T.z, q);
         // planes in pairs: all loads of a pair are issued before its stores
 #pragma unroll
         for (int g0 = 0; g0 < ELLC; g0 += 2) {

@@ -215,7 +215,7 @@ struct NcSweep {
 constexpr int SW_TX = 64;                 // point groups per CTA along x
 
 template <int DIM, int VEC, bool LAST>
-__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P, Dft D,
+__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, 2) k_sweep(Geo g, NcSweep P, Dft D,
                                                                  const double* __restrict__ what,
                                                                  const double* __restrict__ hlo,
                                                                  const double* __restrict__ hhi,
@@ -228,12 +228,15 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P,
   // LAST: final iterates of all blocks at this CTA's points, then the inverse DFT
   extern __shared__ double ysh[];         // [ell planes][SW_TX*VEC]
   const long long N = g.N;
-  const long long p = ((long long)blockIdx.x * SW_TX + threadIdx.x) * VEC;
+  // grid (x-chunks of SW_TX*VEC points, ny, nz): coordinates without index division
+  const int xx = (blockIdx.x * SW_TX + threadIdx.x) * VEC;
+  const long long row0 = ((long long)blockIdx.z * g.ny + blockIdx.y) * g.nx;
+  const long long p = row0 + xx;
   const NcBlk& B = P.b[threadIdx.y];
   double out_r[VEC], out_i[VEC];
-  if (p < N) {
+  if (xx < g.nx) {
     PtV<DIM, VEC> q;
-    load_ptv<DIM, VEC>(g, p, q);
+    load_ptv_xyz<DIM, VEC>(g, xx, blockIdx.y, blockIdx.z, q);
     const double* wr = what + (long long)B.q * N;
     const double* hl = hlo + B.q * g.S;
     const double* hh = hhi + B.q * g.S;
@@ -288,7 +291,8 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P,
     // passive blocks (p_k == 1): y = w / theta straight from hat w
     const int ell = D.ell, h = ell / 2;
     const int npts = SW_TX * VEC;
-    const long long p0 = (long long)blockIdx.x * npts;
+    const long long p0 = row0 + (long long)blockIdx.x * npts;
+    const int xlim = g.nx - blockIdx.x * npts;       // valid points of this CTA's row chunk
     const int nthr = blockDim.x * blockDim.y;
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     for (int kb = 0; kb <= h; ++kb) {
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P,
       const int qq = plane_of(ell, kb);
       const bool cp = (kb != 0 && kb != h);
       for (int t = tid; t < npts; t += nthr) {
-        if (p0 + t >= N) continue;
+        if (t >= xlim) continue;
         const double a = what[(long long)qq * N + p0 + t];
         const double b = cp ? what[(long long)(qq + 1) * N + p0 + t] : 0.0;
         ysh[qq * npts + t] = a * P.ptr[kb] - b * P.pti[kb];
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P,
     // z_j = ell^{-1/2} gamma_j^{-1} (y_0 + (-1)^j y_{ell/2} + 2 sum_{k=1}^{ell/2-1} Re(y_k e^{2 pi i jk/ell}))
     // thread (x, y) -> its VEC points, output planes j = y, y + nact, ...
     const int tp = threadIdx.x * VEC;
-    if (p0 + tp < N) {
+    if (tp < xlim) {
       for (int jj = threadIdx.y; jj < ell; jj += blockDim.y) {
         double acc[VEC];
 #pragma unroll
@@ -337,13 +341,15 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK) k_sweep(Geo g, NcSweep P,
   }
 }
 
-// P_max == 1 (every block exact at p = 1, e.g. c = 0, or k = 1): z = Gamma^{-1} U (w / theta).
+// Inverse transform from per-block sources: y_k = (tr_k + i ti_k) * src_k (planes of block k),
+// z = Gamma^{-1} U y (real by construction). Used when P_max == 1 (y = w / theta), after the
+// temporally blocked sweeps (y = x_{p_k}, passive blocks w / theta) and by the SP solver.
 struct NcFinal {
+  const double* src[AAC_MAX_BLK];   // first plane of block k in its source array
   double tr[AAC_MAX_BLK], ti[AAC_MAX_BLK];
 };
 
 __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
-                                                 const double* __restrict__ what,
                                                  double* __restrict__ zbase, long long zjs,
                                                  const IterState* st) {
   if (st && st->done) return;
@@ -355,10 +361,9 @@ __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
 #pragma unroll
   for (int kb = 0; kb < AAC_MAX_BLK; ++kb) {
     if (kb > h) break;
-    const int q = plane_of(ell, kb);
     const bool cplx = (kb != 0 && kb != h);
-    const double w0 = what[(long long)q * N + p];
-    const double w1 = cplx ? what[(long long)(q + 1) * N + p] : 0.0;
+    const double w0 = F.src[kb][p];
+    const double w1 = cplx ? F.src[kb][N + p] : 0.0;
     yr[kb] = w0 * F.tr[kb] - w1 * F.ti[kb];
     yi[kb] = cplx ? (w0 * F.ti[kb] + w1 * F.tr[kb]) : 0.0;
   }

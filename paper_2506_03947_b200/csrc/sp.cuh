@@ -712,10 +712,11 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
   for (int kb = 0; kb <= h; ++kb) {
     F.tr[kb] = 1.0;
     F.ti[kb] = 0.0;
+    F.src[kb] = P->X + (long long)(kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1)) * N;
   }
   const Dft D = make_dft(ctx);
   LAUNCH(ctx, KID_INV, 2.0 * V,
-         k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, P->X, zbase, zjs, st));
+         k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
   return AAC_OK;
 }
 

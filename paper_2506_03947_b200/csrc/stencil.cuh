@@ -53,14 +53,16 @@ struct PtV {
   double wym[VEC], wyp[VEC], wzm[VEC], wzp[VEC];
 };
 
+// Face weights of the VEC-point group at (x, y, z) (local slab coordinates).
 template <int DIM, int VEC>
-__device__ __forceinline__ void load_ptv(const Geo& g, long long p, PtV<DIM, VEC>& q) {
-  q.p = p;
-  q.x = (int)(p % g.nx);
-  const long long r = p / g.nx;
-  q.y = (int)(r % g.ny);
-  q.z = (int)(r / g.ny);
-  q.li = p % g.S;
+__device__ __forceinline__ void load_ptv_xyz(const Geo& g, int x, int y, int z, PtV<DIM, VEC>& q) {
+  q.x = x;
+  q.y = y;
+  q.z = z;
+  q.li = (long long)y * g.nx + x;                 // index inside the slab layer (3D); 2D: S = nx
+  if (DIM == 2) q.li = x;
+  q.p = ((long long)z * g.ny + y) * g.nx + x;
+  const long long p = q.p;
   ldv<VEC>(g.wx, p, q.wx);
   q.wx[VEC] = __ldg(g.wx + p + VEC);
   if constexpr (DIM >= 2) {
@@ -71,6 +73,14 @@ __device__ __forceinline__ void load_ptv(const Geo& g, long long p, PtV<DIM, VEC
     ldv<VEC>(g.wz, p, q.wzm);
     ldv<VEC>(g.wz, p + g.S, q.wzp);
   }
+}
+
+// Same from a flat index (32-bit index arithmetic: slabs hold < 2^32 points).
+template <int DIM, int VEC>
+__device__ __forceinline__ void load_ptv(const Geo& g, long long p, PtV<DIM, VEC>& q) {
+  const unsigned pp = (unsigned)p, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
+  const unsigned r = pp / nx;
+  load_ptv_xyz<DIM, VEC>(g, (int)(pp - r * nx), (int)(r % ny), (int)(r / ny), q);
 }
 
 // Neighbour pointers of the VEC-point group for one plane (branch-free: boundary neighbours
@@ -174,10 +184,12 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
                                                 double* __restrict__ y,
                                                 const double* __restrict__ hlo,
                                                 const double* __restrict__ hhi) {
-  const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
-  if (p >= g.N) return;
+  // grid (x-chunks, ny, nz): no index division
+  const int xx = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  if (xx >= g.nx) return;
   PtV<DIM, VEC> q;
-  load_ptv<DIM, VEC>(g, p, q);
+  load_ptv_xyz<DIM, VEC>(g, xx, blockIdx.y, blockIdx.z, q);
+  const long long p = q.p;
   double prev[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) prev[e] = 0.0;
