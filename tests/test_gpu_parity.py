@@ -258,3 +258,20 @@ def test_sp_gmres_parity():
     assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
     assert info["matvecs_paper_units"] == info["iters"] * (p.ell + 2 * (p.ell - 1) * p.k)
     s.close()
+
+
+def test_saddle_full_size_gmres_vs_stored_oracle():
+    """BASELINE configs[3] (SP, k = 8) at N = 1024^2 vs oracle values stored by
+    scripts/make_oracle_golden.py (oracle-only)."""
+    g = json.load(open(os.path.join(HERE, "golden", "oracle_saddle.json")))
+    p = synth.make_problem("saddle")
+    s = _solver(p, max_krylov=40)
+    x, info = s.gmres("sp", p.k, _dev(p.b, p.ell), rtol=p.rtol, maxit=40)
+    assert abs(info["iters"] - g["iters"]) <= 1 and info["converged"] == 1
+    assert info["relres_true"] <= 1.5 * p.rtol
+    xs = x.cpu().numpy().ravel()
+    idx = np.array(g["sample_idx"])
+    ref = np.array(g["sample_x"])
+    assert np.linalg.norm(xs[idx] - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert np.linalg.norm(xs) == pytest.approx(g["x_norm"], rel=1e-9)
+    s.close()
