@@ -766,7 +766,9 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
 
 static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z, bool gmres_mode, int host_j = 0) {
   const NcPlan& P = nc_plan(ctx, method, k);
-  const bool v2 = vec2(ctx);
+  // two points per thread (16-byte loads) when nx is even; AAC_SWEEP_VEC=1 forces one
+  static const bool sweep_v1 = getenv("AAC_SWEEP_VEC") && atoi(getenv("AAC_SWEEP_VEC")) == 1;
+  const bool v2 = vec2(ctx) && !sweep_v1;
   switch (ctx->dim) {
     case 1: return v2 ? nc_apply_t<1, 2>(ctx, P, r, z, gmres_mode, host_j) : nc_apply_t<1, 1>(ctx, P, r, z, gmres_mode, host_j);
     case 2: return v2 ? nc_apply_t<2, 2>(ctx, P, r, z, gmres_mode, host_j) : nc_apply_t<2, 1>(ctx, P, r, z, gmres_mode, host_j);

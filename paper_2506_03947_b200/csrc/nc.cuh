@@ -215,7 +215,7 @@ struct NcSweep {
 constexpr int SW_TX = 64;                 // point groups per CTA along x
 
 template <int DIM, int VEC, bool LAST>
-__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, 2) k_sweep(Geo g, NcSweep P, Dft D,
+__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, LAST ? 2 : 1) k_sweep(Geo g, NcSweep P, Dft D,
                                                                  const double* __restrict__ what,
                                                                  const double* __restrict__ hlo,
                                                                  const double* __restrict__ hhi,
@@ -240,29 +240,34 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, 2) k_sweep(Geo g, NcSweep
     const double* wr = what + (long long)B.q * N;
     const double* hl = hlo + B.q * g.S;
     const double* hh = hhi + B.q * g.S;
+    // all loads of the block first (stencil operands of both planes, x_{s-1}, hat w), then
+    // the arithmetic: the loads are independent and stay in flight together
+    SV<VEC> v0, v1;
+    double m0[VEC], m1[VEC], w0[VEC], w1[VEC];
+    load_sv<DIM, VEC>(g, q, B.ps, hl, hh, v0);
+    ldc<VEC>(B.pm, p, m0);
+    ldv<VEC>(wr, p, w0);
+    if (B.cplx) {
+      load_sv<DIM, VEC>(g, q, B.ps + N, hl + g.S, hh + g.S, v1);
+      ldc<VEC>(B.pm + N, p, m1);
+      ldv<VEC>(wr + N, p, w1);
+    }
+    double a0[VEC], a1[VEC];
+    stencil_sv<DIM, VEC>(q, v0, a0);
     if (!B.cplx) {
-      double a[VEC], c[VEC], m[VEC], w0[VEC];
-      apply_Av<DIM, VEC>(g, q, B.ps, hl, hh, a, c);
-      ldc<VEC>(B.pm, p, m);
-      ldv<VEC>(wr, p, w0);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const double xs = B.sr * c[e], Axs = B.sr * a[e], xm = B.mr * m[e];
+        const double xs = B.sr * v0.c[e], Axs = B.sr * a0[e], xm = B.mr * m0[e];
         const double res = w0[e] - (Axs - B.lr * xs);
         out_r[e] = xs + B.ar * (xs - xm) + B.br * res;
       }
       if (!LAST) stv<VEC>(B.xo, p, out_r);
     } else {
-      double a0[VEC], a1[VEC], c0[VEC], c1[VEC], m0[VEC], m1[VEC], w0[VEC], w1[VEC];
-      apply_Av<DIM, VEC>(g, q, B.ps, hl, hh, a0, c0);
-      apply_Av<DIM, VEC>(g, q, B.ps + N, hl + g.S, hh + g.S, a1, c1);
-      ldc<VEC>(B.pm, p, m0);
-      ldc<VEC>(B.pm + N, p, m1);
-      ldv<VEC>(wr, p, w0);
-      ldv<VEC>(wr + N, p, w1);
+      stencil_sv<DIM, VEC>(q, v1, a1);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const double ur = B.sr * c0[e] - B.si * c1[e], ui = B.sr * c1[e] + B.si * c0[e];
+        const double c0 = v0.c[e], c1 = v1.c[e];
+        const double ur = B.sr * c0 - B.si * c1, ui = B.sr * c1 + B.si * c0;
         const double Aur = B.sr * a0[e] - B.si * a1[e], Aui = B.sr * a1[e] + B.si * a0[e];
         const double mr = B.mr * m0[e] - B.mi * m1[e], mi = B.mr * m1[e] + B.mi * m0[e];
         // residual w - (A - Lambda) x
