@@ -519,6 +519,16 @@ static Dft make_dft(const aac_ctx* ctx) {
   return D;
 }
 
+// z = Gamma^{-1} U y from per-block sources (streaming; one point per thread measured faster
+// than two: the per-block register arrays stay small)
+static int run_inverse(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zbase, long long zjs,
+                       const IterState* st) {
+  const long long N = ctx->geo.N;
+  const double V = 8.0 * ctx->ell * N;
+  LAUNCH(ctx, KID_INV, 2 * V, k_inverse<1><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  return AAC_OK;
+}
+
 #include "sp.cuh"
 
 static inline int plane_of_block(int ell, int kb) {
@@ -663,7 +673,7 @@ static int tsweep_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
     F.tr[kb] = cur[kb].r;
     F.ti[kb] = cur[kb].i;
   }
-  LAUNCH(ctx, KID_INV, 2 * V, k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
   return AAC_OK;
 }
 
@@ -695,8 +705,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
       inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
       F.src[kb] = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
     }
-    LAUNCH(ctx, KID_INV, 2 * V,
-           k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+    AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
     return AAC_OK;
   }
   if (DIM == 2 && ctx->nranks == 1 && ctx->use_tsweep && (g.nx % 2) == 0)
@@ -706,8 +715,12 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * g.S;
   const dim3 gsw(grid1d(g.nx / VEC, SW_TX), g.ny, g.nz);
+  // the last step as a regular sweep writing x_{p_k}, then the streaming inverse transform
+  // (measured faster than the fused k_sweep<LAST>, which stays available: AAC_FUSED_LAST=1)
+  static const bool split_last = getenv("AAC_FUSED_LAST") == nullptr;
+  const double* fin[AAC_MAX_BLK] = {};
   for (int t = 1; t < P.pmax; ++t) {
-    const bool last = (t == P.pmax - 1);
+    const bool last = (t == P.pmax - 1) && !split_last;
     NcSweep S{};
     S.nblk = h + 1;
     const double* planes[AAC_MAX_ELL];
@@ -737,6 +750,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
         else { B.pm = slot(s - 1, q); B.mr = 1.0; B.mi = 0.0; }
       }
       B.xo = last ? nullptr : slot(s + 1, q);
+      fin[kb] = slot(s + 1, q);
       B.ar = P.a_re[kb * P.pmax + s]; B.ai = P.a_im[kb * P.pmax + s];
       B.br = P.b_re[kb * P.pmax + s]; B.bi = P.b_im[kb * P.pmax + s];
       shift_of_block(ctx, kb, &B.lr, &B.li);
@@ -760,6 +774,20 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
              (k_sweep<DIM, VEC, false><<<gsw, blk, 0, ctx->stream>>>(g, S, D, ctx->d_what, hlo, hhi, nullptr, 0, st)));
     }
     ctx->sweeps += nplanes;
+  }
+  if (split_last) {
+    NcFinal F{};
+    for (int kb = 0; kb <= h; ++kb) {
+      if (P.p[kb] == 1) {                              // passive: y = w / theta
+        inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
+        F.src[kb] = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
+      } else {
+        F.tr[kb] = 1.0;
+        F.ti[kb] = 0.0;
+        F.src[kb] = fin[kb];
+      }
+    }
+    AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
   }
   return AAC_OK;
 }

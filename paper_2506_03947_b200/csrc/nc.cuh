@@ -354,36 +354,53 @@ struct NcFinal {
   double tr[AAC_MAX_BLK], ti[AAC_MAX_BLK];
 };
 
+template <int VEC>
 __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
                                                  double* __restrict__ zbase, long long zjs,
                                                  const IterState* st) {
   if (st && st->done) return;
   double* z = zbase + (st ? (long long)st->j * zjs : 0LL);
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (p >= N) return;
   const int ell = D.ell, h = ell / 2;
-  double yr[AAC_MAX_BLK], yi[AAC_MAX_BLK];
+  double yr[AAC_MAX_BLK][VEC], yi[AAC_MAX_BLK][VEC];
+#pragma unroll
+  for (int kb = 0; kb < AAC_MAX_BLK; ++kb) {       // all loads first
+    if (kb > h) break;
+    const bool cplx = (kb != 0 && kb != h);
+    ldc<VEC>(F.src[kb], p, yr[kb]);
+    if (cplx) ldc<VEC>(F.src[kb] + N, p, yi[kb]);
+  }
 #pragma unroll
   for (int kb = 0; kb < AAC_MAX_BLK; ++kb) {
     if (kb > h) break;
     const bool cplx = (kb != 0 && kb != h);
-    const double w0 = F.src[kb][p];
-    const double w1 = cplx ? F.src[kb][N + p] : 0.0;
-    yr[kb] = w0 * F.tr[kb] - w1 * F.ti[kb];
-    yi[kb] = cplx ? (w0 * F.ti[kb] + w1 * F.tr[kb]) : 0.0;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const double w0 = yr[kb][e], w1 = cplx ? yi[kb][e] : 0.0;
+      yr[kb][e] = w0 * F.tr[kb] - w1 * F.ti[kb];
+      yi[kb][e] = cplx ? (w0 * F.ti[kb] + w1 * F.tr[kb]) : 0.0;
+    }
   }
   for (int j = 0; j < ell; ++j) {
-    double acc = 0.0;
+    double acc[VEC], o[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
     int m = j;
 #pragma unroll
     for (int kb = 1; kb < AAC_MAX_BLK; ++kb) {
       if (kb >= h) break;
-      acc = fma(yr[kb], D.c[m], acc);
-      acc = fma(-yi[kb], D.s[m], acc);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        acc[e] = fma(yr[kb][e], D.c[m], acc[e]);
+        acc[e] = fma(-yi[kb][e], D.s[m], acc[e]);
+      }
       m += j;
       if (m >= ell) m -= ell;
     }
-    const double u = yr[0] + ((j & 1) ? -yr[h] : yr[h]) + 2.0 * acc;
-    z[(long long)j * N + p] = D.scale * u * D.gi[j];
+    const double f = D.scale * D.gi[j];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) o[e] = f * (yr[0][e] + ((j & 1) ? -yr[h][e] : yr[h][e]) + 2.0 * acc[e]);
+    stv<VEC>(z + (long long)j * N, p, o);
   }
 }

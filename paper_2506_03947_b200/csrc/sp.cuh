@@ -715,8 +715,7 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     F.src[kb] = P->X + (long long)(kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1)) * N;
   }
   const Dft D = make_dft(ctx);
-  LAUNCH(ctx, KID_INV, 2.0 * V,
-         k_inverse<<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
   return AAC_OK;
 }
 
