@@ -380,7 +380,7 @@ static int launch_matvec(aac_ctx* ctx, const double* x, double* y, double bytes)
   const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
   const dim3 grid(grid1d(g.nx / VEC, 256), g.ny, g.nz);
   LAUNCH(ctx, KID_MATVEC, bytes,
-         k_matvec<DIM, VEC><<<grid, 256, 0, ctx->stream>>>(g, ctx->ell, x, y, hlo, hhi));
+         k_matvec<DIM, VEC><<<grid, 256, 0, ctx->stream>>>(g, ctx->ell, x, 0, nullptr, y, hlo, hhi));
   return AAC_OK;
 }
 
@@ -825,34 +825,54 @@ extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* 
 
 // ------------------------------------------------------------------------------------------
 // GMRES
-template <int DIM, int ELLC, bool TMA>
+template <int DIM, int ELLC, bool TMA, bool FUSED>
 static int launch_arnoldi(aac_ctx* ctx, int host_j) {
   const Geo& g = ctx->geo;
   const int ldh = ctx->max_krylov + 1;
-  KAParams P{ctx->d_Z, ctx->d_V, ctx->d_W, (long long)ctx->ell * g.N, ctx->d_part,
+  const long long L = (long long)ctx->ell * g.N;
+  const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
+  KAParams P{ctx->d_Z, ctx->d_V, ctx->d_W, L, ctx->d_part,
              ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, arnoldi_ctx(ctx)};
+  if (!FUSED) {                      // w = calA Z_j by the stencil kernel (j read on the device)
+    const bool v2 = vec2(ctx);
+    const dim3 gm(grid1d(g.nx / (v2 ? 2 : 1), 256), g.ny, g.nz);
+    const int* jd = reinterpret_cast<const int*>(ctx->d_st);
+    const double* hlo = ctx->d_halo;
+    const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
+    if (v2)
+      LAUNCH(ctx, KID_MATVEC, 2 * V + C, (k_matvec<DIM, 2><<<gm, 256, 0, ctx->stream>>>(g, ctx->ell, ctx->d_Z, L, jd, ctx->d_W, hlo, hhi)));
+    else
+      LAUNCH(ctx, KID_MATVEC, 2 * V + C, (k_matvec<DIM, 1><<<gm, 256, 0, ctx->stream>>>(g, ctx->ell, ctx->d_Z, L, jd, ctx->d_W, hlo, hhi)));
+    ctx->sweeps += ctx->ell;
+  }
   const size_t smem = (arnoldi_ring_doubles<ELLC>() + (size_t)(AW + 1) * 2 * ldh) * sizeof(double);
   // persistent grid: exactly the resident capacity (no partial second wave)
-  static thread_local int occ_cache[2][4][2] = {};
-  int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0];
+  static thread_local int occ_cache[2][4][2][2] = {};
+  int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0][FUSED ? 1 : 0];
   if (!occ) {
-    AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA>, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA>, AT + 32, smem);
+    AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA, FUSED>, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA, FUSED>, AT + 32, smem);
     if (occ < 1) occ = 1;
   }
   const long long ntile = (long long)((g.nx + AT - 1) / AT) * g.ny * g.nz;
   const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ntile);
-  const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
-  // algorithmic bytes: Z_j + C in, W out, basis V_0..V_j in
-  LAUNCH(ctx, KID_ARNOLDI, (host_j + 3) * V + C, (k_arnoldi<DIM, ELLC, TMA><<<grid, AT + 32, smem, ctx->stream>>>(g, ctx->ell, P)));
+  // algorithmic bytes: Z_j + C in (fused) or W in (split), W out (fused), basis V_0..V_j in
+  const double bytes = FUSED ? (host_j + 3) * V + C : (host_j + 2) * V;
+  LAUNCH(ctx, KID_ARNOLDI, bytes, (k_arnoldi<DIM, ELLC, TMA, FUSED><<<grid, AT + 32, smem, ctx->stream>>>(g, ctx->ell, P)));
   return AAC_OK;
 }
 
 template <int DIM>
 static int arnoldi_dim(aac_ctx* ctx, int host_j) {
   const bool tma = (ctx->geo.nx % 2) == 0;          // row-aligned tiles start at row * nx
-  if (ctx->ell <= 10) return tma ? launch_arnoldi<DIM, 10, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false>(ctx, host_j);
-  return tma ? launch_arnoldi<DIM, 16, true>(ctx, host_j) : launch_arnoldi<DIM, 16, false>(ctx, host_j);
+  // split (k_matvec + dot kernel) by default; AAC_FUSED_ARNOLDI=1 keeps the stencil in-kernel
+  static const bool fused = getenv("AAC_FUSED_ARNOLDI") != nullptr;
+  if (ctx->ell <= 10) {
+    if (fused) return tma ? launch_arnoldi<DIM, 10, true, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false, true>(ctx, host_j);
+    return tma ? launch_arnoldi<DIM, 10, true, false>(ctx, host_j) : launch_arnoldi<DIM, 10, false, false>(ctx, host_j);
+  }
+  if (fused) return tma ? launch_arnoldi<DIM, 16, true, true>(ctx, host_j) : launch_arnoldi<DIM, 16, false, true>(ctx, host_j);
+  return tma ? launch_arnoldi<DIM, 16, true, false>(ctx, host_j) : launch_arnoldi<DIM, 16, false, false>(ctx, host_j);
 }
 
 static int arnoldi_impl(aac_ctx* ctx, int host_j) {

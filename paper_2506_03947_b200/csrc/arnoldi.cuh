@@ -31,7 +31,9 @@ __host__ __device__ constexpr size_t arnoldi_ring_doubles() { return (size_t)AS 
 
 // Warp-specialised: warps 0..AW-1 compute (stencil, dots), warp AW streams the basis tiles
 // V_i (i <= j) of every tile through the bulk-copy ring (full / empty mbarriers per stage).
-template <int DIM, int ELLC, bool TMA>
+// FUSED: w = calA Z_j computed here (stencil) and stored; otherwise w is read from W (written
+// by k_matvec just before: one more read of W, but both kernels then run at full occupancy).
+template <int DIM, int ELLC, bool TMA, bool FUSED>
 __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams P) {
   IterState* st = P.ac.st;
   if (st->done) return;
@@ -91,7 +93,13 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
       const bool valid = t < len;
       const long long p = b + t;
       double w[ELLC], u[ELLC];
-      if (valid) {
+      if (valid && !FUSED) {
+        FOR_PL(pl) {
+          w[pl] = P.W[(long long)pl * N + p];
+          u[pl] = vj[(long long)pl * N + p];
+        }
+      }
+      if (valid && FUSED) {
         PtV<DIM, 1> q;
         load_ptv_xyz<DIM, 1>(g, T.x0 + t, T.y, T.z, q);
         // planes in pairs: all loads of a pair are issued before its stores

@@ -179,11 +179,15 @@ __device__ __forceinline__ void apply_Av(const Geo& g, const PtV<DIM, VEC>& q, c
 
 // ------------------------------------------------------------------------------------------
 // y = calA x over all ell planes: y_0 = A x_0, y_j = A x_j - x_{j-1}.
+// x = xbase + j * xjs with j read on the device when st != NULL (GMRES mode: x = Z_j).
 template <int DIM, int VEC>
-__global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __restrict__ x,
+__global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __restrict__ xbase,
+                                                long long xjs, const int* jdev,
                                                 double* __restrict__ y,
                                                 const double* __restrict__ hlo,
                                                 const double* __restrict__ hhi) {
+  if (jdev && jdev[1]) return;                    // IterState {j, done, ...}: done
+  const double* x = xbase + (jdev ? (long long)jdev[0] * xjs : 0LL);
   // grid (x-chunks, ny, nz): no index division
   const int xx = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (xx >= g.nx) return;
@@ -193,14 +197,25 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
   double prev[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) prev[e] = 0.0;
-  for (int j = 0; j < ell; ++j) {
-    double ax[VEC], c[VEC];
-    apply_Av<DIM, VEC>(g, q, x + (long long)j * g.N, hlo + j * g.S, hhi + j * g.S, ax, c);
+  // planes in pairs: the loads of both planes are in flight together
+  for (int j = 0; j < ell; j += 2) {
+    const bool two = j + 1 < ell;
+    SV<VEC> v0, v1;
+    load_sv<DIM, VEC>(g, q, x + (long long)j * g.N, hlo + j * g.S, hhi + j * g.S, v0);
+    if (two) load_sv<DIM, VEC>(g, q, x + (long long)(j + 1) * g.N, hlo + (j + 1) * g.S, hhi + (j + 1) * g.S, v1);
+    double a0[VEC], a1[VEC];
+    stencil_sv<DIM, VEC>(q, v0, a0);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      ax[e] -= prev[e];
-      prev[e] = c[e];
+    for (int e = 0; e < VEC; ++e) a0[e] -= prev[e];
+    stv<VEC>(y + (long long)j * g.N, p, a0);
+    if (two) {
+      stencil_sv<DIM, VEC>(q, v1, a1);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        a1[e] -= v0.c[e];
+        prev[e] = v1.c[e];
+      }
+      stv<VEC>(y + (long long)(j + 1) * g.N, p, a1);
     }
-    stv<VEC>(y + (long long)j * g.N, p, ax);
   }
 }
