@@ -14,6 +14,7 @@
 #include "comm.cuh"
 #include "krylov.cuh"
 #include "nc.cuh"
+#include "wave.cuh"
 #include "stencil.cuh"
 #include "tsweep.cuh"
 
@@ -267,6 +268,9 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   if (getenv("AAC_NO_GRAPH")) ctx->use_graphs = false;
   // temporally blocked sweeps: opt-in (AAC_TSWEEP=1) until they beat the per-step kernel
   ctx->use_tsweep = getenv("AAC_TSWEEP") != nullptr;
+  // wavefront temporal blocking (2D, one rank): depth 8 by default, AAC_WAVE_H=0 disables
+  ctx->wave_h = getenv("AAC_WAVE_H") ? atoi(getenv("AAC_WAVE_H")) : 8;
+  if (ctx->wave_h != 0 && ctx->wave_h != 4) ctx->wave_h = 8;
   if (ctx->nranks > 1) ctx->use_graphs = false;
 
   // device allocations
@@ -555,10 +559,19 @@ static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
 
 // ------------------------------------------------------------------------------------------
 // Dynamic shared memory beyond 48 KB needs an explicit opt-in per kernel.
+// The opt-in is per kernel and process-wide: raise it whenever a launch needs more than any
+// earlier one (contexts with a larger max_krylov need more shared memory in k_arnoldi).
 template <typename K>
 static int smem_optin(aac_ctx* ctx, K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
-    CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  static thread_local std::vector<std::pair<const void*, size_t>> done;
+  if (bytes <= 48 * 1024) return AAC_OK;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  for (auto& d : done)
+    if (d.first == key && d.second >= bytes) return AAC_OK;
+  CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  for (auto& d : done)
+    if (d.first == key) { d.second = bytes; return AAC_OK; }
+  done.emplace_back(key, bytes);
   return AAC_OK;
 }
 
@@ -677,6 +690,97 @@ static int tsweep_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   return AAC_OK;
 }
 
+// Wavefront passes (wave.cuh, 2D, one rank): each pass advances every block still running
+// by up to H steps in one read of its inputs; passes ping-pong between the iterate slot sets
+// d_X + (2k, 2k+1) * L; the final iterates feed the streaming inverse transform.
+template <int H, int NT>
+static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long zjs, const IterState* st) {
+  using WG = WGeom<H, NT>;
+  const Geo& g = ctx->geo;
+  const int ell = ctx->ell, h = ell / 2;
+  const long long N = g.N, L = (long long)ell * N;
+  const double C = 8.0 * ctx->dim * N;
+  const Dft D = make_dft(ctx);
+  AAC_TRY(smem_optin(ctx, k_wave<H, NT>, WG::SMEM));
+  const int nstrip = (g.nx + WG::TX - 1) / WG::TX;
+  // rows per chunk: about two CTAs per resident slot, but at least 8 H rows per chunk
+  const int ly_env = getenv("AAC_WAVE_LY") ? atoi(getenv("AAC_WAVE_LY")) : 0;
+  int nb_act = 0;
+  for (int kb = 0; kb <= h; ++kb) nb_act += P.p[kb] > 1;
+  int ly = ly_env;
+  if (ly <= 0) {
+    const long long slots = (H > 4 ? 2LL : 3LL) * ctx->num_sms;
+    const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb_act));
+    ly = (int)std::max<long long>(8LL * H, (g.ny + want - 1) / want);
+  }
+  ly = std::min(ly, g.ny);
+  const int nchunk = (g.ny + ly - 1) / ly;
+  const double* fin[AAC_MAX_BLK] = {};
+  const int steps_max = P.pmax - 1;
+  for (int pass = 0; pass * H < steps_max; ++pass) {
+    const int s0 = 1 + pass * H;
+    const int set = pass & 1, prev_set = set ^ 1;
+    WSweep S{};
+    S.nstrip = nstrip;
+    S.ly = ly;
+    int nb = 0;
+    double passes = 0.0;
+    for (int kb = 0; kb <= h; ++kb) {
+      const int steps = P.p[kb] - 1;
+      if (steps < s0) continue;                       // finished (or passive)
+      const int ns = std::min(H, steps - s0 + 1);
+      const bool cplx = (kb != 0 && kb != h);
+      const int q = plane_of_block(ell, kb);
+      WBlk& B = S.b[nb++];
+      B.q = q;
+      B.np = cplx ? 2 : 1;
+      B.ns = ns;
+      B.virt = pass == 0;
+      if (pass == 0) {
+        inv_theta(ctx, kb, &B.sr, &B.si);
+        B.ps = B.pm = ctx->d_what + (long long)q * N;
+        B.mr = B.mi = 0.0;
+      } else {
+        B.ps = ctx->d_X + (long long)(2 * prev_set) * L + (long long)q * N;
+        B.pm = ctx->d_X + (long long)(2 * prev_set + 1) * L + (long long)q * N;
+        B.sr = 1.0; B.si = 0.0; B.mr = 1.0; B.mi = 0.0;
+      }
+      const bool final_pass = s0 + ns - 1 == steps;
+      B.out_last = ctx->d_X + (long long)(2 * set) * L + (long long)q * N;
+      B.out_prev = final_pass ? nullptr : ctx->d_X + (long long)(2 * set + 1) * L + (long long)q * N;
+      if (final_pass) fin[kb] = B.out_last;
+      for (int l = 0; l < ns; ++l) {
+        const int s = s0 + l;
+        B.ar[l] = P.a_re[kb * P.pmax + s]; B.ai[l] = P.a_im[kb * P.pmax + s];
+        B.br[l] = P.b_re[kb * P.pmax + s]; B.bi[l] = P.b_im[kb * P.pmax + s];
+      }
+      shift_of_block(ctx, kb, &B.lr, &B.li);
+      passes += B.np * ((pass == 0 ? 1.0 : 3.0) + (final_pass ? 1.0 : 2.0));
+      ctx->sweeps += (long long)ns * B.np;
+    }
+    if (nb == 0) break;
+    LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
+           (k_wave<H, NT><<<dim3(nstrip * nchunk, nb), NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
+  }
+  NcFinal F{};
+  for (int kb = 0; kb <= h; ++kb) {
+    if (P.p[kb] == 1) {                                // passive: y = w / theta
+      inv_theta(ctx, kb, &F.tr[kb], &F.ti[kb]);
+      F.src[kb] = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
+    } else {
+      F.tr[kb] = 1.0;
+      F.ti[kb] = 0.0;
+      F.src[kb] = fin[kb];
+    }
+  }
+  return run_inverse(ctx, D, F, zbase, zjs, st);
+}
+
+static int wave_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long zjs, const IterState* st) {
+  if (ctx->wave_h == 4) return wave_passes_t<4, 128>(ctx, P, zbase, zjs, st);
+  return wave_passes_t<8, 128>(ctx, P, zbase, zjs, st);
+}
+
 template <int DIM, int VEC>
 static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zbase, bool gmres_mode, int host_j) {
   const Geo& g = ctx->geo;
@@ -686,8 +790,8 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   const Dft D = make_dft(ctx);
   const IterState* st = gmres_mode ? ctx->d_st : nullptr;
   if (gmres_mode) {
-    // algorithmic bytes: W + V_0..V_{j-1} in, V_j and hat w out
-    AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
+    // algorithmic bytes: W + V_0..V_{j-1} in, V_j and hat w out (j = 0: V_0 in, hat w out)
+    AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
     if (ctx->nranks > 1) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
@@ -708,6 +812,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
     AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
     return AAC_OK;
   }
+  if (DIM == 2 && ctx->nranks == 1 && ctx->wave_h > 0) return wave_passes(ctx, P, zbase, zjs, st);
   if (DIM == 2 && ctx->nranks == 1 && ctx->use_tsweep && (g.nx % 2) == 0)
     return tsweep_passes(ctx, P, zbase, zjs, st);
   double* X = ctx->d_X;
@@ -725,6 +830,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
     S.nblk = h + 1;
     const double* planes[AAC_MAX_ELL];
     int qs[AAC_MAX_ELL], nh = 0, nplanes = 0;
+    double passes = 0.0;             // compulsory plane passes (virtual x_1 = w/theta, x_0 = 0 read nothing)
     for (int kb = 0; kb <= h; ++kb) {
       const int s = t - (P.pmax - P.p[kb]);          // aligned ends: block starts late
       const bool cplx = (kb != 0 && kb != h);
@@ -760,16 +866,17 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
         qs[nh++] = q + e;
       }
       nplanes += np;
+      passes += np * ((s == 1 ? 1.0 : s == 2 ? 2.0 : 3.0) + (last ? 0.0 : 1.0));
     }
     AAC_TRY(comm_halo(ctx, planes, qs, nh));
     const dim3 blk(SW_TX, S.nact);
     if (last) {
       const size_t smem = (size_t)ell * SW_TX * VEC * sizeof(double);
-      const double bytes = 8.0 * N * 3.0 * nplanes + C + V;     // x_s, x_{s-1}, w in; z out
+      const double bytes = 8.0 * N * passes + C + V;           // x_s, x_{s-1}, w in; z out
       LAUNCH(ctx, KID_INV, bytes,
              (k_sweep<DIM, VEC, true><<<gsw, blk, smem, ctx->stream>>>(g, S, D, ctx->d_what, hlo, hhi, zbase, zjs, st)));
     } else {
-      const double bytes = 8.0 * N * 4.0 * nplanes + C;
+      const double bytes = 8.0 * N * passes + C;
       LAUNCH(ctx, KID_SWEEP, bytes,
              (k_sweep<DIM, VEC, false><<<gsw, blk, 0, ctx->stream>>>(g, S, D, ctx->d_what, hlo, hhi, nullptr, 0, st)));
     }
@@ -849,8 +956,8 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
   // persistent grid: exactly the resident capacity (no partial second wave)
   static thread_local int occ_cache[2][4][2][2] = {};
   int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0][FUSED ? 1 : 0];
+  AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA, FUSED>, smem));
   if (!occ) {
-    AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA, FUSED>, smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA, FUSED>, AT + 32, smem);
     if (occ < 1) occ = 1;
   }

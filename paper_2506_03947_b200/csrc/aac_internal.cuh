@@ -112,6 +112,7 @@ struct aac_ctx {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   bool use_tsweep = true;             // temporally blocked sweeps (2D, one rank)
+  int wave_h = 8;                      // wavefront depth (wave.cuh; 0 = per-step sweeps)
   // plans
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;

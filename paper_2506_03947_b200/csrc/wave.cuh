@@ -1,0 +1,270 @@
+// wave.cuh -- temporally blocked Chebyshev solves for 2D grids: a y-wavefront over all steps.
+//
+// The block problems (A - Lambda_k) y_k = w_k (PAPER.md:266-275 Eq. eq:blockproblem) are
+// independent after the forward transform, and the Chebyshev recurrence of reading R8
+//   x_0 = 0, x_1 = w/theta, x_{s+1} = x_s + a_s (x_s - x_{s-1}) + b_s (w - (A - Lambda) x_s)
+// only couples a point to its 5-point neighbourhood from one step to the next. So the whole
+// solve of one block (p_k - 1 stencil steps) can run in ONE pass over HBM: read w, write
+// x_{p_k}, instead of 4 plane-passes per step (k_sweep).
+//
+// Organisation (one CTA = one packed block x one strip of columns x one chunk of rows):
+//  * thread t owns column x = x0 - H + t of the strip (NT columns = TX interior + 2H halo);
+//  * the CTA marches down the rows: at step tau it loads row tau of w (level L_1 = x_{s0}
+//    enters at row tau) and computes level L_{i+1} at row tau - i for i = 1..ns (a skewed
+//    wavefront: L_{i+1}(r) needs L_i at rows r-1, r, r+1 and L_{i-1}(r), all computed by the
+//    same thread in this or an earlier step);
+//  * the y-neighbours live in per-thread register rings (3 rows per level), the x-neighbours
+//    come from the two adjacent threads through a double-buffered shared-memory exchange of
+//    the previous step's rows (one __syncthreads per row);
+//  * w rows are kept in a per-thread shared-memory history (H+1 rows), face weights are
+//    read from L1/L2.
+// Halo columns (H per side) and the warm-up rows of a chunk are computed redundantly and
+// discarded; values outside the domain are zero and carry zero face weights (Neumann), so
+// they never reach an in-domain point. Passes of up to H steps chain through ping-pong
+// iterate buffers when p_k - 1 > H.
+#pragma once
+
+#include "nc.cuh"
+
+constexpr int WAVE_MAXH = 8;
+
+struct WBlk {
+  int q, np, ns;             // first plane, planes (1 real | 2 complex), steps this pass (1..H)
+  int virt;                  // 1: first pass, x_0 = 0 and x_1 = w/theta (sr, si) from w itself
+  const double* ps;          // x_{s0}   plane q (virt == 0), scaled by (sr, si)
+  const double* pm;          // x_{s0-1} plane q (virt == 0), scaled by (mr, mi)
+  double sr, si, mr, mi;
+  double* out_last;          // x_{s0+ns}   plane q
+  double* out_prev;          // x_{s0+ns-1} plane q, or NULL (final pass)
+  double lr, li;             // Lambda_k
+  double ar[WAVE_MAXH], ai[WAVE_MAXH], br[WAVE_MAXH], bi[WAVE_MAXH];   // steps s0 .. s0+ns-1
+};
+struct WSweep {
+  WBlk b[AAC_MAX_BLK];
+  int nstrip, ly;            // strips of TX columns, rows per chunk
+};
+
+template <int H, int NT>
+struct WGeom {
+  static constexpr int TX = NT - 2 * H;                 // interior columns per strip
+  static constexpr int NSLOT = H + 2;                   // history rows (ages 0 .. H+1)
+  static constexpr int XW = NT + 2;                     // exchange row: zero pad at both ends
+  static constexpr int XCH = 2 * H * 2 * XW;            // [2 buffers][H levels][2 planes][XW]
+  static constexpr int HIST = NSLOT * 5 * NT;           // [slot][w_re, w_im, wxl, wxh, wyl][NT]
+  static constexpr size_t SMEM = (size_t)(XCH + HIST) * sizeof(double);
+};
+
+// Per-thread state of one block's wavefront. Register rings use 3 slots per level; at a step
+// of phase PH (tau mod 3) the newest row is written to slot PH, so after that step's push the
+// ages 0, 1, 2 sit in slots PH, PH+2, PH+1 (mod 3): no register moves.
+template <int NS>
+struct WState {
+  double L[NS + 1][3][2];          // L[0] = x_{s0-1}, L[i] = L_i (i = 1..NS): [slot][plane]
+};
+
+template <int H, int NT>
+struct WCtx {                      // per-CTA constants
+  const WBlk* B;
+  const double* what;
+  Geo g;
+  double* xch;
+  double* hist;                    // this thread's column of the history
+  int t, x, y0, y1;
+  bool colin, colout;
+};
+
+struct WRow { double w0, w1, s0, s1, m0, m1, fxl, fxh, fyl; };
+
+template <int H, int NT, bool CPLX>
+__device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow& R) {
+  R.w0 = R.w1 = R.s0 = R.s1 = R.m0 = R.m1 = R.fxl = R.fxh = R.fyl = 0.0;
+  const Geo& g = C.g;
+  if (C.colin && r >= 0 && r < g.ny) {
+    const long long p = (long long)r * g.nx + C.x;
+    const double* wq = C.what + (long long)C.B->q * g.N + p;
+    R.w0 = __ldg(wq);
+    if (CPLX) R.w1 = __ldg(wq + g.N);
+    R.fxl = __ldg(g.wx + p);
+    R.fxh = __ldg(g.wx + p + 1);
+    R.fyl = __ldg(g.wy + p);
+    if (!C.B->virt) {
+      R.s0 = C.B->ps[p];
+      R.m0 = C.B->pm[p];
+      if (CPLX) {
+        R.s1 = C.B->ps[g.N + p];
+        R.m1 = C.B->pm[g.N + p];
+      }
+    }
+  } else if (C.colin && r == g.ny) {
+    R.fyl = __ldg(g.wy + (long long)r * g.nx + C.x);   // upper face of the last row (0 or halo)
+  }
+}
+
+template <int H, int NT, int NS, bool CPLX, int PH>
+__device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<NS>& S, int tau, int slot,
+                                          WRow& nxt, int tau1) {
+  using G = WGeom<H, NT>;
+  constexpr int A0 = PH, A1 = (PH + 2) % 3, A2 = (PH + 1) % 3;   // ages after this step's push
+  const WBlk& B = *C.B;
+  const int t = C.t;
+  double* xb = C.xch + (tau & 1) * (H * 2 * G::XW) + 1 + t;
+  // (1) publish the newest row of every level (L_i at row tau - i; slot A1 before the push)
+#pragma unroll
+  for (int i = 1; i <= NS; ++i) {
+    xb[((i - 1) * 2 + 0) * G::XW] = S.L[i][A1][0];
+    if (CPLX) xb[((i - 1) * 2 + 1) * G::XW] = S.L[i][A1][1];
+  }
+  // (2) row tau enters: history, L_0, L_1; prefetch row tau + 1
+  const WRow cur = nxt;
+  if (tau + 1 < tau1) wave_load_row<H, NT, CPLX>(C, tau + 1, nxt);
+  {
+    double* hs = C.hist + slot * (5 * NT);
+    hs[0] = cur.w0;
+    if (CPLX) hs[NT] = cur.w1;
+    hs[2 * NT] = cur.fxl;
+    hs[3 * NT] = cur.fxh;
+    hs[4 * NT] = cur.fyl;
+  }
+  if (B.virt) {
+    S.L[0][A0][0] = 0.0;
+    S.L[0][A0][1] = 0.0;
+    S.L[1][A0][0] = B.sr * cur.w0 - B.si * cur.w1;
+    S.L[1][A0][1] = B.sr * cur.w1 + B.si * cur.w0;
+  } else {
+    S.L[1][A0][0] = B.sr * cur.s0 - B.si * cur.s1;
+    S.L[1][A0][1] = B.sr * cur.s1 + B.si * cur.s0;
+    S.L[0][A0][0] = B.mr * cur.m0 - B.mi * cur.m1;
+    S.L[0][A0][1] = B.mr * cur.m1 + B.mi * cur.m0;
+  }
+  __syncthreads();
+  // (3) levels: L_{i+1} at row r = tau - i
+  const double lr = B.lr, li = B.li;
+#pragma unroll
+  for (int i = 1; i <= NS; ++i) {
+    int sl = slot - i;                                  // history slot of row r
+    sl += sl < 0 ? G::NSLOT : 0;
+    const int su = sl + 1 == G::NSLOT ? 0 : sl + 1;     // row r + 1 (upper face)
+    const double* hr = C.hist + sl * (5 * NT);
+    const double fxl = hr[2 * NT], fxh = hr[3 * NT], fyl = hr[4 * NT];
+    const double fyh = C.hist[su * (5 * NT) + 4 * NT];
+    const double w0 = hr[0];
+    const double* xl = xb + ((i - 1) * 2) * G::XW;
+    // everything except the y+1 neighbour (L_i at row r + 1, computed just before in this
+    // step) is folded first; the serial chain through the levels is 4 operations deep:
+    //   x_new = c + a (c - m) + b (w - (A - Lambda) c) = Q - b Ap,  Ap = fyh (c - dn) + Bp.
+    const double c0 = S.L[i][A1][0];
+    const double B0 = fma(fyl, c0 - S.L[i][A2][0], fma(fxh, c0 - xl[1], fma(fxl, c0 - xl[-1], c0)));
+    const double m0 = i == 1 ? S.L[0][A1][0] : S.L[i - 1][A2][0];
+    const double ar = B.ar[i - 1], br = B.br[i - 1];
+    double o0, o1 = 0.0;
+    if (CPLX) {
+      const double w1 = hr[NT];
+      const double c1 = S.L[i][A1][1];
+      const double B1 = fma(fyl, c1 - S.L[i][A2][1],
+                            fma(fxh, c1 - xl[G::XW + 1], fma(fxl, c1 - xl[G::XW - 1], c1)));
+      const double m1 = i == 1 ? S.L[0][A1][1] : S.L[i - 1][A2][1];
+      const double ai = B.ai[i - 1], bi = B.bi[i - 1];
+      const double P0 = fma(-li, c1, fma(lr, c0, w0));      // w + Lambda c (r = P - Ap)
+      const double P1 = fma(li, c0, fma(lr, c1, w1));
+      const double dr = c0 - m0, di = c1 - m1;
+      const double X0 = fma(-ai, di, fma(ar, dr, c0));
+      const double X1 = fma(ai, dr, fma(ar, di, c1));
+      const double Q0 = fma(-bi, P1, fma(br, P0, X0));
+      const double Q1 = fma(bi, P0, fma(br, P1, X1));
+      const double Ap0 = fma(fyh, c0 - S.L[i][A0][0], B0);
+      const double Ap1 = fma(fyh, c1 - S.L[i][A0][1], B1);
+      o0 = fma(bi, Ap1, fma(-br, Ap0, Q0));
+      o1 = fma(-bi, Ap0, fma(-br, Ap1, Q1));
+    } else {
+      const double P0 = fma(lr, c0, w0);
+      const double Q0 = fma(br, P0, fma(ar, c0 - m0, c0));
+      const double Ap0 = fma(fyh, c0 - S.L[i][A0][0], B0);
+      o0 = fma(-br, Ap0, Q0);
+    }
+    if (i == NS) {
+      const int r = tau - i;
+      if (C.colout && r >= C.y0 && r < C.y1) {
+        const long long p = (long long)r * C.g.nx + C.x;
+        B.out_last[p] = o0;
+        if (CPLX) B.out_last[C.g.N + p] = o1;
+        if (B.out_prev) {                                // L_NS at row r (age 1)
+          B.out_prev[p] = S.L[i][A1][0];
+          if (CPLX) B.out_prev[C.g.N + p] = S.L[i][A1][1];
+        }
+      }
+    } else {
+      S.L[i + 1][A0][0] = o0;
+      S.L[i + 1][A0][1] = o1;
+    }
+  }
+}
+
+template <int H, int NT, int NS, bool CPLX>
+__device__ __forceinline__ void wave_block(const WCtx<H, NT>& C) {
+  using G = WGeom<H, NT>;
+  WState<NS> S;
+#pragma unroll
+  for (int i = 0; i <= NS; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) S.L[i][a][0] = S.L[i][a][1] = 0.0;
+  const int tau0 = C.y0 - NS, tau1 = C.y1 + NS;         // L_1 rows tau0 .. tau1-1
+  WRow nxt;
+  wave_load_row<H, NT, CPLX>(C, tau0, nxt);
+  int slot = (tau0 % G::NSLOT + G::NSLOT) % G::NSLOT;   // history slot of row tau
+  // tau0 = y0 - NS with y0 a multiple of ly: start the phase at tau0 mod 3 by peeling
+  int tau = tau0;
+  const int ph0 = ((tau0 % 3) + 3) % 3;
+  auto adv = [&]() { slot = slot + 1 == G::NSLOT ? 0 : slot + 1; ++tau; };
+  if (ph0 == 1) {
+    wave_step<H, NT, NS, CPLX, 1>(C, S, tau, slot, nxt, tau1); adv();
+    if (tau < tau1) { wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv(); }
+  } else if (ph0 == 2) {
+    wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv();
+  }
+  while (tau < tau1) {
+    wave_step<H, NT, NS, CPLX, 0>(C, S, tau, slot, nxt, tau1); adv();
+    if (tau >= tau1) break;
+    wave_step<H, NT, NS, CPLX, 1>(C, S, tau, slot, nxt, tau1); adv();
+    if (tau >= tau1) break;
+    wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv();
+  }
+}
+
+template <int H, int NT, int NS>
+__device__ __forceinline__ void wave_dispatch_ns(const WCtx<H, NT>& C, int ns, bool cplx) {
+  if constexpr (NS >= 1) {
+    if (ns == NS) {
+      if (cplx) wave_block<H, NT, NS, true>(C);
+      else wave_block<H, NT, NS, false>(C);
+      return;
+    }
+    wave_dispatch_ns<H, NT, NS - 1>(C, ns, cplx);
+  }
+}
+
+template <int H, int NT>
+__global__ void __launch_bounds__(NT, H > 4 ? 2 : 3) k_wave(Geo g, WSweep W, const double* __restrict__ what,
+                                                            const IterState* st) {
+  using G = WGeom<H, NT>;
+  if (st && st->done) return;
+  extern __shared__ __align__(16) double wsm[];
+  WCtx<H, NT> C;
+  C.B = &W.b[blockIdx.y];
+  C.what = what;
+  C.g = g;
+  C.xch = wsm;
+  C.hist = wsm + G::XCH + threadIdx.x;
+  C.t = threadIdx.x;
+  const int strip = blockIdx.x % W.nstrip, chunk = blockIdx.x / W.nstrip;
+  C.x = strip * G::TX - H + C.t;
+  C.colin = C.x >= 0 && C.x < g.nx;
+  C.colout = C.t >= H && C.t < NT - H && C.x < g.nx;
+  C.y0 = chunk * W.ly;
+  C.y1 = min(C.y0 + W.ly, g.ny);
+  // zero pads of the exchange rows (never written)
+  for (int k = threadIdx.x; k < 2 * H * 2; k += NT) {
+    wsm[k * G::XW] = 0.0;
+    wsm[k * G::XW + G::XW - 1] = 0.0;
+  }
+  wave_dispatch_ns<H, NT, H>(C, C.B->ns, C.B->np == 2);
+}

@@ -19,12 +19,13 @@ nsol = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 p = synth.make_problem(name)
 method = sys.argv[3] if len(sys.argv) > 3 else p.method
 k = int(sys.argv[4]) if len(sys.argv) > 4 else p.k
-s = from_problem(p, max_krylov=60)
+maxk = int(os.environ.get("AAC_MAXK", "20" if p.dim == 3 else "60"))
+s = from_problem(p, max_krylov=maxk)
 b = torch.from_numpy(p.b.reshape(p.ell, -1)).cuda()
 for i in range(nsol):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    x, info = s.gmres(method, k, b, rtol=p.rtol, maxit=60)
+    x, info = s.gmres(method, k, b, rtol=p.rtol, maxit=maxk)
     torch.cuda.synchronize()
     print(f"solve {i}: {info['iters']} its, {1e3 * (time.perf_counter() - t0):.2f} ms, "
           f"relres_true {info['relres_true']:.2e}")

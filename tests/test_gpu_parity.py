@@ -275,3 +275,35 @@ def test_saddle_full_size_gmres_vs_stored_oracle():
     assert np.linalg.norm(xs[idx] - ref) <= 1e-9 * np.linalg.norm(ref)
     assert np.linalg.norm(xs) == pytest.approx(g["x_norm"], rel=1e-9)
     s.close()
+
+
+# ---------------------------------------------------------------- NC sweep organisations
+# The 2D single-rank NC path runs the wavefront kernel (wave.cuh) by default; depth 4, the
+# per-step sweeps (AAC_WAVE_H=0) and small row chunks (AAC_WAVE_LY) must all match the oracle.
+WAVE = [
+    (dict(shape=(1, 173, 251)), "nc2", 8, "8", "16"),       # 3 strips, 11 chunks, ragged tails
+    (dict(shape=(1, 173, 251)), "nc2", 8, "4", "24"),       # two passes per block
+    (dict(shape=(1, 173, 251)), "nc2", 8, "0", "0"),        # per-step k_sweep
+    (dict(shape=(1, 61, 230)), "nc1", 20, "8", "9"),        # 3 passes, chunks shorter than H+1
+    (dict(shape=(1, 61, 230)), "nc1", 20, "4", "0"),
+    (dict(shape=(1, 5, 3)), "nc2", 8, "8", "0"),            # grid smaller than the halo
+]
+
+
+@pytest.mark.parametrize("kw,method,k,h,ly", WAVE)
+def test_precond_sweep_organisations(monkeypatch, kw, method, k, h, ly):
+    monkeypatch.setenv("AAC_WAVE_H", h)
+    monkeypatch.setenv("AAC_WAVE_LY", ly)
+    p = synth.make_problem("headline", **kw)
+    s = _solver(p)
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    r = np.random.default_rng(9).standard_normal((p.ell,) + p.shape)
+    z = s.precond_apply(method, k, _dev(r, p.ell)).cpu().numpy()
+    assert _rel(z, ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)) <= 1e-12
+    x, info = s.gmres(method, k, _dev(p.b, p.ell), rtol=p.rtol, maxit=60)
+    ro = _oracle_gmres(p, method, k, 60)
+    assert abs(info["iters"] - ro.iters) <= 1
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    s.close()
