@@ -16,7 +16,6 @@
 #include "nc.cuh"
 #include "wave.cuh"
 #include "stencil.cuh"
-#include "tsweep.cuh"
 
 // saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
 static int sp_prepare(aac_ctx* ctx, int k);
@@ -266,8 +265,6 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (getenv("AAC_NO_GRAPH")) ctx->use_graphs = false;
-  // temporally blocked sweeps: opt-in (AAC_TSWEEP=1) until they beat the per-step kernel
-  ctx->use_tsweep = getenv("AAC_TSWEEP") != nullptr;
   // wavefront temporal blocking (2D, one rank): depth 8 by default, AAC_WAVE_H=0 disables
   ctx->wave_h = getenv("AAC_WAVE_H") ? atoi(getenv("AAC_WAVE_H")) : 8;
   if (ctx->wave_h != 0 && ctx->wave_h != 4) ctx->wave_h = 8;
@@ -597,99 +594,6 @@ static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
 // Preconditioner: forward DFT (optionally fused with the Arnoldi update), Chebyshev sweeps,
 // last sweep fused with the inverse DFT. gmres_mode: input is the Arnoldi update (W, V, c),
 // output Z_j with j read on the device; otherwise r -> z.
-// Temporally blocked sweeps (tsweep.cuh): passes of up to TS_S global sweeps; every active
-// block advances its steps of the pass inside one CTA tile; the final iterates feed the
-// inverse transform. Slot sets ping-pong between passes: set k = d_X + (2k, 2k+1) * L.
-constexpr int TS_S = 4, TS_TX = 32, TS_TY = 16;
-
-static int tsweep_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long zjs, const IterState* st) {
-  const Geo& g = ctx->geo;
-  const int ell = ctx->ell, h = ell / 2;
-  const long long N = g.N, L = (long long)ell * N;
-  const double V = 8.0 * L, C = 8.0 * ctx->dim * N;
-  const Dft D = make_dft(ctx);
-  struct Src { const double* p; double r, i; };
-  Src cur[AAC_MAX_BLK], prv[AAC_MAX_BLK];
-  for (int kb = 0; kb <= h; ++kb) {
-    const double* wq = ctx->d_what + (long long)plane_of_block(ell, kb) * N;
-    double tr, ti;
-    inv_theta(ctx, kb, &tr, &ti);
-    cur[kb] = {wq, tr, ti};                       // x_1 = w / theta
-    prv[kb] = {wq, 0.0, 0.0};                     // x_0 = 0
-  }
-  using TG = TGeom<TS_S, TS_TX, TS_TY>;
-  const size_t smem = (size_t)TG::NDBL * sizeof(double);
-  AAC_TRY(smem_optin(ctx, k_tsweep<TS_S, TS_TX, TS_TY>, smem));
-  const unsigned ntiles = (unsigned)(((g.nx + TS_TX - 1) / TS_TX) * ((g.ny + TS_TY - 1) / TS_TY));
-  const int pm = P.pmax;
-  int set = 0;
-  for (int t0 = 1; t0 <= pm - 1; t0 += TS_S) {
-    const int t1 = std::min(t0 + TS_S - 1, pm - 1);
-    const bool final_pass = (t1 == pm - 1);
-    TSweep T{};
-    int nb = 0, nplanes = 0, steps = 0;
-    double* outA = ctx->d_X + (long long)(2 * set) * L;
-    double* outB = ctx->d_X + (long long)(2 * set + 1) * L;
-    Src ncur[AAC_MAX_BLK], nprv[AAC_MAX_BLK];
-    for (int kb = 0; kb <= h; ++kb) {
-      ncur[kb] = cur[kb];
-      nprv[kb] = prv[kb];
-      const int off = pm - P.p[kb];
-      const int s_begin = std::max(1, t0 - off), s_end = t1 - off;
-      if (s_end < 1) continue;                     // block not started yet
-      const int ns = s_end - s_begin + 1;
-      const int q = plane_of_block(ell, kb);
-      const bool cplx = (kb != 0 && kb != h);
-      TBlk& B = T.b[nb++];
-      B.cplx = cplx ? 1 : 0;
-      B.q = q;
-      B.ns = ns;
-      B.s0 = s_begin;
-      B.ps = cur[kb].p; B.sr = cur[kb].r; B.si = cur[kb].i;
-      B.pm = prv[kb].p; B.mr = prv[kb].r; B.mi = prv[kb].i;
-      for (int l = 0; l < ns; ++l) {
-        const int s = s_begin + l;
-        B.ar[l] = P.a_re[kb * pm + s]; B.ai[l] = P.a_im[kb * pm + s];
-        B.br[l] = P.b_re[kb * pm + s]; B.bi[l] = P.b_im[kb * pm + s];
-      }
-      shift_of_block(ctx, kb, &B.lr, &B.li);
-      B.out_last = outA + (long long)q * N;
-      ncur[kb] = {B.out_last, 1.0, 0.0};
-      if (final_pass) {
-        B.out_prev = nullptr;
-      } else if (ns == 1 && s_begin == 1) {       // x_{s_end} = x_1 stays virtual
-        B.out_prev = nullptr;
-        nprv[kb] = cur[kb];
-      } else {
-        B.out_prev = outB + (long long)q * N;
-        nprv[kb] = {B.out_prev, 1.0, 0.0};
-      }
-      nplanes += cplx ? 2 : 1;
-      steps += ns * (cplx ? 2 : 1);
-    }
-    if (nb > 0) {
-      // algorithmic bytes: x_s, x_{s-1}, hat w in + up to two iterates out per active plane
-      const double bytes = 8.0 * N * nplanes * (final_pass ? 4.0 : 5.0) + C * nb;
-      LAUNCH(ctx, KID_SWEEP, bytes,
-             (k_tsweep<TS_S, TS_TX, TS_TY><<<dim3(ntiles, nb), 256, smem, ctx->stream>>>(g, T, ctx->d_what, st)));
-      ctx->sweeps += steps;
-    }
-    for (int kb = 0; kb <= h; ++kb) {
-      cur[kb] = ncur[kb];
-      prv[kb] = nprv[kb];
-    }
-    set ^= 1;
-  }
-  NcFinal F{};
-  for (int kb = 0; kb <= h; ++kb) {
-    F.src[kb] = cur[kb].p;
-    F.tr[kb] = cur[kb].r;
-    F.ti[kb] = cur[kb].i;
-  }
-  AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
-  return AAC_OK;
-}
-
 // Wavefront passes (wave.cuh, 2D, one rank): each pass advances every block still running
 // by up to H steps in one read of its inputs; passes ping-pong between the iterate slot sets
 // d_X + (2k, 2k+1) * L; the final iterates feed the streaming inverse transform.
@@ -709,7 +613,7 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   for (int kb = 0; kb <= h; ++kb) nb_act += P.p[kb] > 1;
   int ly = ly_env;
   if (ly <= 0) {
-    const long long slots = (H > 4 ? 2LL : 3LL) * ctx->num_sms;
+    const long long slots = 3LL * ctx->num_sms;
     const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb_act));
     ly = (int)std::max<long long>(8LL * H, (g.ny + want - 1) / want);
   }
@@ -759,6 +663,11 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       ctx->sweeps += (long long)ns * B.np;
     }
     if (nb == 0) break;
+    // heaviest blocks first (the grid is dispatched with blockIdx.y slowest, so the long CTAs
+    // start early and the short ones fill the tail)
+    std::stable_sort(S.b, S.b + nb, [](const WBlk& a, const WBlk& b) {
+      return a.ns * (a.np == 2 ? 58 : 21) > b.ns * (b.np == 2 ? 58 : 21);
+    });
     LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
            (k_wave<H, NT><<<dim3(nstrip * nchunk, nb), NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
   }
@@ -813,8 +722,6 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
     return AAC_OK;
   }
   if (DIM == 2 && ctx->nranks == 1 && ctx->wave_h > 0) return wave_passes(ctx, P, zbase, zjs, st);
-  if (DIM == 2 && ctx->nranks == 1 && ctx->use_tsweep && (g.nx % 2) == 0)
-    return tsweep_passes(ctx, P, zbase, zjs, st);
   double* X = ctx->d_X;
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;

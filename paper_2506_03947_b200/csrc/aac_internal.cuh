@@ -111,7 +111,6 @@ struct aac_ctx {
   IterState* h_st = nullptr;           // pinned mirror (graph memcpy node target)
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool use_tsweep = true;             // temporally blocked sweeps (2D, one rank)
   int wave_h = 8;                      // wavefront depth (wave.cuh; 0 = per-step sweeps)
   // plans
   NcPlan nc[2];                        // cached NC plans

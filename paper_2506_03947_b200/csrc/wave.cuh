@@ -47,19 +47,20 @@ struct WSweep {
 template <int H, int NT>
 struct WGeom {
   static constexpr int TX = NT - 2 * H;                 // interior columns per strip
-  static constexpr int NSLOT = H + 2;                   // history rows (ages 0 .. H+1)
+  static constexpr int NSLOT = H + 2;                   // ages 0 .. H, +1: thread t+1 may run a step ahead
+  static constexpr int HW = NT + 1;                     // history row: one pad column
   static constexpr int XW = NT + 2;                     // exchange row: zero pad at both ends
   static constexpr int XCH = 2 * H * 2 * XW;            // [2 buffers][H levels][2 planes][XW]
-  static constexpr int HIST = NSLOT * 5 * NT;           // [slot][w_re, w_im, wxl, wxh, wyl][NT]
+  static constexpr int HIST = NSLOT * 4 * HW;           // [slot][w_re, w_im, wxl, wyl][HW]
   static constexpr size_t SMEM = (size_t)(XCH + HIST) * sizeof(double);
 };
 
-// Per-thread state of one block's wavefront. Register rings use 3 slots per level; at a step
-// of phase PH (tau mod 3) the newest row is written to slot PH, so after that step's push the
-// ages 0, 1, 2 sit in slots PH, PH+2, PH+1 (mod 3): no register moves.
-template <int NS>
+// Per-thread register rings: 3 rows per level (age 0 = newest), shifted by moves. (Renaming
+// the slots by unrolling the row loop 3 times saves the moves but triples the loop body, and
+// the instruction cache (L1.5 ~32 KB) then misses when CTAs of different blocks share an SM.)
+template <int H>
 struct WState {
-  double L[NS + 1][3][2];          // L[0] = x_{s0-1}, L[i] = L_i (i = 1..NS): [slot][plane]
+  double L[H + 1][3][2];           // L[0] = x_{s0-1}, L[i] = L_i (i = 1..ns): [age][plane]
 };
 
 template <int H, int NT>
@@ -68,16 +69,16 @@ struct WCtx {                      // per-CTA constants
   const double* what;
   Geo g;
   double* xch;
-  double* hist;                    // this thread's column of the history
+  double* hist;                    // this thread's column of the history (x+1: next thread)
   int t, x, y0, y1;
   bool colin, colout;
 };
 
-struct WRow { double w0, w1, s0, s1, m0, m1, fxl, fxh, fyl; };
+struct WRow { double w0, w1, s0, s1, m0, m1, fxl, fyl; };
 
 template <int H, int NT, bool CPLX>
 __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow& R) {
-  R.w0 = R.w1 = R.s0 = R.s1 = R.m0 = R.m1 = R.fxl = R.fxh = R.fyl = 0.0;
+  R.w0 = R.w1 = R.s0 = R.s1 = R.m0 = R.m1 = R.fxl = R.fyl = 0.0;
   const Geo& g = C.g;
   if (C.colin && r >= 0 && r < g.ny) {
     const long long p = (long long)r * g.nx + C.x;
@@ -85,7 +86,6 @@ __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow&
     R.w0 = __ldg(wq);
     if (CPLX) R.w1 = __ldg(wq + g.N);
     R.fxl = __ldg(g.wx + p);
-    R.fxh = __ldg(g.wx + p + 1);
     R.fyl = __ldg(g.wy + p);
     if (!C.B->virt) {
       R.s0 = C.B->ps[p];
@@ -100,69 +100,79 @@ __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow&
   }
 }
 
-template <int H, int NT, int NS, bool CPLX, int PH>
-__device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<NS>& S, int tau, int slot,
+template <int H, int NT, int ns, bool CPLX>
+__device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, int tau, int slot,
                                           WRow& nxt, int tau1) {
   using G = WGeom<H, NT>;
-  constexpr int A0 = PH, A1 = (PH + 2) % 3, A2 = (PH + 1) % 3;   // ages after this step's push
   const WBlk& B = *C.B;
   const int t = C.t;
   double* xb = C.xch + (tau & 1) * (H * 2 * G::XW) + 1 + t;
-  // (1) publish the newest row of every level (L_i at row tau - i; slot A1 before the push)
+  // (1) publish the newest row of every level (L_i at row tau - i) for the x-neighbours
 #pragma unroll
-  for (int i = 1; i <= NS; ++i) {
-    xb[((i - 1) * 2 + 0) * G::XW] = S.L[i][A1][0];
-    if (CPLX) xb[((i - 1) * 2 + 1) * G::XW] = S.L[i][A1][1];
+  for (int i = 1; i <= H; ++i) {
+    if (i > ns) break;
+    xb[((i - 1) * 2 + 0) * G::XW] = S.L[i][0][0];
+    if (CPLX) xb[((i - 1) * 2 + 1) * G::XW] = S.L[i][0][1];
   }
   // (2) row tau enters: history, L_0, L_1; prefetch row tau + 1
   const WRow cur = nxt;
   if (tau + 1 < tau1) wave_load_row<H, NT, CPLX>(C, tau + 1, nxt);
   {
-    double* hs = C.hist + slot * (5 * NT);
+    double* hs = C.hist + slot * (4 * G::HW);
     hs[0] = cur.w0;
-    if (CPLX) hs[NT] = cur.w1;
-    hs[2 * NT] = cur.fxl;
-    hs[3 * NT] = cur.fxh;
-    hs[4 * NT] = cur.fyl;
+    if (CPLX) hs[G::HW] = cur.w1;
+    hs[2 * G::HW] = cur.fxl;
+    hs[3 * G::HW] = cur.fyl;
+  }
+#pragma unroll
+  for (int e = 0; e < (CPLX ? 2 : 1); ++e) {
+    S.L[0][1][e] = S.L[0][0][e];
+    S.L[1][2][e] = S.L[1][1][e];
+    S.L[1][1][e] = S.L[1][0][e];
   }
   if (B.virt) {
-    S.L[0][A0][0] = 0.0;
-    S.L[0][A0][1] = 0.0;
-    S.L[1][A0][0] = B.sr * cur.w0 - B.si * cur.w1;
-    S.L[1][A0][1] = B.sr * cur.w1 + B.si * cur.w0;
+    S.L[0][0][0] = 0.0;
+    S.L[1][0][0] = B.sr * cur.w0 - B.si * cur.w1;
+    if (CPLX) {
+      S.L[0][0][1] = 0.0;
+      S.L[1][0][1] = B.sr * cur.w1 + B.si * cur.w0;
+    }
   } else {
-    S.L[1][A0][0] = B.sr * cur.s0 - B.si * cur.s1;
-    S.L[1][A0][1] = B.sr * cur.s1 + B.si * cur.s0;
-    S.L[0][A0][0] = B.mr * cur.m0 - B.mi * cur.m1;
-    S.L[0][A0][1] = B.mr * cur.m1 + B.mi * cur.m0;
+    S.L[1][0][0] = B.sr * cur.s0 - B.si * cur.s1;
+    S.L[0][0][0] = B.mr * cur.m0 - B.mi * cur.m1;
+    if (CPLX) {
+      S.L[1][0][1] = B.sr * cur.s1 + B.si * cur.s0;
+      S.L[0][0][1] = B.mr * cur.m1 + B.mi * cur.m0;
+    }
   }
   __syncthreads();
   // (3) levels: L_{i+1} at row r = tau - i
   const double lr = B.lr, li = B.li;
+  int su = slot;                                        // history slot of row r + 1
 #pragma unroll
-  for (int i = 1; i <= NS; ++i) {
-    int sl = slot - i;                                  // history slot of row r
-    sl += sl < 0 ? G::NSLOT : 0;
-    const int su = sl + 1 == G::NSLOT ? 0 : sl + 1;     // row r + 1 (upper face)
-    const double* hr = C.hist + sl * (5 * NT);
-    const double fxl = hr[2 * NT], fxh = hr[3 * NT], fyl = hr[4 * NT];
-    const double fyh = C.hist[su * (5 * NT) + 4 * NT];
+  for (int i = 1; i <= H; ++i) {
+    if (i > ns) break;
+    const int sl = su == 0 ? G::NSLOT - 1 : su - 1;     // history slot of row r
+    const double* hr = C.hist + sl * (4 * G::HW);
+    // upper x-face = lower x-face of the next column (stored by thread t+1 in an earlier step)
+    const double fxl = hr[2 * G::HW], fxh = hr[2 * G::HW + 1], fyl = hr[3 * G::HW];
+    const double fyh = C.hist[su * (4 * G::HW) + 3 * G::HW];
     const double w0 = hr[0];
     const double* xl = xb + ((i - 1) * 2) * G::XW;
     // everything except the y+1 neighbour (L_i at row r + 1, computed just before in this
     // step) is folded first; the serial chain through the levels is 4 operations deep:
     //   x_new = c + a (c - m) + b (w - (A - Lambda) c) = Q - b Ap,  Ap = fyh (c - dn) + Bp.
-    const double c0 = S.L[i][A1][0];
-    const double B0 = fma(fyl, c0 - S.L[i][A2][0], fma(fxh, c0 - xl[1], fma(fxl, c0 - xl[-1], c0)));
-    const double m0 = i == 1 ? S.L[0][A1][0] : S.L[i - 1][A2][0];
+    const double c0 = S.L[i][1][0];
+    const double B0 = fma(fyl, c0 - S.L[i][2][0], fma(fxh, c0 - xl[1], fma(fxl, c0 - xl[-1], c0)));
+    const double m0 = i == 1 ? S.L[0][1][0] : S.L[i - 1][2][0];
     const double ar = B.ar[i - 1], br = B.br[i - 1];
     double o0, o1 = 0.0;
     if (CPLX) {
-      const double w1 = hr[NT];
-      const double c1 = S.L[i][A1][1];
-      const double B1 = fma(fyl, c1 - S.L[i][A2][1],
+      const double w1 = hr[G::HW];
+      const double c1 = S.L[i][1][1];
+      const double B1 = fma(fyl, c1 - S.L[i][2][1],
                             fma(fxh, c1 - xl[G::XW + 1], fma(fxl, c1 - xl[G::XW - 1], c1)));
-      const double m1 = i == 1 ? S.L[0][A1][1] : S.L[i - 1][A2][1];
+      const double m1 = i == 1 ? S.L[0][1][1] : S.L[i - 1][2][1];
       const double ai = B.ai[i - 1], bi = B.bi[i - 1];
       const double P0 = fma(-li, c1, fma(lr, c0, w0));      // w + Lambda c (r = P - Ap)
       const double P1 = fma(li, c0, fma(lr, c1, w1));
@@ -171,65 +181,60 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<NS>& S, i
       const double X1 = fma(ai, dr, fma(ar, di, c1));
       const double Q0 = fma(-bi, P1, fma(br, P0, X0));
       const double Q1 = fma(bi, P0, fma(br, P1, X1));
-      const double Ap0 = fma(fyh, c0 - S.L[i][A0][0], B0);
-      const double Ap1 = fma(fyh, c1 - S.L[i][A0][1], B1);
+      const double Ap0 = fma(fyh, c0 - S.L[i][0][0], B0);
+      const double Ap1 = fma(fyh, c1 - S.L[i][0][1], B1);
       o0 = fma(bi, Ap1, fma(-br, Ap0, Q0));
       o1 = fma(-bi, Ap0, fma(-br, Ap1, Q1));
     } else {
       const double P0 = fma(lr, c0, w0);
       const double Q0 = fma(br, P0, fma(ar, c0 - m0, c0));
-      const double Ap0 = fma(fyh, c0 - S.L[i][A0][0], B0);
+      const double Ap0 = fma(fyh, c0 - S.L[i][0][0], B0);
       o0 = fma(-br, Ap0, Q0);
     }
-    if (i == NS) {
+    if (i == ns) {
       const int r = tau - i;
       if (C.colout && r >= C.y0 && r < C.y1) {
         const long long p = (long long)r * C.g.nx + C.x;
         B.out_last[p] = o0;
         if (CPLX) B.out_last[C.g.N + p] = o1;
-        if (B.out_prev) {                                // L_NS at row r (age 1)
-          B.out_prev[p] = S.L[i][A1][0];
-          if (CPLX) B.out_prev[C.g.N + p] = S.L[i][A1][1];
+        if (B.out_prev) {                                // L_ns at row r (age 1)
+          B.out_prev[p] = S.L[i][1][0];
+          if (CPLX) B.out_prev[C.g.N + p] = S.L[i][1][1];
         }
       }
-    } else {
-      S.L[i + 1][A0][0] = o0;
-      S.L[i + 1][A0][1] = o1;
+    } else if (i < H) {
+      S.L[i + 1][2][0] = S.L[i + 1][1][0];
+      S.L[i + 1][1][0] = S.L[i + 1][0][0];
+      S.L[i + 1][0][0] = o0;
+      if (CPLX) {
+        S.L[i + 1][2][1] = S.L[i + 1][1][1];
+        S.L[i + 1][1][1] = S.L[i + 1][0][1];
+        S.L[i + 1][0][1] = o1;
+      }
     }
+    su = sl;
   }
 }
 
-template <int H, int NT, int NS, bool CPLX>
+template <int H, int NT, int ns, bool CPLX>
 __device__ __forceinline__ void wave_block(const WCtx<H, NT>& C) {
   using G = WGeom<H, NT>;
-  WState<NS> S;
+  WState<H> S;
 #pragma unroll
-  for (int i = 0; i <= NS; ++i)
+  for (int i = 0; i <= H; ++i)
 #pragma unroll
     for (int a = 0; a < 3; ++a) S.L[i][a][0] = S.L[i][a][1] = 0.0;
-  const int tau0 = C.y0 - NS, tau1 = C.y1 + NS;         // L_1 rows tau0 .. tau1-1
+  const int tau0 = C.y0 - ns, tau1 = C.y1 + ns;         // L_1 rows tau0 .. tau1-1
   WRow nxt;
   wave_load_row<H, NT, CPLX>(C, tau0, nxt);
   int slot = (tau0 % G::NSLOT + G::NSLOT) % G::NSLOT;   // history slot of row tau
-  // tau0 = y0 - NS with y0 a multiple of ly: start the phase at tau0 mod 3 by peeling
-  int tau = tau0;
-  const int ph0 = ((tau0 % 3) + 3) % 3;
-  auto adv = [&]() { slot = slot + 1 == G::NSLOT ? 0 : slot + 1; ++tau; };
-  if (ph0 == 1) {
-    wave_step<H, NT, NS, CPLX, 1>(C, S, tau, slot, nxt, tau1); adv();
-    if (tau < tau1) { wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv(); }
-  } else if (ph0 == 2) {
-    wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv();
-  }
-  while (tau < tau1) {
-    wave_step<H, NT, NS, CPLX, 0>(C, S, tau, slot, nxt, tau1); adv();
-    if (tau >= tau1) break;
-    wave_step<H, NT, NS, CPLX, 1>(C, S, tau, slot, nxt, tau1); adv();
-    if (tau >= tau1) break;
-    wave_step<H, NT, NS, CPLX, 2>(C, S, tau, slot, nxt, tau1); adv();
+  for (int tau = tau0; tau < tau1; ++tau) {
+    wave_step<H, NT, ns, CPLX>(C, S, tau, slot, nxt, tau1);
+    slot = slot + 1 == G::NSLOT ? 0 : slot + 1;
   }
 }
 
+// one compact specialised loop per (steps, real/complex): no level guards in the loop
 template <int H, int NT, int NS>
 __device__ __forceinline__ void wave_dispatch_ns(const WCtx<H, NT>& C, int ns, bool cplx) {
   if constexpr (NS >= 1) {
@@ -261,10 +266,11 @@ __global__ void __launch_bounds__(NT, H > 4 ? 2 : 3) k_wave(Geo g, WSweep W, con
   C.colout = C.t >= H && C.t < NT - H && C.x < g.nx;
   C.y0 = chunk * W.ly;
   C.y1 = min(C.y0 + W.ly, g.ny);
-  // zero pads of the exchange rows (never written)
+  // zero pads of the exchange rows and of the history rows (never written)
   for (int k = threadIdx.x; k < 2 * H * 2; k += NT) {
     wsm[k * G::XW] = 0.0;
     wsm[k * G::XW + G::XW - 1] = 0.0;
   }
+  for (int k = threadIdx.x; k < G::NSLOT * 4; k += NT) wsm[G::XCH + k * G::HW + NT] = 0.0;
   wave_dispatch_ns<H, NT, H>(C, C.B->ns, C.B->np == 2);
 }
