@@ -526,7 +526,12 @@ static int run_inverse(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zba
                        const IterState* st) {
   const long long N = ctx->geo.N;
   const double V = 8.0 * ctx->ell * N;
-  LAUNCH(ctx, KID_INV, 2 * V, k_inverse<1><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  if (ctx->ell == 10)
+    LAUNCH(ctx, KID_INV, 2 * V, k_inverse_exact<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  else if (ctx->ell == 12)
+    LAUNCH(ctx, KID_INV, 2 * V, k_inverse_exact<12><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
+  else
+    LAUNCH(ctx, KID_INV, 2 * V, k_inverse<1><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
   return AAC_OK;
 }
 
@@ -586,7 +591,9 @@ static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
 
 static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
   const bool tma = (ctx->geo.N % 2) == 0;         // 16-byte aligned plane tiles
+  // plane capacity = ell rounded up to 10 / 12 / 16: the shared-memory ring scales with it
   if (ctx->ell <= 10) return tma ? launch_fwd_upd_t<10, true>(ctx, bytes) : launch_fwd_upd_t<10, false>(ctx, bytes);
+  if (ctx->ell <= 12) return tma ? launch_fwd_upd_t<12, true>(ctx, bytes) : launch_fwd_upd_t<12, false>(ctx, bytes);
   return tma ? launch_fwd_upd_t<16, true>(ctx, bytes) : launch_fwd_upd_t<16, false>(ctx, bytes);
 }
 
@@ -726,7 +733,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * g.S;
-  const dim3 gsw(grid1d(g.nx / VEC, SW_TX), g.ny, g.nz);
+  const unsigned ncx_last = grid1d(g.nx / VEC, SW_TX), ncx = grid1d(g.nx / VEC, SW_FX);
   // the last step as a regular sweep writing x_{p_k}, then the streaming inverse transform
   // (measured faster than the fused k_sweep<LAST>, which stays available: AAC_FUSED_LAST=1)
   static const bool split_last = getenv("AAC_FUSED_LAST") == nullptr;
@@ -776,7 +783,8 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
       passes += np * ((s == 1 ? 1.0 : s == 2 ? 2.0 : 3.0) + (last ? 0.0 : 1.0));
     }
     AAC_TRY(comm_halo(ctx, planes, qs, nh));
-    const dim3 blk(SW_TX, S.nact);
+    const dim3 blk = last ? dim3(SW_TX, S.nact) : dim3(SW_FX, 1);
+    const dim3 gsw(last ? ncx_last : ncx * S.nact, g.ny, g.nz);
     if (last) {
       const size_t smem = (size_t)ell * SW_TX * VEC * sizeof(double);
       const double bytes = 8.0 * N * passes + C + V;           // x_s, x_{s-1}, w in; z out
@@ -861,8 +869,8 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
   }
   const size_t smem = (arnoldi_ring_doubles<ELLC>() + (size_t)(AW + 1) * 2 * ldh) * sizeof(double);
   // persistent grid: exactly the resident capacity (no partial second wave)
-  static thread_local int occ_cache[2][4][2][2] = {};
-  int& occ = occ_cache[ELLC == 10 ? 0 : 1][DIM][TMA ? 1 : 0][FUSED ? 1 : 0];
+  static thread_local int occ_cache[3][4][2][2] = {};
+  int& occ = occ_cache[ELLC == 10 ? 0 : (ELLC == 12 ? 1 : 2)][DIM][TMA ? 1 : 0][FUSED ? 1 : 0];
   AAC_TRY(smem_optin(ctx, k_arnoldi<DIM, ELLC, TMA, FUSED>, smem));
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi<DIM, ELLC, TMA, FUSED>, AT + 32, smem);
@@ -884,6 +892,10 @@ static int arnoldi_dim(aac_ctx* ctx, int host_j) {
   if (ctx->ell <= 10) {
     if (fused) return tma ? launch_arnoldi<DIM, 10, true, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false, true>(ctx, host_j);
     return tma ? launch_arnoldi<DIM, 10, true, false>(ctx, host_j) : launch_arnoldi<DIM, 10, false, false>(ctx, host_j);
+  }
+  if (ctx->ell <= 12) {
+    if (fused) return tma ? launch_arnoldi<DIM, 12, true, true>(ctx, host_j) : launch_arnoldi<DIM, 12, false, true>(ctx, host_j);
+    return tma ? launch_arnoldi<DIM, 12, true, false>(ctx, host_j) : launch_arnoldi<DIM, 12, false, false>(ctx, host_j);
   }
   if (fused) return tma ? launch_arnoldi<DIM, 16, true, true>(ctx, host_j) : launch_arnoldi<DIM, 16, false, true>(ctx, host_j);
   return tma ? launch_arnoldi<DIM, 16, true, false>(ctx, host_j) : launch_arnoldi<DIM, 16, false, false>(ctx, host_j);

@@ -77,6 +77,35 @@ __device__ __forceinline__ void dft_store(const Dft& D, long long N, long long p
   }
 }
 
+// Same with ell == ELLC known at compile time: every twiddle index (k*pl mod ell) is static,
+// so the transform is straight-line FMAs on registers with constant-bank twiddles.
+template <int ELLC>
+__device__ __forceinline__ void dft_store_exact(const Dft& D, long long N, long long p, double* w,
+                                                double* __restrict__ what) {
+  constexpr int h = ELLC / 2;
+#pragma unroll
+  for (int pl = 0; pl < ELLC; ++pl) w[pl] *= D.g[pl];
+  double s0 = 0.0, sh = 0.0;
+#pragma unroll
+  for (int pl = 0; pl < ELLC; ++pl) {
+    s0 += w[pl];
+    sh += (pl & 1) ? -w[pl] : w[pl];
+  }
+  what[p] = D.scale * s0;
+  what[(long long)(ELLC - 1) * N + p] = D.scale * sh;
+#pragma unroll
+  for (int k = 1; k < h; ++k) {
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int pl = 0; pl < ELLC; ++pl) {
+      re = fma(w[pl], D.c[(k * pl) % ELLC], re);
+      im = fma(-w[pl], D.s[(k * pl) % ELLC], im);
+    }
+    what[(long long)(2 * k - 1) * N + p] = D.scale * re;
+    what[(long long)(2 * k) * N + p] = D.scale * im;
+  }
+}
+
 // Standalone forward transform: hat w = U^* Gamma r.
 template <int ELLC>
 __global__ void __launch_bounds__(256) k_forward(long long N, Dft D, const double* __restrict__ r,
@@ -159,7 +188,8 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
         FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
       }
       FOR_PL(pl) nrm = fma(w[pl], w[pl], nrm);
-      dft_store<ELLC>(D, N, p, w, what);
+      if (ell == ELLC) dft_store_exact<ELLC>(D, N, p, w, what);
+      else dft_store<ELLC>(D, N, p, w, what);
     }
     nrm = warp_sum(nrm);
     if (lane == 0) red[warp] = nrm;
@@ -212,10 +242,11 @@ struct NcSweep {
   int nblk;
 };
 
-constexpr int SW_TX = 64;                 // point groups per CTA along x
+constexpr int SW_TX = 64;                 // LAST: point groups per CTA along x (threadIdx.y = block)
+constexpr int SW_FX = 128;                // otherwise: one block per CTA, flat grid (chunk, block)
 
 template <int DIM, int VEC, bool LAST>
-__global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, LAST ? 2 : 1) k_sweep(Geo g, NcSweep P, Dft D,
+__global__ void __launch_bounds__(LAST ? SW_TX * AAC_MAX_BLK : SW_FX, LAST ? 2 : 4) k_sweep(Geo g, NcSweep P, Dft D,
                                                                  const double* __restrict__ what,
                                                                  const double* __restrict__ hlo,
                                                                  const double* __restrict__ hhi,
@@ -229,10 +260,14 @@ __global__ void __launch_bounds__(SW_TX * AAC_MAX_BLK, LAST ? 2 : 1) k_sweep(Geo
   extern __shared__ double ysh[];         // [ell planes][SW_TX*VEC]
   const long long N = g.N;
   // grid (x-chunks of SW_TX*VEC points, ny, nz): coordinates without index division
-  const int xx = (blockIdx.x * SW_TX + threadIdx.x) * VEC;
+  // (not LAST: blocks are independent, so each CTA runs one block and the grid is flat over
+  // (x-chunk, block): full occupancy whatever the number of active blocks)
+  constexpr int TXB = LAST ? SW_TX : SW_FX;
+  const int cx = LAST ? (int)blockIdx.x : (int)blockIdx.x / P.nact;
+  const int xx = (cx * TXB + threadIdx.x) * VEC;
   const long long row0 = ((long long)blockIdx.z * g.ny + blockIdx.y) * g.nx;
   const long long p = row0 + xx;
-  const NcBlk& B = P.b[threadIdx.y];
+  const NcBlk& B = P.b[LAST ? (int)threadIdx.y : (int)blockIdx.x % P.nact];
   double out_r[VEC], out_i[VEC];
   if (xx < g.nx) {
     PtV<DIM, VEC> q;
@@ -402,5 +437,39 @@ __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
 #pragma unroll
     for (int e = 0; e < VEC; ++e) o[e] = f * (yr[0][e] + ((j & 1) ? -yr[h][e] : yr[h][e]) + 2.0 * acc[e]);
     stv<VEC>(z + (long long)j * N, p, o);
+  }
+}
+
+// k_inverse with ell == ELL at compile time (static twiddle indices, all planes in registers).
+template <int ELL>
+__global__ void __launch_bounds__(256) k_inverse_exact(long long N, Dft D, NcFinal F,
+                                                       double* __restrict__ zbase, long long zjs,
+                                                       const IterState* st) {
+  if (st && st->done) return;
+  double* z = zbase + (st ? (long long)st->j * zjs : 0LL);
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  constexpr int h = ELL / 2;
+  double yr[h + 1], yi[h + 1];
+#pragma unroll
+  for (int kb = 0; kb <= h; ++kb) {                // all loads first
+    yr[kb] = F.src[kb][p];
+    yi[kb] = (kb != 0 && kb != h) ? F.src[kb][N + p] : 0.0;
+  }
+#pragma unroll
+  for (int kb = 0; kb <= h; ++kb) {
+    const double a = yr[kb], b = yi[kb];
+    yr[kb] = a * F.tr[kb] - b * F.ti[kb];
+    yi[kb] = (kb != 0 && kb != h) ? (a * F.ti[kb] + b * F.tr[kb]) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < ELL; ++j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int kb = 1; kb < h; ++kb) {
+      acc = fma(yr[kb], D.c[(j * kb) % ELL], acc);
+      acc = fma(-yi[kb], D.s[(j * kb) % ELL], acc);
+    }
+    z[(long long)j * N + p] = D.scale * D.gi[j] * (yr[0] + ((j & 1) ? -yr[h] : yr[h]) + 2.0 * acc);
   }
 }
