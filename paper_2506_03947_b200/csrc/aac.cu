@@ -370,7 +370,12 @@ struct StreamScope {
   }
 };
 
-static inline bool vec2(const aac_ctx* ctx) { return (ctx->geo.nx % 2) == 0; }
+// Two points per thread (16-byte loads) when nx is even (AAC_VEC3=1 forces one point per
+// thread in 3D: measured 8% slower at 256^3 despite the higher occupancy).
+static inline bool vec2(const aac_ctx* ctx) {
+  static const bool v3_one = getenv("AAC_VEC3") && atoi(getenv("AAC_VEC3")) == 1;
+  return (ctx->geo.nx % 2) == 0 && !(ctx->dim == 3 && v3_one);
+}
 
 // ------------------------------------------------------------------------------------------
 // calA apply

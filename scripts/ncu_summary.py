@@ -29,5 +29,5 @@ for r in rows[2:]:
     name = d["Kernel Name"].split("(")[0]
     extra = " ".join(f"{k.split('.')[0].split('__')[1][:14]}={d[k]}" for k in want[8:] if k in d)
     print(f"{name:32s} blk={d['Block Size']:12s} grid={d['Grid Size']:14s} t={tus:9.1f}us rd={rd:8.1f}MB wr={wr:8.1f}MB "
-          f"GB/s={(rd + wr) / tus * 1e-3 * 1e3:7.0f} dram%={float(d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']):5.1f} "
+          f"GB/s={(rd + wr) / tus * 1e3:7.0f} dram%={float(d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']):5.1f} "
           f"regs={d['launch__registers_per_thread']} {extra}")
