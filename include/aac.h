@@ -144,6 +144,9 @@ int aac_profile_enable(aac_ctx* ctx, int enable);
 int aac_profile_count(void);
 int aac_profile_read(aac_ctx* ctx, int id, const char** name, double* ms, long long* launches,
                      double* model_bytes);
+/* Model (algorithmic) fp64 flops accumulated by kernel class `id` -- non-zero only for the
+ * classes whose roofline is arithmetic (the wavefront Chebyshev kernel).                 */
+int aac_profile_flops(aac_ctx* ctx, int id, double* model_flops);
 int aac_profile_reset(aac_ctx* ctx);
 long long aac_launch_count(const aac_ctx* ctx);
 

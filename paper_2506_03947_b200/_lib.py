@@ -20,7 +20,7 @@ METHODS = {"nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_matvec", "aac_precond_apply", "aac_gmres",
            "aac_gmres_host", "aac_query", "aac_profile_enable", "aac_profile_count",
-           "aac_profile_read", "aac_profile_reset", "aac_launch_count", "aac_last_error",
+           "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_launch_count", "aac_last_error",
            "aac_destroy"]
 
 
@@ -67,6 +67,7 @@ def _load():
         "aac_profile_count": (I, []),
         "aac_profile_read": (I, [P, I, ctypes.POINTER(ctypes.c_char_p), dp,
                                  ctypes.POINTER(L), dp]),
+        "aac_profile_flops": (I, [P, I, dp]),
         "aac_profile_reset": (I, [P]),
         "aac_launch_count": (L, [P]),
         "aac_last_error": (ctypes.c_char_p, [P]),

@@ -44,6 +44,8 @@ LaunchScope::LaunchScope(aac_ctx* c, int kid, double bytes) : ctx(c), id(kid) {
   ctx->launches++;
   ctx->prof_n[kid]++;
   ctx->prof_bytes[kid] += bytes;
+  ctx->prof_flops[kid] += ctx->next_flops;
+  ctx->next_flops = 0.0;
   if (ctx->prof) {
     if (ctx->ev_pool.size() < 2) {
       for (int i = 0; i < 64; ++i) {
@@ -640,7 +642,7 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
     S.nstrip = nstrip;
     S.ly = ly;
     int nb = 0;
-    double passes = 0.0;
+    double passes = 0.0, flops = 0.0;
     for (int kb = 0; kb <= h; ++kb) {
       const int steps = P.p[kb] - 1;
       if (steps < s0) continue;                       // finished (or passive)
@@ -672,6 +674,9 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       }
       shift_of_block(ctx, kb, &B.lr, &B.li);
       passes += B.np * ((pass == 0 ? 1.0 : 3.0) + (final_pass ? 1.0 : 2.0));
+      // algorithmic fp64 flops of the recurrence per point and step:
+      // complex 58 (2 x 5-point stencils in difference form + complex three-term update), real 21
+      flops += (double)N * ns * (cplx ? 58.0 : 21.0);
       ctx->sweeps += (long long)ns * B.np;
     }
     if (nb == 0) break;
@@ -680,6 +685,7 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
     std::stable_sort(S.b, S.b + nb, [](const WBlk& a, const WBlk& b) {
       return a.ns * (a.np == 2 ? 58 : 21) > b.ns * (b.np == 2 ? 58 : 21);
     });
+    ctx->next_flops = flops;
     LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
            (k_wave<H, NT><<<dim3(nstrip * nchunk, nb), NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
   }
@@ -1112,6 +1118,11 @@ extern "C" int aac_profile_read(aac_ctx* ctx, int id, const char** name, double*
   if (model_bytes) *model_bytes = ctx->prof_bytes[id];
   return AAC_OK;
 }
+extern "C" int aac_profile_flops(aac_ctx* ctx, int id, double* model_flops) {
+  if (!ctx || id < 0 || id >= KID_COUNT || !model_flops) return aac_fail(ctx, AAC_EINVAL, "bad profile id");
+  *model_flops = ctx->prof_flops[id];
+  return AAC_OK;
+}
 extern "C" int aac_profile_reset(aac_ctx* ctx) {
   if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "NULL ctx");
   AAC_TRY(prof_collect(ctx));
@@ -1119,6 +1130,7 @@ extern "C" int aac_profile_reset(aac_ctx* ctx) {
     ctx->prof_ms[i] = 0;
     ctx->prof_n[i] = 0;
     ctx->prof_bytes[i] = 0;
+    ctx->prof_flops[i] = 0;
   }
   return AAC_OK;
 }

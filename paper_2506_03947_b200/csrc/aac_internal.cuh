@@ -127,6 +127,8 @@ struct aac_ctx {
   double prof_ms[KID_COUNT] = {0};
   long long prof_n[KID_COUNT] = {0};
   double prof_bytes[KID_COUNT] = {0};
+  double prof_flops[KID_COUNT] = {0};  // model fp64 flops (set for ALU-bound kernels)
+  double next_flops = 0.0;             // attached to the next launch
   std::string err;
 };
 

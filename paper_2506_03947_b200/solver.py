@@ -134,7 +134,10 @@ class Solver:
             nl = ctypes.c_longlong()
             check(lib.aac_profile_read(self.ctx, i, ctypes.byref(name), ctypes.byref(ms),
                                        ctypes.byref(nl), ctypes.byref(nb)), self.ctx)
-            out[name.value.decode()] = {"ms": ms.value, "launches": nl.value, "model_bytes": nb.value}
+            fl = ctypes.c_double()
+            check(lib.aac_profile_flops(self.ctx, i, ctypes.byref(fl)), self.ctx)
+            out[name.value.decode()] = {"ms": ms.value, "launches": nl.value, "model_bytes": nb.value,
+                                        "model_flops": fl.value}
         return out
 
     def launch_count(self):

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round bench: every BASELINE config through bench.py, then the headline launch list and one
+# ncu --set full capture of one GMRES iteration (all kernel classes).
+set -u
+TAG=${1:-bench}
+O=gpurun_out/$TAG; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
+timeout 600 python bench.py > $O/b_head.json 2> $O/b_head.err; echo "head rc=$?"
+for c in saddle 2d256 1d; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > $O/b_$c.json 2> $O/b_$c.err; echo "$c rc=$?"
+done
+timeout 900 python bench.py --config 3d --maxit 20 --steps 2 --no-cpu-baseline > $O/b_3d.json 2> $O/b_3d.err; echo "3d rc=$?"
+timeout 900 python bench.py --impl reference --steps 2 > $O/b_ref.json 2> $O/b_ref.err; echo "ref rc=$?"
+CMD="python scripts/one_solve.py headline 2"
+timeout 300 $CMD > $O/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv $CMD > $O/ncu1.log 2>&1; echo "ncu launches rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_wave|k_fwd|k_arnoldi|k_matvec|k_inverse" -s 40 -c 5 -o $O/prof $CMD > $O/ncu2.log 2>&1; echo "ncu full rc=$?"
