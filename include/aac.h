@@ -97,6 +97,30 @@ int aac_setup(const aac_grid* g, const double* kx, const double* ky, const doubl
               double c, int ell, double alpha, int max_krylov, void* cuda_stream,
               const void* nccl_id, aac_ctx** out);
 
+/* Host-staged transport for the slab exchanges (alternative to NCCL). The library copies
+ * the data of every exchange step to pinned host memory, synchronises its stream, calls the
+ * callback and copies the result back: slow, but it lets any host process group (e.g.
+ * torch.distributed "gloo") carry the slab decomposition -- used to verify the multi-rank
+ * path with several processes sharing fewer GPUs than ranks, where NCCL cannot run.
+ *  allreduce(user, buf, n, op): in-place all-reduce of n HOST doubles over all ranks,
+ *                               op 0 = sum, 1 = max. Return 0 on success.
+ *  sendrecv(user, n, send_lo, recv_lo, send_hi, recv_hi): exchange n HOST doubles with
+ *      the rank below (send_lo -> its recv_hi, its send_hi -> recv_lo) and the rank above;
+ *      the pointers of a missing neighbour are NULL. Return 0 on success.
+ * A non-zero return makes the calling entry point fail with AAC_ENCCL.                 */
+typedef struct {
+  void* user;
+  int (*allreduce)(void* user, double* buf, int n, int op);
+  int (*sendrecv)(void* user, int64_t n, const double* send_lo, double* recv_lo,
+                  const double* send_hi, double* recv_hi);
+} aac_host_transport;
+
+/* aac_setup with the host-staged transport instead of NCCL (same arguments otherwise;
+ * `tr` is copied; its callbacks must stay valid until aac_destroy).                    */
+int aac_setup_host_transport(const aac_grid* g, const double* kx, const double* ky,
+                             const double* kz, double c, int ell, double alpha, int max_krylov,
+                             void* cuda_stream, const aac_host_transport* tr, aac_ctx** out);
+
 /* y = calA x: y_0 = A x_0, y_j = A x_j - x_{j-1}.
  * x, y: device, [ell][n_local]; x != y. One halo exchange when nranks > 1.       */
 int aac_matvec(aac_ctx* ctx, const double* x, double* y);

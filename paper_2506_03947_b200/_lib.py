@@ -18,7 +18,7 @@ AAC_NC1, AAC_NC2, AAC_SP = 1, 2, 3
 METHODS = {"nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
-SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_matvec", "aac_precond_apply", "aac_gmres",
+SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",
            "aac_gmres_host", "aac_query", "aac_profile_enable", "aac_profile_count",
            "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_launch_count", "aac_last_error",
            "aac_destroy"]
@@ -36,6 +36,17 @@ class aac_gmres_info(ctypes.Structure):
 
     def asdict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                ctypes.c_int, ctypes.c_int)
+SENDRECV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
+
+
+class aac_host_transport(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("allreduce", ALLREDUCE_FN), ("sendrecv", SENDRECV_FN)]
 
 
 class AacError(RuntimeError):
@@ -58,6 +69,8 @@ def _load():
                                  ctypes.POINTER(ctypes.c_int64), dp]),
         "aac_setup": (I, [ctypes.POINTER(aac_grid), dp, dp, dp, D, I, D, I, P, P,
                           ctypes.POINTER(P)]),
+        "aac_setup_host_transport": (I, [ctypes.POINTER(aac_grid), dp, dp, dp, D, I, D, I, P,
+                                         ctypes.POINTER(aac_host_transport), ctypes.POINTER(P)]),
         "aac_matvec": (I, [P, P, P]),
         "aac_precond_apply": (I, [P, I, I, P, P]),
         "aac_gmres": (I, [P, I, I, P, P, D, I, ctypes.POINTER(aac_gmres_info)]),

@@ -186,9 +186,28 @@ extern "C" int aac_slab_weights(const aac_grid* g, const double* kx, const doubl
   return ok ? AAC_OK : aac_fail(nullptr, AAC_EINVAL, "kappa must be finite and > 0 on every interior face");
 }
 
+static int setup_impl(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+                      double c, int ell, double alpha, int max_krylov, void* cuda_stream,
+                      const void* nccl_id, const aac_host_transport* tr, aac_ctx** out);
+
 extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, const double* kz,
                          double c, int ell, double alpha, int max_krylov, void* cuda_stream,
                          const void* nccl_id, aac_ctx** out) {
+  return setup_impl(g, kx, ky, kz, c, ell, alpha, max_krylov, cuda_stream, nccl_id, nullptr, out);
+}
+
+extern "C" int aac_setup_host_transport(const aac_grid* g, const double* kx, const double* ky,
+                                        const double* kz, double c, int ell, double alpha,
+                                        int max_krylov, void* cuda_stream,
+                                        const aac_host_transport* tr, aac_ctx** out) {
+  if (!tr || !tr->allreduce || !tr->sendrecv)
+    return aac_fail(nullptr, AAC_EINVAL, "aac_setup_host_transport: incomplete transport");
+  return setup_impl(g, kx, ky, kz, c, ell, alpha, max_krylov, cuda_stream, nullptr, tr, out);
+}
+
+static int setup_impl(const aac_grid* g, const double* kx, const double* ky, const double* kz,
+                      double c, int ell, double alpha, int max_krylov, void* cuda_stream,
+                      const void* nccl_id, const aac_host_transport* tr, aac_ctx** out) {
   if (!g || !out) return aac_fail(nullptr, AAC_EINVAL, "aac_setup: NULL grid or out");
   *out = nullptr;
   if (g->dim < 1 || g->dim > 3) return aac_fail(nullptr, AAC_EINVAL, "dim must be 1, 2 or 3");
@@ -247,6 +266,10 @@ extern "C" int aac_setup(const aac_grid* g, const double* kx, const double* ky, 
   }
   const long long lenx = lens[0], leny = lens[1];
 
+  if (tr) {
+    ctx->host_tr = true;
+    ctx->htr = *tr;
+  }
   int rc = comm_init(ctx, nccl_id);
   if (rc != AAC_OK) {
     g_last_err = ctx->err;

@@ -116,8 +116,12 @@ struct aac_ctx {
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;
   SpPlan* sp = nullptr;
-  // NCCL (dlopen'ed)
+  // NCCL (dlopen'ed), or the host-staged transport
   void* nccl_comm = nullptr;
+  bool host_tr = false;
+  aac_host_transport htr{};
+  double* h_stage = nullptr;           // pinned staging for host-transport exchanges
+  long long stage_len = 0;
   // bookkeeping
   long long launches = 0;
   long long sweeps = 0;

@@ -56,7 +56,7 @@ static int nccl_load(aac_ctx* ctx) {
   } while (0)
 
 static int comm_init(aac_ctx* ctx, const void* nccl_id) {
-  if (ctx->nranks == 1) return AAC_OK;
+  if (ctx->nranks == 1 || ctx->host_tr) return AAC_OK;
   if (!nccl_id) return aac_fail(ctx, AAC_EINVAL, "nccl_id required when nranks > 1");
   AAC_TRY(nccl_load(ctx));
   ncclUniqueId id;
@@ -70,11 +70,37 @@ static int comm_init(aac_ctx* ctx, const void* nccl_id) {
 static void comm_destroy(aac_ctx* ctx) {
   if (ctx->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)ctx->nccl_comm);
   ctx->nccl_comm = nullptr;
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  ctx->h_stage = nullptr;
+}
+
+// Pinned staging for the host transport: [send_lo | recv_lo | send_hi | recv_hi] halo layers of
+// up to ell planes, or the all-reduce payload.
+static int host_stage(aac_ctx* ctx, long long need) {
+  if (ctx->stage_len >= need) return AAC_OK;
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  ctx->h_stage = nullptr;
+  ctx->stage_len = 0;
+  CUDA_TRY(ctx, cudaMallocHost((void**)&ctx->h_stage, (size_t)need * sizeof(double)));
+  ctx->stage_len = need;
+  return AAC_OK;
+}
+
+static int host_allreduce(aac_ctx* ctx, double* d, int n, int op) {
+  AAC_TRY(host_stage(ctx, n));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stage, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->htr.allreduce(ctx->htr.user, ctx->h_stage, n, op) != 0)
+    return aac_fail(ctx, AAC_ENCCL, "host transport all-reduce failed");
+  CUDA_TRY(ctx, cudaMemcpyAsync(d, ctx->h_stage, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // the staging buffer is reused next call
+  return AAC_OK;
 }
 
 // In-place all-reduce of n doubles on the context stream (no-op on one rank).
 static int comm_allreduce(aac_ctx* ctx, double* d, int n, ncclRedOp_t op) {
   if (ctx->nranks == 1 || n <= 0) return AAC_OK;
+  if (ctx->host_tr) return host_allreduce(ctx, d, n, op == ncclMax ? 1 : 0);
   NCCL_TRY(ctx, g_nccl.AllReduce(d, d, (size_t)n, ncclFloat64, op, (ncclComm_t)ctx->nccl_comm,
                                  ctx->stream));
   return AAC_OK;
@@ -89,6 +115,33 @@ static int comm_halo(aac_ctx* ctx, const double* const* planes, const int* qs, i
   const long long S = g.S;
   double* hlo = ctx->d_halo;
   double* hhi = ctx->d_halo + (long long)ctx->ell * S;
+  if (ctx->host_tr) {
+    const long long n = (long long)count * S;
+    AAC_TRY(host_stage(ctx, 4 * n));
+    double* slo = ctx->h_stage;
+    double* rlo = slo + n;
+    double* shi = rlo + n;
+    double* rhi = shi + n;
+    for (int i = 0; i < count; ++i) {
+      if (g.has_lo)
+        CUDA_TRY(ctx, cudaMemcpyAsync(slo + i * S, planes[i], S * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      if (g.has_hi)
+        CUDA_TRY(ctx, cudaMemcpyAsync(shi + i * S, planes[i] + g.N - S, S * sizeof(double), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->htr.sendrecv(ctx->htr.user, n, g.has_lo ? slo : nullptr, g.has_lo ? rlo : nullptr,
+                          g.has_hi ? shi : nullptr, g.has_hi ? rhi : nullptr) != 0)
+      return aac_fail(ctx, AAC_ENCCL, "host transport halo exchange failed");
+    for (int i = 0; i < count; ++i) {
+      if (g.has_lo)
+        CUDA_TRY(ctx, cudaMemcpyAsync(hlo + qs[i] * S, rlo + i * S, S * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      if (g.has_hi)
+        CUDA_TRY(ctx, cudaMemcpyAsync(hhi + qs[i] * S, rhi + i * S, S * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return AAC_OK;
+  }
   ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
   NCCL_TRY(ctx, g_nccl.GroupStart());
   for (int i = 0; i < count; ++i) {

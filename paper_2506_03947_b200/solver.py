@@ -26,6 +26,48 @@ def slab_range(n: int, nranks: int, rank: int):
     return lo.value, hi.value
 
 
+class HostTransport:
+    """aac_host_transport over a torch.distributed process group (e.g. "gloo"): the library
+    stages every exchange through pinned host memory and these callbacks move it. Marshalling
+    only -- no arithmetic of the method happens here (an all-reduce is a sum of the ranks'
+    partial sums, as NCCL's would be)."""
+
+    def __init__(self, group, rank: int, nranks: int):
+        import torch.distributed as dist
+        self.group, self.rank, self.nranks = group, rank, nranks
+        self.error = None
+
+        def allreduce(user, buf, n, op):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
+                dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM,
+                                group=self.group)
+                return 0
+            except Exception as e:  # reported through aac_last_error as AAC_ENCCL
+                self.error = e
+                return -1
+
+        def sendrecv(user, n, send_lo, recv_lo, send_hi, recv_hi):
+            try:
+                reqs = []
+                for snd, rcv, peer in ((send_lo, recv_lo, self.rank - 1), (send_hi, recv_hi, self.rank + 1)):
+                    if snd:
+                        g = dist.get_global_rank(self.group, peer) if self.group is not None else peer
+                        reqs.append(dist.isend(torch.from_numpy(np.ctypeslib.as_array(snd, shape=(n,))),
+                                               g, group=self.group))
+                        reqs.append(dist.irecv(torch.from_numpy(np.ctypeslib.as_array(rcv, shape=(n,))),
+                                               g, group=self.group))
+                for r in reqs:
+                    r.wait()
+                return 0
+            except Exception as e:
+                self.error = e
+                return -1
+
+        self._fns = (_lib.ALLREDUCE_FN(allreduce), _lib.SENDRECV_FN(sendrecv))   # keep alive
+        self.struct = _lib.aac_host_transport(None, self._fns[0], self._fns[1])
+
+
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
@@ -36,7 +78,8 @@ def _method(m):
 
 class Solver:
     def __init__(self, dim, n, kx, ky=None, kz=None, c=0.0, ell=10, alpha=1e-4, *,
-                 max_krylov=64, device=None, stream=None, rank=0, nranks=1, nccl_id=None):
+                 max_krylov=64, device=None, stream=None, rank=0, nranks=1, nccl_id=None,
+                 host_group=None):
         n = tuple(int(v) for v in n) + (1,) * (3 - len(n))   # (nx, ny, nz)
         self.dim, self.n, self.ell, self.alpha, self.c = dim, n, ell, alpha, c
         self.rank, self.nranks = rank, nranks
@@ -57,9 +100,17 @@ class Solver:
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         ctx = ctypes.c_void_p()
-        check(lib.aac_setup(ctypes.byref(g), arr(kx), arr(ky), arr(kz), float(c), int(ell),
-                            float(alpha), int(max_krylov), ctypes.c_void_p(self.stream.cuda_stream),
-                            idbuf, ctypes.byref(ctx)))
+        if host_group is not None:
+            # slab exchanges through a host process group (verification without NCCL)
+            self._transport = HostTransport(host_group, rank, nranks)
+            check(lib.aac_setup_host_transport(ctypes.byref(g), arr(kx), arr(ky), arr(kz), float(c),
+                                               int(ell), float(alpha), int(max_krylov),
+                                               ctypes.c_void_p(self.stream.cuda_stream),
+                                               ctypes.byref(self._transport.struct), ctypes.byref(ctx)))
+        else:
+            check(lib.aac_setup(ctypes.byref(g), arr(kx), arr(ky), arr(kz), float(c), int(ell),
+                                float(alpha), int(max_krylov), ctypes.c_void_p(self.stream.cuda_stream),
+                                idbuf, ctypes.byref(ctx)))
         self.ctx = ctx
         nl = ctypes.c_int64()
         mu0, mu1 = ctypes.c_double(), ctypes.c_double()
