@@ -644,18 +644,8 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   const Dft D = make_dft(ctx);
   AAC_TRY(smem_optin(ctx, k_wave<H, NT>, WG::SMEM));
   const int nstrip = (g.nx + WG::TX - 1) / WG::TX;
-  // rows per chunk: about two CTAs per resident slot, but at least 8 H rows per chunk
+  // rows per chunk: AAC_WAVE_LY overrides the default below
   const int ly_env = getenv("AAC_WAVE_LY") ? atoi(getenv("AAC_WAVE_LY")) : 0;
-  int nb_act = 0;
-  for (int kb = 0; kb <= h; ++kb) nb_act += P.p[kb] > 1;
-  int ly = ly_env;
-  if (ly <= 0) {
-    const long long slots = 3LL * ctx->num_sms;
-    const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb_act));
-    ly = (int)std::max<long long>(8LL * H, (g.ny + want - 1) / want);
-  }
-  ly = std::min(ly, g.ny);
-  const int nchunk = (g.ny + ly - 1) / ly;
   const double* fin[AAC_MAX_BLK] = {};
   const int steps_max = P.pmax - 1;
   for (int pass = 0; pass * H < steps_max; ++pass) {
@@ -663,7 +653,6 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
     const int set = pass & 1, prev_set = set ^ 1;
     WSweep S{};
     S.nstrip = nstrip;
-    S.ly = ly;
     int nb = 0;
     double passes = 0.0, flops = 0.0;
     for (int kb = 0; kb <= h; ++kb) {
@@ -703,14 +692,33 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       ctx->sweeps += (long long)ns * B.np;
     }
     if (nb == 0) break;
-    // heaviest blocks first (the grid is dispatched with blockIdx.y slowest, so the long CTAs
-    // start early and the short ones fill the tail)
-    std::stable_sort(S.b, S.b + nb, [](const WBlk& a, const WBlk& b) {
-      return a.ns * (a.np == 2 ? 58 : 21) > b.ns * (b.np == 2 ? 58 : 21);
-    });
+    // heaviest blocks first (lowest CTA indices are dispatched first)
+    auto cost = [](const WBlk& b) { return (double)b.ns * (b.np == 2 ? 58.0 : 21.0); };
+    std::stable_sort(S.b, S.b + nb, [&](const WBlk& a, const WBlk& b) { return cost(a) > cost(b); });
+    S.nb = nb;
+    // rows per chunk (all blocks alike): ~2 CTAs per resident slot over the active blocks,
+    // at least 8 steps' worth of rows (measured at the headline: 9.29 ms at 80 rows, within 3%
+    // from 48 to 140; an equal-work split with taller chunks for cheaper blocks was 20% slower)
+    auto layout = [&](int ly0) {                      // fills S.ly / S.cta0, returns #CTAs
+      int ncta = 0;
+      for (int i = 0; i < nb; ++i) {
+        S.ly[i] = std::max(1, std::min(ly0, g.ny));
+        S.cta0[i] = ncta;
+        ncta += nstrip * ((g.ny + S.ly[i] - 1) / S.ly[i]);
+      }
+      S.cta0[nb] = ncta;
+      return ncta;
+    };
+    int ly0 = ly_env;
+    if (ly0 <= 0) {
+      const long long slots = (long long)(NT > 128 ? 2 : 3) * ctx->num_sms;
+      const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb));
+      ly0 = (int)std::max<long long>(10LL * H, (g.ny + want - 1) / want);
+    }
+    const int ncta = layout(ly0);
     ctx->next_flops = flops;
     LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
-           (k_wave<H, NT><<<dim3(nstrip * nchunk, nb), NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
+           (k_wave<H, NT><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
   }
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
@@ -728,6 +736,11 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
 
 static int wave_passes(aac_ctx* ctx, const NcPlan& P, double* zbase, long long zjs, const IterState* st) {
   if (ctx->wave_h == 4) return wave_passes_t<4, 128>(ctx, P, zbase, zjs, st);
+  // strip width 128 threads (112 columns + 2 x 8 halo); AAC_WAVE_NT=192 selects 176-column
+  // strips (fewer halo columns at nx = 1024, 1152 vs 1280 thread-columns, but 2 instead of 3
+  // CTAs per SM: measured no faster)
+  static const int nt_env = getenv("AAC_WAVE_NT") ? atoi(getenv("AAC_WAVE_NT")) : 0;
+  if (nt_env == 192) return wave_passes_t<8, 192>(ctx, P, zbase, zjs, st);
   return wave_passes_t<8, 128>(ctx, P, zbase, zjs, st);
 }
 

@@ -41,7 +41,11 @@ struct WBlk {
 };
 struct WSweep {
   WBlk b[AAC_MAX_BLK];
-  int nstrip, ly;            // strips of TX columns, rows per chunk
+  int nb;                    // blocks in this launch
+  int nstrip;                // strips of TX columns
+  int ly[AAC_MAX_BLK];       // rows per chunk of each block (equal work per CTA: a block with
+                             // fewer steps or a real plane gets taller chunks)
+  int cta0[AAC_MAX_BLK + 1]; // first CTA of each block (prefix sums of nstrip x chunks)
 };
 
 template <int H, int NT>
@@ -248,24 +252,27 @@ __device__ __forceinline__ void wave_dispatch_ns(const WCtx<H, NT>& C, int ns, b
 }
 
 template <int H, int NT>
-__global__ void __launch_bounds__(NT, H > 4 ? 2 : 3) k_wave(Geo g, WSweep W, const double* __restrict__ what,
+__global__ void __launch_bounds__(NT, NT > 128 ? 2 : 3) k_wave(Geo g, WSweep W, const double* __restrict__ what,
                                                             const IterState* st) {
   using G = WGeom<H, NT>;
   if (st && st->done) return;
   extern __shared__ __align__(16) double wsm[];
   WCtx<H, NT> C;
-  C.B = &W.b[blockIdx.y];
+  int bi = 0;                                           // this CTA's block (flat 1-D grid)
+  while (bi + 1 < W.nb && (int)blockIdx.x >= W.cta0[bi + 1]) ++bi;
+  const int cta = (int)blockIdx.x - W.cta0[bi];
+  C.B = &W.b[bi];
   C.what = what;
   C.g = g;
   C.xch = wsm;
   C.hist = wsm + G::XCH + threadIdx.x;
   C.t = threadIdx.x;
-  const int strip = blockIdx.x % W.nstrip, chunk = blockIdx.x / W.nstrip;
+  const int strip = cta % W.nstrip, chunk = cta / W.nstrip;
   C.x = strip * G::TX - H + C.t;
   C.colin = C.x >= 0 && C.x < g.nx;
   C.colout = C.t >= H && C.t < NT - H && C.x < g.nx;
-  C.y0 = chunk * W.ly;
-  C.y1 = min(C.y0 + W.ly, g.ny);
+  C.y0 = chunk * W.ly[bi];
+  C.y1 = min(C.y0 + W.ly[bi], g.ny);
   // zero pads of the exchange rows and of the history rows (never written)
   for (int k = threadIdx.x; k < 2 * H * 2; k += NT) {
     wsm[k * G::XW] = 0.0;
