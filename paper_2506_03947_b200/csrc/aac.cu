@@ -324,16 +324,18 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   G.wx = ctx->d_w;
   G.wy = ctx->d_w + lenx;
   G.wz = ctx->d_w + lenx + leny;
+  // (a pageable cudaMemcpy may return before its DMA completes; the library stream does not
+  // order after the legacy stream: synchronise the device before any stream work)
   if (cudaMemcpy(ctx->d_w, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(ctx->d_halo, 0, 2LL * ell * G.S * sizeof(double)) != cudaSuccess ||
-      cudaMemset(ctx->d_st, 0, sizeof(IterState)) != cudaSuccess) {
+      cudaMemset(ctx->d_st, 0, sizeof(IterState)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     aac_destroy(ctx);
     return aac_fail(nullptr, AAC_ECUDA, "setup copy failed");
   }
   // global Gershgorin max (all-reduce max over slabs)
   if (ctx->nranks > 1) {
     ctx->h_stat[0] = gmax;
-    cudaMemcpy(ctx->d_stat, ctx->h_stat, sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(ctx->d_stat, ctx->h_stat, sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
     rc = comm_allreduce(ctx, ctx->d_stat, 1, ncclMax);
     if (rc == AAC_OK && cudaStreamSynchronize(ctx->stream) == cudaSuccess)
       cudaMemcpy(&gmax, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost);
@@ -962,7 +964,10 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
     AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
-    if (ctx->nranks > 1) return aac_fail(ctx, AAC_EINVAL, "AAC_SP runs on one rank");
+    if (ctx->nranks > 1) {
+      AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
+      LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+    }
     AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
   } else {
     AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j));

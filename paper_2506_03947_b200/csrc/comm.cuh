@@ -109,12 +109,12 @@ static int comm_allreduce(aac_ctx* ctx, double* d, int n, ncclRedOp_t op) {
 // Halo exchange of the stencil inputs: for each (plane pointer, plane index q) send the
 // first / last slab layer to the rank below / above and receive the neighbours' layers into
 // halo_lo[q] / halo_hi[q]. Layers are contiguous (S doubles), so no packing is needed.
-static int comm_halo(aac_ctx* ctx, const double* const* planes, const int* qs, int count) {
+// General form: layers of S doubles at the start / end (offset N - S) of each plane, received
+// into hlo + q * S / hhi + q * S (any level of the slab decomposition; g carries has_lo/hi).
+static int comm_halo_ex(aac_ctx* ctx, const Geo& g, const double* const* planes, const int* qs,
+                        int count, double* hlo, double* hhi) {
   if (ctx->nranks == 1 || count == 0) return AAC_OK;
-  const Geo& g = ctx->geo;
   const long long S = g.S;
-  double* hlo = ctx->d_halo;
-  double* hhi = ctx->d_halo + (long long)ctx->ell * S;
   if (ctx->host_tr) {
     const long long n = (long long)count * S;
     AAC_TRY(host_stage(ctx, 4 * n));
@@ -158,4 +158,9 @@ static int comm_halo(aac_ctx* ctx, const double* const* planes, const int* qs, i
   }
   NCCL_TRY(ctx, g_nccl.GroupEnd());
   return AAC_OK;
+}
+
+static int comm_halo(aac_ctx* ctx, const double* const* planes, const int* qs, int count) {
+  return comm_halo_ex(ctx, ctx->geo, planes, qs, count, ctx->d_halo,
+                      ctx->d_halo + (long long)ctx->ell * ctx->geo.S);
 }

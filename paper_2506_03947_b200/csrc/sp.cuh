@@ -47,11 +47,15 @@ struct SpConst {               // per-block constants, passed by value
 };
 
 struct SpLevel {               // one multigrid level (device arrays)
-  Geo g;                       // extents + face weights (lower-face convention), no halos
+  Geo g;                       // extents + face weights (lower-face convention); has_lo / has_hi
+                               // on the slab-decomposed levels of a multi-rank run
   double* cnt;                 // Galerkin image of I: fine cells per aggregate
   double* b;                   // [ell][N] right-hand sides (levels >= 1)
   double* x;                   // [ell][N] pre-smoothed iterate
   double* x2;                  // [ell][N] post-smoothed iterate (the level's result, levels >= 1)
+  int local = 1;               // 1: this rank's slab (halo exchanges); 0: the global level
+  Geo gl{};                    // gathered level: this rank's slab of it (extents only) ...
+  long long goff = 0;          // ... and its offset in the global arrays (points)
 };
 
 struct SpPlan {
@@ -69,6 +73,8 @@ struct SpPlan {
   SpBlk* blk = nullptr;        // [h+1]
   double* part = nullptr;      // partials [planes or blocks][tiles]
   unsigned* tick = nullptr;
+  double* red = nullptr;       // multi-rank: local sums for the all-reduce (AAC_MAX_ELL)
+  int gather = -1;             // multi-rank: index of the gathered (first global) level
 };
 
 // ------------------------------------------------------------------------------------------
@@ -78,10 +84,12 @@ __device__ __forceinline__ int sp_block_of(int ell, int pl) {
 }
 
 // A_l(s) u at the point: m u_p + sum_f w_f (u_p - u_nb), m = (1 + s) cnt_p
+// hlo / hhi: the plane's halo layers (slab-decomposed levels; unused when g has no neighbours)
 template <int DIM>
-__device__ __forceinline__ double mg_apply(const Geo& g, const PtV<DIM, 1>& q, const double* u, double m) {
+__device__ __forceinline__ double mg_apply(const Geo& g, const PtV<DIM, 1>& q, const double* u, double m,
+                                           const double* hlo = nullptr, const double* hhi = nullptr) {
   double a[1], c[1];
-  apply_Av<DIM, 1>(g, q, u, nullptr, nullptr, a, c);
+  apply_Av<DIM, 1>(g, q, u, hlo, hhi, a, c);
   return a[0] + (m - 1.0) * c[0];
 }
 
@@ -105,6 +113,10 @@ struct SpStepCtx {
   SpConst K;
   int phase;                   // step B: 0 = initial (gamma / rho), 1 = iteration
   const IterState* st;
+  double* red;                 // multi-rank: the last CTA stores the local sums here (an
+                               // all-reduce and k_sp_scalar follow); NULL: it runs the step
+  const double* hlo;           // level-0 halo layers (slab decomposition), plane stride g.S
+  const double* hhi;
 };
 
 // ---- scalar steps (thread 0 of the last CTA) ---------------------------------------------
@@ -200,12 +212,28 @@ __device__ __forceinline__ void sp_reduce(const SpStepCtx& S, double v, bool ste
   }
   if (t == 0) {
     *S.tick = 0;
-    if (stepB) sp_scalar_B(S, tot);
-    else sp_scalar_A(S, tot);
+    if (S.red) {
+      for (int q = 0; q < (int)gridDim.y; ++q) S.red[q] = tot[q];
+    } else if (stepB) {
+      sp_scalar_B(S, tot);
+    } else {
+      sp_scalar_A(S, tot);
+    }
   }
 }
 
+// Multi-rank: the scalar step on the all-reduced sums.
+__global__ void k_sp_scalar(SpStepCtx S, int stepB) {
+  if (S.st && S.st->done) return;
+  double tot[AAC_MAX_ELL];
+  for (int q = 0; q < AAC_MAX_ELL; ++q) tot[q] = S.red[q];
+  if (stepB) sp_scalar_B(S, tot);
+  else sp_scalar_A(S, tot);
+}
+
 // ---- multigrid kernels (grid: tiles x planes) ----------------------------------------------
+// Slab-decomposed levels carry has_lo / has_hi in their Geo and read the neighbours' boundary
+// layers from hlo / hhi (plane stride g.S).
 // x = omega b / D (pre-smoothing from zero)
 template <int DIM>
 __global__ void __launch_bounds__(SP_T) k_mg_smooth0(Geo g, const double* __restrict__ cnt, SpConst K,
@@ -223,11 +251,15 @@ __global__ void __launch_bounds__(SP_T) k_mg_smooth0(Geo g, const double* __rest
 }
 
 // b_{l+1} = P^T (b - A_l x): one thread per COARSE point sums its children
+// gc: this rank's part of the coarse level; the result goes to bc[pl * cstride + coff + pc]
+// (cstride / coff: the plane stride and slab offset of the coarse array -- the global array of
+// a gathered level, or the local one).
 template <int DIM>
 __global__ void __launch_bounds__(SP_T) k_mg_restrict(Geo g, const double* __restrict__ cnt, Geo gc,
                                                       SpConst K, MgIo io, const double* bl,
                                                       const double* xl, double* bc,
-                                                      const IterState* st) {
+                                                      const IterState* st, const double* hlo,
+                                                      const double* hhi, long long cstride, long long coff) {
   if (st && st->done) return;
   const int pl = blockIdx.y;
   const long long pc = (long long)blockIdx.x * SP_T + threadIdx.x;
@@ -247,9 +279,10 @@ __global__ void __launch_bounds__(SP_T) k_mg_restrict(Geo g, const double* __res
         const long long p = ((long long)fz * g.ny + fy) * g.nx + fx;
         PtV<DIM, 1> q;
         load_ptv<DIM, 1>(g, p, q);
-        acc += b[p] - mg_apply<DIM>(g, q, x, (1.0 + s) * cnt[p]);
+        acc += b[p] - mg_apply<DIM>(g, q, x, (1.0 + s) * cnt[p], hlo + (long long)pl * g.S,
+                                    hhi + (long long)pl * g.S);
       }
-  bc[(long long)pl * gc.N + pc] = acc;
+  bc[(long long)pl * cstride + coff + pc] = acc;
 }
 
 // x_c = A_c(s)^{-1} b_c with the precomputed dense inverse of the plane's block (CTA per plane)
@@ -269,7 +302,7 @@ __global__ void __launch_bounds__(SP_T) k_mg_coarse(int nc, const double* __rest
 // x_l += P x_c (injection from the aggregate)
 template <int DIM>
 __global__ void __launch_bounds__(SP_T) k_mg_prolong(Geo g, Geo gc, double* xl, const double* xc,
-                                                     const IterState* st) {
+                                                     const IterState* st, long long cstride, long long coff) {
   if (st && st->done) return;
   const int pl = blockIdx.y;
   const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
@@ -278,7 +311,7 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong(Geo g, Geo gc, double* xl, 
   const long long r = p / g.nx;
   const int y = (int)(r % g.ny), z = (int)(r / g.ny);
   const long long pc = ((long long)(z / 2) * gc.ny + y / 2) * gc.nx + x / 2;
-  xl[(long long)pl * g.N + p] += xc[(long long)pl * gc.N + pc];
+  xl[(long long)pl * g.N + p] += xc[(long long)pl * cstride + coff + pc];
 }
 
 // x2 = x + omega (b - A x)/D. Level 0: written to io.out[pl], dot partial <x2, b> per plane,
@@ -286,7 +319,8 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong(Geo g, Geo gc, double* xl, 
 template <int DIM>
 __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restrict__ cnt, MgIo io,
                                                   const double* bl, const double* xl, double* x2l,
-                                                  SpStepCtx S, int level0) {
+                                                  SpStepCtx S, int level0, const double* hlo,
+                                                  const double* hhi) {
   if (S.st && S.st->done) return;
   const int pl = blockIdx.y;
   const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
@@ -297,7 +331,9 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
     const double m = (1.0 + S.K.s[pl]) * cnt[p];
     const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
     const double* x = xl + (long long)pl * g.N;
-    const double xn = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m)) / diag_of<DIM>(q, m);
+    const double xn = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m, hlo + (long long)pl * g.S,
+                                                              hhi + (long long)pl * g.S)) /
+                                 diag_of<DIM>(q, m);
     if (level0) {
       io.out[pl][p] = xn;
       dotp = xn * b[p];
@@ -354,15 +390,18 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
     if (kb == 0 || kb == h) {
       const int pl = kb == 0 ? 0 : ell - 1;
       const double* pp = v.P + (long long)pl * N;
-      const double a = mg_apply<DIM>(g, q, pp, 1.0 + S.K.s[pl]);   // (A - Lambda) p
+      const double a = mg_apply<DIM>(g, q, pp, 1.0 + S.K.s[pl], S.hlo + (long long)pl * g.S,
+                                     S.hhi + (long long)pl * g.S);   // (A - Lambda) p
       v.SZ[(long long)pl * N + p] = a;
       dotp = pp[p] * a;
     } else {
       const int qu = 2 * kb - 1, qv = qu + 1;
       const double invg = 1.0 / b.gamma;
       double azu[1], azv[1], zu[1], zv[1];
-      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qu * N, nullptr, nullptr, azu, zu);
-      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qv * N, nullptr, nullptr, azv, zv);
+      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qu * N, S.hlo + (long long)qu * g.S, S.hhi + (long long)qu * g.S,
+                       azu, zu);
+      apply_Av<DIM, 1>(g, q, v.Zc + (long long)qv * N, S.hlo + (long long)qv * g.S, S.hhi + (long long)qv * g.S,
+                       azv, zv);
       const double us = zu[0] * invg, vs = zv[0] * invg;
       const double Au = azu[0] * invg, Av = azv[0] * invg;
       const double lr = S.K.lre[kb], li = S.K.lim[kb];
@@ -463,10 +502,19 @@ static HostLevel coarsen(const HostLevel& f, int dim) {
         const long long pc = ci(X, Y, Z);
         c.cnt[pc] += f.cnt[pf];
         // a fine lower face between two different aggregates adds to the coarse lower face
-        if (x > 0 && (x & 1) == 0) c.wx[pc] += f.wx[pf];
-        if (dim >= 2 && y > 0 && (y & 1) == 0) c.wy[pc] += f.wy[pf];
-        if (dim >= 3 && z > 0 && (z & 1) == 0) c.wz[pc] += f.wz[pf];
+        // (index 0 included: zero on a physical boundary, the face to the neighbour rank's
+        // slab on a slab boundary -- slab boundaries are aggregate boundaries)
+        if ((x & 1) == 0) c.wx[pc] += f.wx[pf];
+        if (dim >= 2 && (y & 1) == 0) c.wy[pc] += f.wy[pf];
+        if (dim >= 3 && (z & 1) == 0) c.wz[pc] += f.wz[pf];
       }
+  // the upper face of the slab (extra layer of the slab axis) when it bounds an aggregate
+  if (dim == 2 && (f.ny & 1) == 0)
+    for (long long x = 0; x < f.nx; ++x) c.wy[(long long)c.ny * c.nx + x / 2] += f.wy[(long long)f.ny * f.nx + x];
+  if (dim == 3 && (f.nz & 1) == 0)
+    for (long long y = 0; y < f.ny; ++y)
+      for (long long x = 0; x < f.nx; ++x)
+        c.wz[(long long)c.nz * c.nx * c.ny + (y / 2) * c.nx + x / 2] += f.wz[(long long)f.nz * f.nx * f.ny + y * f.nx + x];
   return c;
 }
 
@@ -494,7 +542,11 @@ static bool dense_inverse(const HostLevel& c, int dim, double s, std::vector<dou
   for (int j = 0; j < n; ++j) {
     double d = A[(size_t)j * n + j];
     for (int k = 0; k < j; ++k) d -= A[(size_t)j * n + k] * A[(size_t)j * n + k];
-    if (!(d > 0.0)) return false;
+    if (!(d > 0.0)) {
+      if (getenv("AAC_SP_DEBUG"))
+        fprintf(stderr, "[sp] dense Cholesky failed at %d of %d (%dx%dx%d), d=%g s=%g\n", j, n, c.nx, c.ny, c.nz, d, s);
+      return false;
+    }
     d = sqrt(d);
     A[(size_t)j * n + j] = d;
     for (int i = j + 1; i < n; ++i) {
@@ -526,8 +578,6 @@ static void shift_of_block(const aac_ctx* ctx, int kb, double* lr, double* li);
 static int sp_prepare(aac_ctx* ctx, int k) {
   (void)k;
   if (ctx->sp) return AAC_OK;
-  if (ctx->nranks > 1)
-    return aac_fail(ctx, AAC_EINVAL, "AAC_SP runs on one rank (multigrid across slabs not built)");
   SpPlan* P = new SpPlan();
   ctx->sp = P;
   const int ell = ctx->ell, h = ell / 2, dim = ctx->dim;
@@ -561,16 +611,100 @@ static int sp_prepare(aac_ctx* ctx, int k) {
   f.wx.resize(lenx);
   f.wy.resize(leny);
   f.wz.resize(lenz);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(f.wx.data(), g0.wx, lenx * sizeof(double), cudaMemcpyDeviceToHost));
   CUDA_TRY(ctx, cudaMemcpy(f.wy.data(), g0.wy, leny * sizeof(double), cudaMemcpyDeviceToHost));
   CUDA_TRY(ctx, cudaMemcpy(f.wz.data(), g0.wz, lenz * sizeof(double), cudaMemcpyDeviceToHost));
   f.cnt.assign(N, 1.0);
   std::vector<HostLevel> hl{f};
-  while (std::max(hl.back().nx, std::max(hl.back().ny, hl.back().nz)) > SP_COARSE_MAX_AXIS)
-    hl.push_back(coarsen(hl.back(), dim));
-  // device levels
+  int G = -1;                                   // multi-rank: first global (gathered) level
+  long long gLo = 0;                            // this rank's slab start on the gathered level
+  if (ctx->nranks == 1) {
+    while (std::max(hl.back().nx, std::max(hl.back().ny, hl.back().nz)) > SP_COARSE_MAX_AXIS)
+      hl.push_back(coarsen(hl.back(), dim));
+  } else {
+    // Coarsen inside the slabs while every slab boundary is an aggregate boundary of the
+    // GLOBAL hierarchy (even offsets; an odd count only at the top of the domain), so the
+    // levels are exactly those of the one-rank hierarchy; then gather the last local level
+    // on every rank and continue (and solve) redundantly.
+    const int P_ = ctx->nranks;
+    const long long n0 = dim == 2 ? ctx->n[1] : ctx->n[2];
+    std::vector<int64_t> lo(P_), hi(P_);
+    for (int r = 0; r < P_; ++r) aac_slab_range(n0, P_, r, &lo[r], &hi[r]);
+    long long nslab = n0;
+    auto gmax = [&](const HostLevel& H) {
+      return std::max<long long>(H.nx, dim == 2 ? nslab : std::max<long long>(H.ny, nslab));
+    };
+    while (gmax(hl.back()) > SP_COARSE_MAX_AXIS) {
+      bool ok = true;
+      for (int r = 0; r < P_; ++r)
+        ok = ok && lo[r] % 2 == 0 && (hi[r] % 2 == 0 || hi[r] == nslab) && hi[r] - lo[r] >= 2;
+      if (!ok) break;
+      hl.push_back(coarsen(hl.back(), dim));
+      for (int r = 0; r < P_; ++r) {
+        lo[r] /= 2;
+        hi[r] = (hi[r] + 1) / 2;
+      }
+      nslab = (nslab + 1) / 2;
+    }
+    if (hl.size() < 2)
+      return aac_fail(ctx, AAC_EINVAL,
+                      "AAC_SP on %d ranks needs even slab boundaries (slab rows per rank even)", P_);
+    G = (int)hl.size() - 1;
+    gLo = lo[ctx->rank];
+    // global level G: every rank contributes the lower faces / counts of its own layers
+    const HostLevel& Lg = hl.back();
+    HostLevel Gg;
+    Gg.nx = Lg.nx;
+    Gg.ny = dim == 2 ? (int)nslab : Lg.ny;
+    Gg.nz = dim == 3 ? (int)nslab : 1;
+    const long long Ng = (long long)Gg.nx * Gg.ny * Gg.nz, Sg = dim == 3 ? (long long)Gg.nx * Gg.ny : Gg.nx;
+    const long long Nl = (long long)Lg.nx * Lg.ny * Lg.nz, off = gLo * Sg;
+    Gg.wx.assign(pad4l(Ng + 1), 0.0);
+    Gg.wy.assign(pad4l(Ng + Gg.nx), 0.0);
+    Gg.wz.assign(pad4l(Ng + Sg), 0.0);
+    Gg.cnt.assign(Ng, 0.0);
+    const long long tot = (long long)Gg.wx.size() + Gg.wy.size() + Gg.wz.size() + Ng;
+    std::vector<double> buf(tot, 0.0);
+    double* bx = buf.data();
+    double* by = bx + Gg.wx.size();
+    double* bz = by + Gg.wy.size();
+    double* bc = bz + Gg.wz.size();
+    for (long long i = 0; i < Nl; ++i) {
+      bx[off + i] = Lg.wx[i];
+      if (dim >= 2) by[off + i] = Lg.wy[i];
+      if (dim >= 3) bz[off + i] = Lg.wz[i];
+      bc[off + i] = Lg.cnt[i];
+    }
+    double* dbuf = nullptr;
+    AAC_TRY(sp_alloc(ctx, P, &dbuf, tot));
+    // (stream-ordered copies: a pageable cudaMemcpy may return before its DMA completes, and
+    // the library stream does not synchronise with the legacy stream)
+    CUDA_TRY(ctx, cudaMemcpyAsync(dbuf, buf.data(), tot * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    AAC_TRY(comm_allreduce(ctx, dbuf, (int)tot, ncclSum));
+    CUDA_TRY(ctx, cudaMemcpyAsync(buf.data(), dbuf, tot * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::copy(bx, bx + Gg.wx.size(), Gg.wx.begin());
+    std::copy(by, by + Gg.wy.size(), Gg.wy.begin());
+    std::copy(bz, bz + Gg.wz.size(), Gg.wz.begin());
+    std::copy(bc, bc + Ng, Gg.cnt.begin());
+    hl.push_back(Gg);                            // hl[G] = local slab, hl[G + 1] = global level G
+    while (std::max(hl.back().nx, std::max(hl.back().ny, hl.back().nz)) > SP_COARSE_MAX_AXIS)
+      hl.push_back(coarsen(hl.back(), dim));
+  }
+  P->gather = G;
+  // device levels (multi-rank: hl[G] is only the slab geometry of the gathered level hl[G+1])
+  Geo gslab{};
   for (size_t l = 0; l < hl.size(); ++l) {
     const HostLevel& H = hl[l];
+    if (G >= 0 && (int)l == G) {
+      gslab.nx = H.nx;
+      gslab.ny = H.ny;
+      gslab.nz = H.nz;
+      gslab.N = (long long)H.nx * H.ny * H.nz;
+      gslab.S = dim == 3 ? (long long)H.nx * H.ny : H.nx;
+      continue;
+    }
     SpLevel lv{};
     Geo& g = lv.g;
     g.nx = H.nx;
@@ -578,7 +712,13 @@ static int sp_prepare(aac_ctx* ctx, int k) {
     g.nz = H.nz;
     g.N = (long long)H.nx * H.ny * H.nz;
     g.S = dim == 3 ? (long long)H.nx * H.ny : H.nx;
-    g.has_lo = g.has_hi = 0;
+    lv.local = (G < 0 || (int)l < G) ? 1 : 0;
+    g.has_lo = (G >= 0 && lv.local) ? ctx->geo.has_lo : 0;
+    g.has_hi = (G >= 0 && lv.local) ? ctx->geo.has_hi : 0;
+    if (G >= 0 && (int)l == G + 1) {
+      lv.gl = gslab;
+      lv.goff = gLo * g.S;
+    }
     double* w = nullptr;
     const size_t nw = H.wx.size() + H.wy.size() + H.wz.size();
     AAC_TRY(sp_alloc(ctx, P, &w, nw));
@@ -596,6 +736,8 @@ static int sp_prepare(aac_ctx* ctx, int k) {
     if (l > 0) AAC_TRY(sp_alloc(ctx, P, &lv.x2, (long long)ell * g.N));
     P->lev.push_back(lv);
   }
+  if (G >= 0) P->gather = G;                    // index into P->lev of the global level
+  AAC_TRY(sp_alloc(ctx, P, &P->red, AAC_MAX_ELL));
   // coarsest dense inverses, one per block shift
   const HostLevel& Hc = hl.back();
   P->nc = Hc.nx * Hc.ny * Hc.nz;
@@ -623,24 +765,50 @@ static int sp_prepare(aac_ctx* ctx, int k) {
   AAC_TRY(sp_alloc(ctx, P, &tk, 1));
   P->tick = reinterpret_cast<unsigned*>(tk);
   CUDA_TRY(ctx, cudaMemset(P->tick, 0, sizeof(double)));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());     // legacy-stream uploads complete before stream work
   return AAC_OK;
 }
 
+// Halo exchange of the ell planes of a slab-decomposed level (no-op on one rank).
+static int sp_halo(aac_ctx* ctx, const Geo& g, const double* x) {
+  if (ctx->nranks == 1) return AAC_OK;
+  const double* planes[AAC_MAX_ELL];
+  int qs[AAC_MAX_ELL];
+  for (int pl = 0; pl < ctx->ell; ++pl) {
+    planes[pl] = x + (long long)pl * g.N;
+    qs[pl] = pl;
+  }
+  return comm_halo_ex(ctx, g, planes, qs, ctx->ell, ctx->d_halo, ctx->d_halo + (long long)ctx->ell * ctx->geo.S);
+}
+
+// One V(1,1) cycle on all ell planes. Multi-rank: the slab-decomposed levels exchange halos
+// after the pre-smoothing (restriction stencil) and after the prolongation (post-smoothing
+// stencil); the restriction into the gathered level writes this rank's rows of the zeroed
+// global right-hand side, which an all-reduce completes on every rank; the global levels run
+// redundantly and the prolongation back reads this rank's rows of their result.
 template <int DIM>
 static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
   SpPlan* P = ctx->sp;
   const int ell = P->ell;
   const int nl = (int)P->lev.size();
   const IterState* st = S.st;
+  const double* hlo = ctx->d_halo;
+  const double* hhi = ctx->d_halo + (long long)ell * ctx->geo.S;
   for (int l = 0; l < nl - 1; ++l) {                       // down
     SpLevel& a = P->lev[l];
     SpLevel& c = P->lev[l + 1];
     const double* bl = l == 0 ? nullptr : a.b;
-    const dim3 gf(grid1d(a.g.N, SP_T), ell), gc(grid1d(c.g.N, SP_T), ell);
+    const bool gat = a.local && !c.local;                  // restriction into the gathered level
+    const Geo& gcl = gat ? c.gl : c.g;                     // this rank's part of the coarse level
+    const dim3 gf(grid1d(a.g.N, SP_T), ell), gc(grid1d(gcl.N, SP_T), ell);
     LAUNCH(ctx, KID_SP_MG, 16.0 * ell * a.g.N,
            k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, P->K, io, bl, a.x, st));
+    if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
+    if (gat) CUDA_TRY(ctx, cudaMemsetAsync(c.b, 0, (size_t)ell * c.g.N * sizeof(double), ctx->stream));
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_restrict<DIM><<<gc, SP_T, 0, ctx->stream>>>(a.g, a.cnt, c.g, P->K, io, bl, a.x, c.b, st));
+           k_mg_restrict<DIM><<<gc, SP_T, 0, ctx->stream>>>(a.g, a.cnt, gcl, P->K, io, bl, a.x, c.b, st, hlo,
+                                                            hhi, c.g.N, gat ? c.goff : 0));
+    if (gat) AAC_TRY(comm_allreduce(ctx, c.b, (int)(ell * c.g.N), ncclSum));
   }
   SpLevel& cl = P->lev[nl - 1];
   if (nl == 1) return aac_fail(ctx, AAC_EINVAL, "SP needs at least one coarsening (grid too small)");
@@ -650,11 +818,15 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     SpLevel& a = P->lev[l];
     SpLevel& c = P->lev[l + 1];
     const double* bl = l == 0 ? nullptr : a.b;
+    const bool gat = a.local && !c.local;
     const dim3 gf(grid1d(a.g.N, SP_T), ell);
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, c.g, a.x, c.x2, st));
+           k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, gat ? c.gl : c.g, a.x, c.x2, st, c.g.N,
+                                                           gat ? c.goff : 0));
+    if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_post<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0));
+           k_mg_post<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
+                                                        hlo, hhi));
   }
   return AAC_OK;
 }
@@ -688,18 +860,40 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     }
     return io;
   };
-  SpStepCtx S{P->blk, P->part, P->tick, P->K, 0, st};
+  const bool multi = ctx->nranks > 1;
+  SpStepCtx S{P->blk, P->part, P->tick, P->K, 0, st, multi ? P->red : nullptr, ctx->d_halo,
+              ctx->d_halo + (long long)ell * ctx->geo.S};
+  // multi-rank: all-reduce the local sums of the last kernel, then the scalar step
+  auto finish = [&](int nq, int stepB) -> int {
+    if (!multi) return AAC_OK;
+    AAC_TRY(comm_allreduce(ctx, P->red, nq, ncclSum));
+    LAUNCH(ctx, KID_SCALAR, 0, k_sp_scalar<<<1, 1, 0, ctx->stream>>>(S, stepB));
+    return AAC_OK;
+  };
   const unsigned gt = grid1d(N, SP_T);
   LAUNCH(ctx, KID_SP_VEC, 2.0 * V, k_sp_init<<<gt, SP_T, 0, ctx->stream>>>(N, ell, vecs(), st));
   S.phase = 0;
   AAC_TRY(sp_vcycle<DIM>(ctx, io_for(true), S));          // z_1 = M v_1 ; p_0 = M r_0
+  AAC_TRY(finish(ell, 1));
   S.phase = 1;
   for (int it = 0; it < k; ++it) {
+    if (multi) {                                           // halos of P (real) and Z (complex)
+      const double* planes[AAC_MAX_ELL];
+      int qs[AAC_MAX_ELL];
+      for (int pl = 0; pl < ell; ++pl) {
+        const int kb = pl == 0 ? 0 : (pl == ell - 1 ? h : (pl + 1) / 2);
+        planes[pl] = ((kb == 0 || kb == h) ? P->P : Zc) + (long long)pl * N;
+        qs[pl] = pl;
+      }
+      AAC_TRY(comm_halo(ctx, planes, qs, ell));
+    }
     LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
            k_sp_apply<DIM><<<dim3(gt, h + 1), SP_T, 0, ctx->stream>>>(ctx->geo, vecs(), S));
+    AAC_TRY(finish(h + 1, 0));
     LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
            k_sp_upd1<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
     AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
+    AAC_TRY(finish(ell, 1));
     LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
            k_sp_upd2<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
     // rotate: v_prev <- v <- v_next, z <- z_next, w_prev <- w <- w_next

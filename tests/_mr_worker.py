@@ -47,11 +47,15 @@ def main():
     out["x"] = xs.cpu().numpy()
     out["iters"] = info["iters"]
     out["relres_true"] = info["relres_true"]
-    try:
-        s.precond_apply("sp", 2, local(r))
+    try:                                           # SP needs even slab boundaries
+        out["z_sp"] = s.precond_apply("sp", case["k_sp"], local(r)).cpu().numpy()
+        xsp, isp = s.gmres("sp", case["k_sp"], local(p.b), rtol=p.rtol, maxit=60)
+        out["x_sp"] = xsp.cpu().numpy()
+        out["iters_sp"] = isp["iters"]
         out["sp_error"] = 0
-    except AacError:
+    except AacError as e:
         out["sp_error"] = 1
+        out["sp_msg"] = str(e)
     s.close()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), **out)
     dist.barrier()

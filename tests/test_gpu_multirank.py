@@ -6,7 +6,9 @@ group (include/aac.h, aac_setup_host_transport), so the ranks never run kernels 
 each other. This exercises every slab-specific piece of the CUDA path -- halo layers in the
 stencil kernels, slab face weights, local partial sums + all-reduce in the Arnoldi and norm
 steps, the Gershgorin max -- against the single-domain oracle. (The NCCL transport differs only
-in who moves the same buffers; it needs one GPU per rank.)
+in who moves the same buffers; it needs one GPU per rank.) The saddle-point solver's multigrid
+coarsens inside the slabs and gathers the first level whose slab boundaries are no longer
+aggregate boundaries, so its hierarchy -- and its result -- equals the one-rank oracle's.
 """
 import json
 import os
@@ -47,11 +49,14 @@ def _rel(a, b):
     return np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b))
 
 
+# sp: whether the saddle-point solver can run on that split (its multigrid coarsens inside the
+# slabs, so every slab boundary must be even -- otherwise aac_* returns AAC_EINVAL)
 CASES = [
-    (2, dict(name="headline", kw=dict(shape=(1, 37, 29)), method="nc2", k=8)),
-    (3, dict(name="headline", kw=dict(shape=(1, 40, 33)), method="nc2", k=8)),
-    (2, dict(name="3d", kw=dict(shape=(10, 9, 8)), method="nc1", k=10)),
-    (3, dict(name="3d", kw=dict(shape=(7, 6, 9), ell=4), method="nc2", k=5)),
+    (2, dict(name="headline", kw=dict(shape=(1, 40, 29)), method="nc2", k=8, k_sp=3, sp=True)),
+    (3, dict(name="headline", kw=dict(shape=(1, 36, 33)), method="nc2", k=8, k_sp=3, sp=True)),
+    (2, dict(name="headline", kw=dict(shape=(1, 37, 29)), method="nc2", k=8, k_sp=3, sp=False)),
+    (2, dict(name="3d", kw=dict(shape=(12, 9, 8)), method="nc1", k=10, k_sp=2, sp=True)),
+    (3, dict(name="3d", kw=dict(shape=(7, 6, 9), ell=4), method="nc2", k=5, k_sp=2, sp=False)),
 ]
 
 
@@ -83,4 +88,16 @@ def test_multirank_slabs_match_oracle(tmp_path, world, case):
     assert len(its) == 1 and abs(its.pop() - ro.iters) <= 1
     assert _rel(_stitch(parts, "x", p), ro.x) <= 1e-9
     assert all(float(d["relres_true"]) <= 1.5 * p.rtol for d in parts)
-    assert all(int(d["sp_error"]) == 1 for d in parts)        # SP is single-rank
+    if not case["sp"]:
+        assert all(int(d["sp_error"]) == 1 for d in parts)    # odd slab boundary: clean error
+        return
+    from oracle import saddle
+    assert all(int(d["sp_error"]) == 0 for d in parts), [str(d.get("sp_msg")) for d in parts]
+    lev = saddle.hierarchy(w)
+    zsp = saddle.sp_apply(w, rr, p.ell, p.alpha, case["k_sp"], lev)
+    assert _rel(_stitch(parts, "z_sp", p), zsp) <= 1e-12
+    rs = og.fgmres(lambda v: op.apply_allatonce(w, v),
+                   lambda v: saddle.sp_apply(w, v, p.ell, p.alpha, case["k_sp"], lev), p.b, p.rtol, 60)
+    its = {int(d["iters_sp"]) for d in parts}
+    assert len(its) == 1 and abs(its.pop() - rs.iters) <= 1
+    assert _rel(_stitch(parts, "x_sp", p), rs.x) <= 1e-9
