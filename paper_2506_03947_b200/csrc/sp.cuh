@@ -323,9 +323,11 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
                                                   const double* hhi) {
   if (S.st && S.st->done) return;
   const int pl = blockIdx.y;
-  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
   double dotp = 0.0;
-  if (p < g.N) {
+  // grid-stride over tiles: on level 0 the grid is kept small, because every CTA of a
+  // reducing kernel takes a ticket on ONE counter (tens of thousands of same-address atomics
+  // serialised in L2 cost more than the kernel's memory traffic)
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < g.N; p += (long long)gridDim.x * SP_T) {
     PtV<DIM, 1> q;
     load_ptv<DIM, 1>(g, p, q);
     const double m = (1.0 + S.K.s[pl]) * cnt[p];
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
                                  diag_of<DIM>(q, m);
     if (level0) {
       io.out[pl][p] = xn;
-      dotp = xn * b[p];
+      dotp = fma(xn, b[p], dotp);
     } else {
       x2l[(long long)pl * g.N + p] = xn;
     }
@@ -381,10 +383,10 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
   if (S.st && S.st->done) return;
   const int kb = blockIdx.y, ell = S.K.ell, h = ell / 2;
   const long long N = g.N;
-  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
   const SpBlk& b = S.blk[kb];
   double dotp = 0.0;
-  if (p < N && !b.stop) {
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N && !b.stop;
+       p += (long long)gridDim.x * SP_T) {     // grid-stride: few reducing CTAs (see k_mg_post)
     PtV<DIM, 1> q;
     load_ptv<DIM, 1>(g, p, q);
     if (kb == 0 || kb == h) {
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
       const double a = mg_apply<DIM>(g, q, pp, 1.0 + S.K.s[pl], S.hlo + (long long)pl * g.S,
                                      S.hhi + (long long)pl * g.S);   // (A - Lambda) p
       v.SZ[(long long)pl * N + p] = a;
-      dotp = pp[p] * a;
+      dotp = fma(pp[p], a, dotp);
     } else {
       const int qu = 2 * kb - 1, qv = qu + 1;
       const double invg = 1.0 / b.gamma;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
       const double Sv = (Au - lr * us) - li * vs;
       v.SZ[(long long)qu * N + p] = Su;
       v.SZ[(long long)qv * N + p] = Sv;
-      dotp = Su * us + Sv * vs;
+      dotp = fma(Sv, vs, fma(Su, us, dotp));
     }
   }
   sp_reduce(S, dotp, false);
@@ -820,12 +822,13 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     const double* bl = l == 0 ? nullptr : a.b;
     const bool gat = a.local && !c.local;
     const dim3 gf(grid1d(a.g.N, SP_T), ell);
+    const dim3 gp(l == 0 ? std::min<unsigned>(gf.x, std::max(1, 8 * ctx->num_sms / ell)) : gf.x, ell);
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
            k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, gat ? c.gl : c.g, a.x, c.x2, st, c.g.N,
                                                            gat ? c.goff : 0));
     if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_post<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
+           k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
                                                         hlo, hhi));
   }
   return AAC_OK;
@@ -888,7 +891,8 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
       AAC_TRY(comm_halo(ctx, planes, qs, ell));
     }
     LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
-           k_sp_apply<DIM><<<dim3(gt, h + 1), SP_T, 0, ctx->stream>>>(ctx->geo, vecs(), S));
+           k_sp_apply<DIM><<<dim3(std::min<unsigned>(gt, std::max(1, 8 * ctx->num_sms / (h + 1))), h + 1), SP_T, 0,
+                              ctx->stream>>>(ctx->geo, vecs(), S));
     AAC_TRY(finish(h + 1, 0));
     LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
            k_sp_upd1<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
