@@ -346,6 +346,103 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
   if (level0) sp_reduce(S, dotp, true);
 }
 
+// ---- coarse tail of the V-cycle in ONE launch ----------------------------------------------
+// Levels T..L (all global, each <= SP_TAIL_MAX points) for one plane per CTA: the same
+// smoothing / restriction / dense solve / prolongation / post-smoothing steps as the per-level
+// kernels, separated by __syncthreads instead of kernel boundaries (the small levels are
+// launch- and latency-bound: ~16 launches of a few hundred points each per cycle).
+constexpr int SP_TAIL_MAX = 4096;
+constexpr int SP_TAIL_T = 1024;
+constexpr int SP_TAIL_LEV = 8;
+struct MgTail {
+  int nlev;                      // levels T .. T + nlev - 1 (the last one is the coarsest)
+  Geo g[SP_TAIL_LEV];
+  const double* cnt[SP_TAIL_LEV];
+  double* b[SP_TAIL_LEV];        // b[0] = the tail's input (written by the level above)
+  double* x[SP_TAIL_LEV];
+  double* x2[SP_TAIL_LEV];       // x2[0] = the tail's output
+  const double* minv;
+  int nc;
+};
+
+template <int DIM>
+__device__ __forceinline__ void tail_xyz(const Geo& g, long long p, int& x, int& y, int& z) {
+  x = (int)(p % g.nx);
+  const long long r = p / g.nx;
+  y = (int)(r % g.ny);
+  z = (int)(r / g.ny);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(SP_TAIL_T) k_mg_tail(MgTail T, SpConst K, const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.x;
+  const double s = K.s[pl];
+  const int t = threadIdx.x;
+  for (int l = 0; l + 1 < T.nlev; ++l) {                   // down
+    const Geo& g = T.g[l];
+    const Geo& gc = T.g[l + 1];
+    const double* b = T.b[l] + (long long)pl * g.N;
+    double* x = T.x[l] + (long long)pl * g.N;
+    for (long long p = t; p < g.N; p += blockDim.x) {
+      PtV<DIM, 1> q;
+      load_ptv<DIM, 1>(g, p, q);
+      x[p] = SP_OMEGA * b[p] / diag_of<DIM>(q, (1.0 + s) * T.cnt[l][p]);
+    }
+    __syncthreads();
+    double* bc = T.b[l + 1] + (long long)pl * gc.N;
+    for (long long pc = t; pc < gc.N; pc += blockDim.x) {
+      int X, Y, Z;
+      tail_xyz<DIM>(gc, pc, X, Y, Z);
+      double acc = 0.0;
+      for (int dz = 0; dz < (DIM >= 3 ? 2 : 1); ++dz)
+        for (int dy = 0; dy < (DIM >= 2 ? 2 : 1); ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            const int fx = 2 * X + dx, fy = DIM >= 2 ? 2 * Y + dy : 0, fz = DIM >= 3 ? 2 * Z + dz : 0;
+            if (fx >= g.nx || fy >= g.ny || fz >= g.nz) continue;
+            PtV<DIM, 1> q;
+            load_ptv_xyz<DIM, 1>(g, fx, fy, fz, q);
+            acc += b[q.p] - mg_apply<DIM>(g, q, x, (1.0 + s) * T.cnt[l][q.p]);
+          }
+      bc[pc] = acc;
+    }
+    __syncthreads();
+  }
+  {                                                        // coarsest: dense solve
+    const int nc = T.nc, L = T.nlev - 1;
+    const double* M = T.minv + (long long)sp_block_of(K.ell, pl) * nc * nc;
+    const double* b = T.b[L] + (long long)pl * nc;
+    double* xc = T.x2[L] + (long long)pl * nc;
+    for (int i = t; i < nc; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < nc; ++k) acc = fma(M[(long long)i * nc + k], b[k], acc);
+      xc[i] = acc;
+    }
+    __syncthreads();
+  }
+  for (int l = T.nlev - 2; l >= 0; --l) {                  // up
+    const Geo& g = T.g[l];
+    const Geo& gc = T.g[l + 1];
+    double* x = T.x[l] + (long long)pl * g.N;
+    const double* xc = T.x2[l + 1] + (long long)pl * gc.N;
+    for (long long p = t; p < g.N; p += blockDim.x) {
+      int xx, yy, zz;
+      tail_xyz<DIM>(g, p, xx, yy, zz);
+      x[p] += xc[((long long)(zz / 2) * gc.ny + yy / 2) * gc.nx + xx / 2];
+    }
+    __syncthreads();
+    const double* b = T.b[l] + (long long)pl * g.N;
+    double* x2 = T.x2[l] + (long long)pl * g.N;
+    for (long long p = t; p < g.N; p += blockDim.x) {
+      PtV<DIM, 1> q;
+      load_ptv<DIM, 1>(g, p, q);
+      const double m = (1.0 + s) * T.cnt[l][p];
+      x2[p] = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m)) / diag_of<DIM>(q, m);
+    }
+    __syncthreads();
+  }
+}
+
 // ---- Krylov kernels -------------------------------------------------------------------------
 struct SpVec {
   double* X;
@@ -796,7 +893,19 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
   const IterState* st = S.st;
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * ctx->geo.S;
-  for (int l = 0; l < nl - 1; ++l) {                       // down
+  // first level of the fused coarse tail: global, <= SP_TAIL_MAX points, and not level 0
+  // (level 0 takes the V-cycle's input and output pointers); AAC_SP_TAIL=0 disables it
+  static const bool tail_on = !(getenv("AAC_SP_TAIL") && atoi(getenv("AAC_SP_TAIL")) == 0);
+  int tl = nl;                                             // nl: no tail
+  if (tail_on)
+    for (int l = 1; l < nl; ++l)
+      if (!(P->lev[l].local && ctx->nranks > 1) && P->lev[l].g.N <= SP_TAIL_MAX && nl - l <= SP_TAIL_LEV &&
+          nl - l >= 2) {
+        tl = l;
+        break;
+      }
+  const int ldown = tl < nl ? tl : nl - 1;                 // per-level kernels above the tail
+  for (int l = 0; l < ldown; ++l) {                        // down
     SpLevel& a = P->lev[l];
     SpLevel& c = P->lev[l + 1];
     const double* bl = l == 0 ? nullptr : a.b;
@@ -814,9 +923,27 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
   }
   SpLevel& cl = P->lev[nl - 1];
   if (nl == 1) return aac_fail(ctx, AAC_EINVAL, "SP needs at least one coarsening (grid too small)");
-  LAUNCH(ctx, KID_SP_MG, 8.0 * ell * P->nc * P->nc,
-         k_mg_coarse<<<ell, SP_T, 0, ctx->stream>>>(P->nc, P->minv, ell, cl.b, cl.x2, st));
-  for (int l = nl - 2; l >= 0; --l) {                      // up
+  if (tl < nl) {
+    MgTail T{};
+    T.nlev = nl - tl;
+    double bytes = 8.0 * ell * P->nc * P->nc;
+    for (int i = 0; i < T.nlev; ++i) {
+      const SpLevel& L = P->lev[tl + i];
+      T.g[i] = L.g;
+      T.cnt[i] = L.cnt;
+      T.b[i] = L.b;
+      T.x[i] = L.x;
+      T.x2[i] = L.x2;
+      bytes += 8.0 * ell * L.g.N * 6;
+    }
+    T.minv = P->minv;
+    T.nc = P->nc;
+    LAUNCH(ctx, KID_SP_MG, bytes, k_mg_tail<DIM><<<ell, SP_TAIL_T, 0, ctx->stream>>>(T, P->K, st));
+  } else {
+    LAUNCH(ctx, KID_SP_MG, 8.0 * ell * P->nc * P->nc,
+           k_mg_coarse<<<ell, SP_T, 0, ctx->stream>>>(P->nc, P->minv, ell, cl.b, cl.x2, st));
+  }
+  for (int l = (tl < nl ? tl : nl - 1) - 1; l >= 0; --l) { // up
     SpLevel& a = P->lev[l];
     SpLevel& c = P->lev[l + 1];
     const double* bl = l == 0 ? nullptr : a.b;
