@@ -346,6 +346,54 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
   if (level0) sp_reduce(S, dotp, true);
 }
 
+// Prolongation fused into the post-smoothing (saves the prolonged iterate's write and re-read):
+// xt = x + P x_c evaluated at the point and its stencil neighbours (halo layers: the neighbour
+// rank's x AFTER its own prolongation, i.e. exchanged by the caller -- so on slab-decomposed
+// levels the unfused pair k_mg_prolong + halo + k_mg_post is used instead).
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_prolong_post(Geo g, const double* __restrict__ cnt, Geo gc,
+                                                          MgIo io, const double* bl, const double* xl,
+                                                          const double* __restrict__ xc, double* x2l,
+                                                          SpStepCtx S, int level0) {
+  if (S.st && S.st->done) return;
+  const int pl = blockIdx.y;
+  double dotp = 0.0;
+  const double* x = xl + (long long)pl * g.N;
+  const double* xcp = xc + (long long)pl * gc.N;
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < g.N; p += (long long)gridDim.x * SP_T) {
+    PtV<DIM, 1> q;
+    load_ptv<DIM, 1>(g, p, q);
+    const Nbr nb = nbr<DIM, 1>(g, q, x, nullptr, nullptr);
+    // aggregates of the point and its neighbours from the coordinates (a boundary neighbour
+    // aliases the point and so its aggregate)
+    auto agg = [&](int xx, int yy, int zz) { return ((long long)(zz / 2) * gc.ny + yy / 2) * gc.nx + xx / 2; };
+    const long long ac = agg(q.x, q.y, q.z);
+    const double u0 = *nb.c + xcp[ac];
+    const double m = (1.0 + S.K.s[pl]) * (cnt ? cnt[p] : 1.0);
+    double a = m * u0;
+    a = fma(q.wx[0], u0 - (*nb.w + xcp[q.x > 0 ? agg(q.x - 1, q.y, q.z) : ac]), a);
+    a = fma(q.wx[1], u0 - (*nb.e + xcp[q.x < g.nx - 1 ? agg(q.x + 1, q.y, q.z) : ac]), a);
+    if constexpr (DIM >= 2) {
+      a = fma(q.wym[0], u0 - (*nb.n + xcp[q.y > 0 ? agg(q.x, q.y - 1, q.z) : ac]), a);
+      a = fma(q.wyp[0], u0 - (*nb.s + xcp[q.y < g.ny - 1 ? agg(q.x, q.y + 1, q.z) : ac]), a);
+    }
+    if constexpr (DIM >= 3) {
+      a = fma(q.wzm[0], u0 - (*nb.d + xcp[q.z > 0 ? agg(q.x, q.y, q.z - 1) : ac]), a);
+      a = fma(q.wzp[0], u0 - (*nb.u + xcp[q.z < g.nz - 1 ? agg(q.x, q.y, q.z + 1) : ac]), a);
+    }
+    const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
+    const double bp = b[p];
+    const double xn = u0 + SP_OMEGA * (bp - a) / diag_of<DIM>(q, m);
+    if (level0) {
+      io.out[pl][p] = xn;
+      dotp = fma(xn, bp, dotp);
+    } else {
+      x2l[(long long)pl * g.N + p] = xn;
+    }
+  }
+  if (level0) sp_reduce(S, dotp, true);
+}
+
 // ---- coarse tail of the V-cycle in ONE launch ----------------------------------------------
 // Levels T..L (all global, each <= SP_TAIL_MAX points) for one plane per CTA: the same
 // smoothing / restriction / dense solve / prolongation / post-smoothing steps as the per-level
@@ -950,13 +998,19 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     const bool gat = a.local && !c.local;
     const dim3 gf(grid1d(a.g.N, SP_T), ell);
     const dim3 gp(l == 0 ? std::min<unsigned>(gf.x, std::max(1, 8 * ctx->num_sms / ell)) : gf.x, ell);
-    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, gat ? c.gl : c.g, a.x, c.x2, st, c.g.N,
-                                                           gat ? c.goff : 0));
-    if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
-    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
-                                                        hlo, hhi));
+    if (ctx->nranks > 1 && a.local) {                      // slab level: prolong, halo, post
+      LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+             k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, gat ? c.gl : c.g, a.x, c.x2, st, c.g.N,
+                                                             gat ? c.goff : 0));
+      AAC_TRY(sp_halo(ctx, a.g, a.x));
+      LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+             k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
+                                                          hlo, hhi));
+    } else {                                               // x, x_c, b in; x2 out (+ C)
+      LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
+             k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, c.g, io, bl, a.x, c.x2, a.x2, S,
+                                                                  l == 0 ? 1 : 0));
+    }
   }
   return AAC_OK;
 }
