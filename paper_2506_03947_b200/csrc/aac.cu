@@ -312,6 +312,7 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
             alloc(&ctx->d_red, 3LL * ldh + 8) && alloc(&ctx->d_H, (long long)ldh * max_krylov) &&
             alloc(&ctx->d_G, (long long)ldh * ldh) && alloc(&ctx->d_giv, 6LL * ldh) &&
             alloc(&ctx->d_stat, 64) &&
+            cudaMalloc((void**)&ctx->d_grp, (size_t)(ctx->part_len / 32 + 2) * sizeof(unsigned)) == cudaSuccess &&
             cudaMalloc((void**)&ctx->d_st, sizeof(IterState)) == cudaSuccess;
   if (ok) ok = cudaMallocHost((void**)&ctx->h_stat, 64 * sizeof(double)) == cudaSuccess &&
                cudaMallocHost((void**)&ctx->h_st, sizeof(IterState)) == cudaSuccess;
@@ -328,7 +329,9 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   // order after the legacy stream: synchronise the device before any stream work)
   if (cudaMemcpy(ctx->d_w, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(ctx->d_halo, 0, 2LL * ell * G.S * sizeof(double)) != cudaSuccess ||
-      cudaMemset(ctx->d_st, 0, sizeof(IterState)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaMemset(ctx->d_st, 0, sizeof(IterState)) != cudaSuccess ||
+      cudaMemset(ctx->d_grp, 0, (size_t)(ctx->part_len / 32 + 2) * sizeof(unsigned)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
     aac_destroy(ctx);
     return aac_fail(nullptr, AAC_ECUDA, "setup copy failed");
   }
@@ -362,6 +365,7 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   for (double* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_st) cudaFree(ctx->d_st);
+  if (ctx->d_grp) cudaFree(ctx->d_grp);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};
@@ -612,7 +616,7 @@ static int smem_optin(aac_ctx* ctx, K kernel, size_t bytes) {
 template <int ELLC, bool TMA>
 static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
   const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
-  FwdUpd U{ctx->d_W, ctx->d_V, L, ctx->d_part, arnoldi_ctx(ctx)};
+  FwdUpd U{ctx->d_W, ctx->d_V, L, ctx->d_part, arnoldi_ctx(ctx), ctx->d_grp};
   const Dft D = make_dft(ctx);
   const size_t smem = TMA ? (size_t)FS * ELLC * FT * sizeof(double) : 0;
   AAC_TRY(smem_optin(ctx, k_fwd_upd<ELLC, TMA>, smem));

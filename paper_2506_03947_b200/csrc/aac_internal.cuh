@@ -100,6 +100,7 @@ struct aac_ctx {
   double* d_bx = nullptr;              // [2][ell][N] staging for aac_gmres_host
   double* d_halo = nullptr;            // [2][ell][S]  lo | hi
   double* d_part = nullptr;            // per-CTA partial sums
+  unsigned* d_grp = nullptr;           // two-level ticket counters (zeroed)
   long long part_len = 0;
   double* d_red = nullptr;             // reduced sums / scratch (3 * ldh)
   double* d_H = nullptr;               // Hessenberg ldh x max_krylov, col-major

@@ -48,6 +48,7 @@ struct FwdUpd {
   long long L;
   double* part;              // per-CTA partials of ||u||^2
   ArnoldiCtx ac;             // st, sigma, c (CGS2 coefficients of column j-1), Givens state
+  unsigned* grp;             // per-32-CTA ticket counters (zero between launches)
 };
 
 // gamma-scale + real -> packed half-complex DFT of the ell values w[] of one point.
@@ -202,8 +203,17 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
     for (int w2 = 0; w2 < FW; ++w2) tot += red[w2];
     U.part[blockIdx.x] = tot;
     __threadfence();
-    const unsigned tk = atomicAdd(&st->tick, 1u);
-    last = (tk == gridDim.x - 1);
+    // two-level ticket: thousands of CTAs taking a ticket on ONE counter serialise in L2;
+    // the last CTA of each group of 32 takes the global ticket (and resets its group counter)
+    const unsigned gid = blockIdx.x >> 5;
+    const unsigned gsz = min(32u, gridDim.x - (gid << 5));
+    bool lst = false;
+    if (atomicAdd(&U.grp[gid], 1u) == gsz - 1) {
+      U.grp[gid] = 0;
+      __threadfence();
+      lst = atomicAdd(&st->tick, 1u) == ((gridDim.x + 31) >> 5) - 1;
+    }
+    last = lst;
   }
   __syncthreads();
   if (last) {
