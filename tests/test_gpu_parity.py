@@ -307,3 +307,59 @@ def test_precond_sweep_organisations(monkeypatch, kw, method, k, h, ly):
     assert abs(info["iters"] - ro.iters) <= 1
     assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
     s.close()
+
+
+# ---------------------------------------------------------------- full-size 3D (configs[4])
+def _sub_weights(w, lo, hi):
+    """Face weights of the box [lo, hi) of the full grid (faces inside the box only): the box
+    is its own Neumann problem, identical to the full one within its interior."""
+    sub = op.Weights.__new__(op.Weights)
+    (z0, y0, x0), (z1, y1, x1) = lo, hi
+    sub.shape = (z1 - z0, y1 - y0, x1 - x0)
+    sub.wx = w.wx[z0:z1, y0:y1, x0:x1 - 1]
+    sub.wy = w.wy[z0:z1, y0:y1 - 1, x0:x1]
+    sub.wz = w.wz[z0:z1 - 1, y0:y1, x0:x1]
+    return sub
+
+
+def test_3d_full_size_sampled_parity():
+    """calA and P_NC1 (k = 10) at 256^3, ell = 12 -- the bench launch configuration -- on sampled
+    points. The preconditioner is a polynomial of degree p - 1 = 9 in A per Fourier block, so its
+    value at a point depends only on r within 9 cells: the oracle on a 25^3 box around the point
+    (the box is a Neumann problem that agrees with the full one inside) gives the exact value."""
+    p = synth.make_problem("3d")
+    s = _solver(p, max_krylov=16)
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    assert s.mu_max == pytest.approx(mu, rel=1e-14)
+    r = np.random.default_rng(13).standard_normal((p.ell,) + p.shape)
+    rd = _dev(r, p.ell)
+    y = s.matvec(rd).cpu().numpy().reshape((p.ell,) + p.shape)
+    z = s.precond_apply("nc1", p.k, rd).cpu().numpy().reshape((p.ell,) + p.shape)
+    del rd
+    n = p.shape[0]
+    R = 12
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * p.k, "nc1", p.k)
+    for pt in [(0, 0, 0), (5, 130, 255), (128, 127, 129), (255, 3, 77), (200, 255, 0)]:
+        lo = tuple(max(0, c - R) for c in pt)
+        hi = tuple(min(n, c + R + 1) for c in pt)
+        sub = _sub_weights(w, lo, hi)
+        sl = (slice(None),) + tuple(slice(a, b) for a, b in zip(lo, hi))
+        ctr = (slice(None),) + tuple(c - a for c, a in zip(pt, lo))
+        yo = op.apply_allatonce(sub, r[sl]).reshape((p.ell,) + sub.shape)[ctr]
+        zo = ch.nc_apply(sub, r[sl], p.ell, p.alpha, 1.0, mu, al).reshape((p.ell,) + sub.shape)[ctr]
+        gi = (slice(None),) + pt
+        assert _rel(y[gi], yo) <= 1e-12, pt
+        assert _rel(z[gi], zo) <= 1e-12, pt
+    s.close()
+
+
+def test_3d_full_size_gmres_properties():
+    """configs[4] solve at full size: converged to rtol on the TRUE residual, iteration count in
+    the band the survey's 64^3 proxy and the 1-GPU bench show (11)."""
+    p = synth.make_problem("3d")
+    s = _solver(p, max_krylov=16)
+    x, info = s.gmres("nc1", p.k, _dev(p.b, p.ell), rtol=p.rtol, maxit=16)
+    assert info["converged"] == 1 and 9 <= info["iters"] <= 13
+    assert info["relres_true"] <= 1.5 * p.rtol
+    s.close()
