@@ -335,6 +335,36 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
     aac_destroy(ctx);
     return aac_fail(nullptr, AAC_ECUDA, "setup copy failed");
   }
+  // slab-decomposed wavefront (2D): face weights of the slab +- WAVE_MAXH rows, halo buffers
+  if (ctx->nranks > 1 && g->dim == 2) {
+    const int hd = WAVE_MAXH;
+    bool thick = true;
+    for (int r = 0; r < g->nranks; ++r) {
+      int64_t rl, rh;
+      aac_slab_range(ny, g->nranks, r, &rl, &rh);
+      thick = thick && rh - rl >= hd;
+    }
+    if (thick) {
+      const long long elo = std::max<long long>(0, lo - hd), ehi = std::min<long long>(ny, hi + hd);
+      std::vector<double> he;
+      long long le[3];
+      double gdummy;
+      slab_weights(g, kx, ky, kz, c, elo, ehi, he, le, &gdummy);
+      if (cudaMalloc((void**)&ctx->d_wext, (size_t)(le[0] + le[1]) * sizeof(double)) != cudaSuccess ||
+          cudaMalloc((void**)&ctx->d_whalo, (size_t)2 * ell * hd * nx * sizeof(double)) != cudaSuccess ||
+          cudaMemcpy(ctx->d_wext, he.data(), (size_t)(le[0] + le[1]) * sizeof(double), cudaMemcpyHostToDevice) !=
+              cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        aac_destroy(ctx);
+        return aac_fail(nullptr, AAC_ENOMEM, "wavefront halo allocation failed");
+      }
+      ctx->wext_x = le[0];
+      ctx->wext_off = (int)(lo - elo);
+      ctx->wext_rows = (int)(ehi - elo);
+      ctx->wave_hd = hd;
+    }
+  }
   // global Gershgorin max (all-reduce max over slabs)
   if (ctx->nranks > 1) {
     ctx->h_stat[0] = gmax;
@@ -366,6 +396,8 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
     if (p) cudaFree(p);
   if (ctx->d_st) cudaFree(ctx->d_st);
   if (ctx->d_grp) cudaFree(ctx->d_grp);
+  if (ctx->d_wext) cudaFree(ctx->d_wext);
+  if (ctx->d_whalo) cudaFree(ctx->d_whalo);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};
@@ -722,9 +754,25 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       ly0 = (int)std::max<long long>(10LL * H, (g.ny + want - 1) / want);
     }
     const int ncta = layout(ly0);
+    WSlab sl{g.wx, g.wy, 0, g.ny, nullptr, nullptr, 0};
+    if (ctx->nranks > 1) {                             // hd rows of hat w from each neighbour
+      const int hd = ctx->wave_hd;
+      Geo gh = g;
+      gh.S = (long long)hd * g.nx;
+      const double* planes[AAC_MAX_ELL];
+      int qs[AAC_MAX_ELL];
+      for (int q = 0; q < ell; ++q) {
+        planes[q] = ctx->d_what + (long long)q * N;
+        qs[q] = q;
+      }
+      double* hl = ctx->d_whalo;
+      double* hh = ctx->d_whalo + (long long)ell * hd * g.nx;
+      AAC_TRY(comm_halo_ex(ctx, gh, planes, qs, ell, hl, hh));
+      sl = WSlab{ctx->d_wext, ctx->d_wext + ctx->wext_x, ctx->wext_off, ctx->wext_rows, hl, hh, hd};
+    }
     ctx->next_flops = flops;
     LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
-           (k_wave<H, NT><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st)));
+           (k_wave<H, NT><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
   }
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
@@ -781,7 +829,11 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
     AAC_TRY(run_inverse(ctx, D, F, zbase, zjs, st));
     return AAC_OK;
   }
-  if (DIM == 2 && ctx->nranks == 1 && ctx->wave_h > 0) return wave_passes(ctx, P, zbase, zjs, st);
+  // wavefront: one rank, or slabs of >= WAVE_MAXH rows with every block done in one pass (the
+  // halo exchange covers hat w only)
+  if (DIM == 2 && ctx->wave_h > 0 &&
+      (ctx->nranks == 1 || (ctx->wave_hd > 0 && P.pmax - 1 <= WAVE_MAXH && ctx->wave_h == WAVE_MAXH)))
+    return wave_passes(ctx, P, zbase, zjs, st);
   double* X = ctx->d_X;
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;

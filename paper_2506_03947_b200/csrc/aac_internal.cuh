@@ -113,6 +113,13 @@ struct aac_ctx {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   int wave_h = 8;                      // wavefront depth (wave.cuh; 0 = per-step sweeps)
+  // slab-decomposed wavefront (2D, several ranks): face weights of rows [elo, ehi) of the
+  // global grid (this slab +- WAVE halo rows) and halo rows of hat w
+  double* d_wext = nullptr;            // wx | wy of the extended row range
+  long long wext_x = 0;                // offset of wy in d_wext
+  int wext_off = 0, wext_rows = 0;     // lo - elo, ehi - elo
+  double* d_whalo = nullptr;           // [2][ell][hd][nx]
+  int wave_hd = 0;                     // halo depth (0: slabs too thin, per-step sweeps)
   // plans
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;

@@ -39,6 +39,19 @@ struct WBlk {
   double lr, li;             // Lambda_k
   double ar[WAVE_MAXH], ai[WAVE_MAXH], br[WAVE_MAXH], bi[WAVE_MAXH];   // steps s0 .. s0+ns-1
 };
+// Slab decomposition (several ranks): rows outside this rank's slab come from halo buffers
+// (the neighbours' last / first hd rows of hat w, exchanged once per preconditioner apply) and
+// the face weights from arrays extended by hd rows on each side (built at setup from the global
+// kappa). One rank: no halo rows, the extended arrays are the slab's own.
+struct WSlab {
+  const double* wxe;         // extended lower x-faces, row e = local row + eoff
+  const double* wye;         // extended lower y-faces (row ne = the top face of the range)
+  int eoff, ne;              // local row r lies in the global domain iff 0 <= r + eoff < ne
+  const double* whlo;        // [ell][hd][nx] rows -hd .. -1 of hat w (NULL: none)
+  const double* whhi;        // [ell][hd][nx] rows ny .. ny+hd-1
+  int hd;
+};
+
 struct WSweep {
   WBlk b[AAC_MAX_BLK];
   int nb;                    // blocks in this launch
@@ -72,6 +85,7 @@ struct WCtx {                      // per-CTA constants
   const WBlk* B;
   const double* what;
   Geo g;
+  WSlab sl;
   double* xch;
   double* hist;                    // this thread's column of the history (x+1: next thread)
   int t, x, y0, y1;
@@ -84,14 +98,27 @@ template <int H, int NT, bool CPLX>
 __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow& R) {
   R.w0 = R.w1 = R.s0 = R.s1 = R.m0 = R.m1 = R.fxl = R.fyl = 0.0;
   const Geo& g = C.g;
-  if (C.colin && r >= 0 && r < g.ny) {
+  const int er = r + C.sl.eoff;                          // row of the extended weight arrays
+  if (C.colin && er >= 0 && er < C.sl.ne) {
     const long long p = (long long)r * g.nx + C.x;
-    const double* wq = C.what + (long long)C.B->q * g.N + p;
+    const long long pe = (long long)er * g.nx + C.x;
+    const double* wq;                                    // hat w: own slab or a halo row
+    long long ws;
+    if (r < 0) {
+      ws = (long long)C.sl.hd * g.nx;
+      wq = C.sl.whlo + (long long)C.B->q * ws + (long long)(r + C.sl.hd) * g.nx + C.x;
+    } else if (r >= g.ny) {
+      ws = (long long)C.sl.hd * g.nx;
+      wq = C.sl.whhi + (long long)C.B->q * ws + (long long)(r - g.ny) * g.nx + C.x;
+    } else {
+      ws = g.N;
+      wq = C.what + (long long)C.B->q * g.N + p;
+    }
     R.w0 = __ldg(wq);
-    if (CPLX) R.w1 = __ldg(wq + g.N);
-    R.fxl = __ldg(g.wx + p);
-    R.fyl = __ldg(g.wy + p);
-    if (!C.B->virt) {
+    if (CPLX) R.w1 = __ldg(wq + ws);
+    R.fxl = __ldg(C.sl.wxe + pe);
+    R.fyl = __ldg(C.sl.wye + pe);
+    if (!C.B->virt) {                                    // (later passes: one rank only)
       R.s0 = C.B->ps[p];
       R.m0 = C.B->pm[p];
       if (CPLX) {
@@ -99,8 +126,8 @@ __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow&
         R.m1 = C.B->pm[g.N + p];
       }
     }
-  } else if (C.colin && r == g.ny) {
-    R.fyl = __ldg(g.wy + (long long)r * g.nx + C.x);   // upper face of the last row (0 or halo)
+  } else if (C.colin && er == C.sl.ne) {
+    R.fyl = __ldg(C.sl.wye + (long long)er * g.nx + C.x);   // upper face of the last row
   }
 }
 
@@ -253,7 +280,7 @@ __device__ __forceinline__ void wave_dispatch_ns(const WCtx<H, NT>& C, int ns, b
 
 template <int H, int NT>
 __global__ void __launch_bounds__(NT, NT > 128 ? 2 : 3) k_wave(Geo g, WSweep W, const double* __restrict__ what,
-                                                            const IterState* st) {
+                                                            const IterState* st, WSlab sl) {
   using G = WGeom<H, NT>;
   if (st && st->done) return;
   extern __shared__ __align__(16) double wsm[];
@@ -264,6 +291,7 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 2 : 3) k_wave(Geo g, WSweep W, 
   C.B = &W.b[bi];
   C.what = what;
   C.g = g;
+  C.sl = sl;
   C.xch = wsm;
   C.hist = wsm + G::XCH + threadIdx.x;
   C.t = threadIdx.x;

@@ -41,8 +41,13 @@ def main():
     r = rng.standard_normal((p.ell,) + p.shape)
     out = {"lo": lo, "hi": hi, "mu_max": s.mu_max}
     out["y"] = s.matvec(local(x)).cpu().numpy()
+    s.profile_reset()
+    s.profile(True)
     for m in ("nc1", "nc2"):
         out["z_" + m] = s.precond_apply(m, case["k"], local(r)).cpu().numpy()
+    prof = s.profile_read()
+    s.profile(False)
+    out["wave_flops"] = prof["cheb_sweep"]["model_flops"]     # > 0 only for the wavefront kernel
     xs, info = s.gmres(case["method"], case["k"], local(p.b), rtol=p.rtol, maxit=60)
     out["x"] = xs.cpu().numpy()
     out["iters"] = info["iters"]

@@ -6,7 +6,9 @@ group (include/aac.h, aac_setup_host_transport), so the ranks never run kernels 
 each other. This exercises every slab-specific piece of the CUDA path -- halo layers in the
 stencil kernels, slab face weights, local partial sums + all-reduce in the Arnoldi and norm
 steps, the Gershgorin max -- against the single-domain oracle. (The NCCL transport differs only
-in who moves the same buffers; it needs one GPU per rank.) The saddle-point solver's multigrid
+in who moves the same buffers; it needs one GPU per rank.) In 2D the Chebyshev solves run as
+the slab-decomposed wavefront (halo rows of hat w exchanged once per apply) when every slab has
+at least 8 rows, else as per-step sweeps. The saddle-point solver's multigrid
 coarsens inside the slabs and gathers the first level whose slab boundaries are no longer
 aggregate boundaries, so its hierarchy -- and its result -- equals the one-rank oracle's.
 """
@@ -55,6 +57,8 @@ CASES = [
     (2, dict(name="headline", kw=dict(shape=(1, 40, 29)), method="nc2", k=8, k_sp=3, sp=True)),
     (3, dict(name="headline", kw=dict(shape=(1, 36, 33)), method="nc2", k=8, k_sp=3, sp=True)),
     (2, dict(name="headline", kw=dict(shape=(1, 37, 29)), method="nc2", k=8, k_sp=3, sp=False)),
+    # slabs thinner than the wavefront halo (8 rows): the per-step sweeps run instead
+    (4, dict(name="headline", kw=dict(shape=(1, 26, 21)), method="nc2", k=8, k_sp=3, sp=False)),
     (2, dict(name="3d", kw=dict(shape=(12, 9, 8)), method="nc1", k=10, k_sp=2, sp=True)),
     (3, dict(name="3d", kw=dict(shape=(7, 6, 9), ell=4), method="nc2", k=5, k_sp=2, sp=False)),
 ]
@@ -77,6 +81,9 @@ def test_multirank_slabs_match_oracle(tmp_path, world, case):
     x = rng.standard_normal((p.ell,) + p.shape)
     rr = rng.standard_normal((p.ell,) + p.shape)
     assert _rel(_stitch(parts, "y", p), op.apply_allatonce(w, x)) <= 1e-12
+    if p.dim == 2:                                             # which NC organisation ran
+        thick = min(d["hi"] - d["lo"] for d in parts) >= 8
+        assert all((float(d["wave_flops"]) > 0) == thick for d in parts)
     for m in ("nc1", "nc2"):
         al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * case["k"], m, case["k"])
         zo = ch.nc_apply(w, rr, p.ell, p.alpha, 1.0, mu, al)
