@@ -53,6 +53,9 @@ struct SpLevel {               // one multigrid level (device arrays)
   double* b;                   // [ell][N] right-hand sides (levels >= 1)
   double* x;                   // [ell][N] pre-smoothed iterate
   double* x2;                  // [ell][N] post-smoothed iterate (the level's result, levels >= 1)
+  double* dinv = nullptr;      // [h+1][N] 1 / diag(A_l + s_k I) per block shift (setup; the
+                               // smoother multiplies instead of dividing -- fp64 division is
+                               // ~10x the cost of the rest of the point update)
   int local = 1;               // 1: this rank's slab (halo exchanges); 0: the global level
   Geo gl{};                    // gathered level: this rank's slab of it (extents only) ...
   long long goff = 0;          // ... and its offset in the global arrays (points)
@@ -236,18 +239,15 @@ __global__ void k_sp_scalar(SpStepCtx S, int stepB) {
 // layers from hlo / hhi (plane stride g.S).
 // x = omega b / D (pre-smoothing from zero)
 template <int DIM>
-__global__ void __launch_bounds__(SP_T) k_mg_smooth0(Geo g, const double* __restrict__ cnt, SpConst K,
+__global__ void __launch_bounds__(SP_T) k_mg_smooth0(Geo g, const double* __restrict__ dinv, SpConst K,
                                                      MgIo io, const double* bl, double* xl,
                                                      const IterState* st) {
   if (st && st->done) return;
   const int pl = blockIdx.y;
   const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
   if (p >= g.N) return;
-  PtV<DIM, 1> q;
-  load_ptv<DIM, 1>(g, p, q);
-  const double m = (1.0 + K.s[pl]) * cnt[p];
   const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
-  xl[(long long)pl * g.N + p] = SP_OMEGA * b[p] / diag_of<DIM>(q, m);
+  xl[(long long)pl * g.N + p] = SP_OMEGA * b[p] * dinv[(long long)sp_block_of(K.ell, pl) * g.N + p];
 }
 
 // b_{l+1} = P^T (b - A_l x): one thread per COARSE point sums its children
@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong(Geo g, Geo gc, double* xl, 
 // x2 = x + omega (b - A x)/D. Level 0: written to io.out[pl], dot partial <x2, b> per plane,
 // last CTA: scalar step B.
 template <int DIM>
-__global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restrict__ cnt, MgIo io,
+__global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restrict__ cnt,
+                                                  const double* __restrict__ dinv, MgIo io,
                                                   const double* bl, const double* xl, double* x2l,
                                                   SpStepCtx S, int level0, const double* hlo,
                                                   const double* hhi) {
@@ -334,8 +335,8 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
     const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
     const double* x = xl + (long long)pl * g.N;
     const double xn = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m, hlo + (long long)pl * g.S,
-                                                              hhi + (long long)pl * g.S)) /
-                                 diag_of<DIM>(q, m);
+                                                              hhi + (long long)pl * g.S)) *
+                                 dinv[(long long)sp_block_of(S.K.ell, pl) * g.N + p];
     if (level0) {
       io.out[pl][p] = xn;
       dotp = fma(xn, b[p], dotp);
@@ -351,7 +352,8 @@ __global__ void __launch_bounds__(SP_T) k_mg_post(Geo g, const double* __restric
 // rank's x AFTER its own prolongation, i.e. exchanged by the caller -- so on slab-decomposed
 // levels the unfused pair k_mg_prolong + halo + k_mg_post is used instead).
 template <int DIM>
-__global__ void __launch_bounds__(SP_T) k_mg_prolong_post(Geo g, const double* __restrict__ cnt, Geo gc,
+__global__ void __launch_bounds__(SP_T) k_mg_prolong_post(Geo g, const double* __restrict__ cnt,
+                                                          const double* __restrict__ dinv, Geo gc,
                                                           MgIo io, const double* bl, const double* xl,
                                                           const double* __restrict__ xc, double* x2l,
                                                           SpStepCtx S, int level0) {
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong_post(Geo g, const double* _
     }
     const double* b = bl ? bl + (long long)pl * g.N : io.in[pl];
     const double bp = b[p];
-    const double xn = u0 + SP_OMEGA * (bp - a) / diag_of<DIM>(q, m);
+    const double xn = u0 + SP_OMEGA * (bp - a) * dinv[(long long)sp_block_of(S.K.ell, pl) * g.N + p];
     if (level0) {
       io.out[pl][p] = xn;
       dotp = fma(xn, bp, dotp);
@@ -406,6 +408,7 @@ struct MgTail {
   int nlev;                      // levels T .. T + nlev - 1 (the last one is the coarsest)
   Geo g[SP_TAIL_LEV];
   const double* cnt[SP_TAIL_LEV];
+  const double* dinv[SP_TAIL_LEV];
   double* b[SP_TAIL_LEV];        // b[0] = the tail's input (written by the level above)
   double* x[SP_TAIL_LEV];
   double* x2[SP_TAIL_LEV];       // x2[0] = the tail's output
@@ -432,11 +435,8 @@ __global__ void __launch_bounds__(SP_TAIL_T) k_mg_tail(MgTail T, SpConst K, cons
     const Geo& gc = T.g[l + 1];
     const double* b = T.b[l] + (long long)pl * g.N;
     double* x = T.x[l] + (long long)pl * g.N;
-    for (long long p = t; p < g.N; p += blockDim.x) {
-      PtV<DIM, 1> q;
-      load_ptv<DIM, 1>(g, p, q);
-      x[p] = SP_OMEGA * b[p] / diag_of<DIM>(q, (1.0 + s) * T.cnt[l][p]);
-    }
+    const double* di = T.dinv[l] + (long long)sp_block_of(K.ell, pl) * g.N;
+    for (long long p = t; p < g.N; p += blockDim.x) x[p] = SP_OMEGA * b[p] * di[p];
     __syncthreads();
     double* bc = T.b[l + 1] + (long long)pl * gc.N;
     for (long long pc = t; pc < gc.N; pc += blockDim.x) {
@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(SP_TAIL_T) k_mg_tail(MgTail T, SpConst K, cons
       PtV<DIM, 1> q;
       load_ptv<DIM, 1>(g, p, q);
       const double m = (1.0 + s) * T.cnt[l][p];
-      x2[p] = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m)) / diag_of<DIM>(q, m);
+      x2[p] = x[p] + SP_OMEGA * (b[p] - mg_apply<DIM>(g, q, x, m)) *
+                     T.dinv[l][(long long)sp_block_of(K.ell, pl) * g.N + p];
     }
     __syncthreads();
   }
@@ -877,6 +878,20 @@ static int sp_prepare(aac_ctx* ctx, int k) {
     g.wy = w + H.wx.size();
     g.wz = w + H.wx.size() + H.wy.size();
     AAC_TRY(sp_alloc(ctx, P, &lv.cnt, g.N));
+    {                                            // 1 / diag, in diag_of's summation order
+      std::vector<double> di((size_t)(h + 1) * g.N);
+      for (int kb = 0; kb <= h; ++kb) {
+        const double sk = P->K.s[kb == 0 ? 0 : (kb == h ? ell - 1 : 2 * kb - 1)];
+        for (long long pt = 0; pt < g.N; ++pt) {
+          double d = (1.0 + sk) * H.cnt[pt] + H.wx[pt] + H.wx[pt + 1];
+          if (dim >= 2) d += H.wy[pt] + H.wy[pt + g.nx];
+          if (dim >= 3) d += H.wz[pt] + H.wz[pt + g.S];
+          di[(size_t)kb * g.N + pt] = 1.0 / d;
+        }
+      }
+      AAC_TRY(sp_alloc(ctx, P, &lv.dinv, (long long)di.size()));
+      CUDA_TRY(ctx, cudaMemcpy(lv.dinv, di.data(), di.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(ctx, cudaMemcpy(lv.cnt, H.cnt.data(), g.N * sizeof(double), cudaMemcpyHostToDevice));
     if (l > 0) AAC_TRY(sp_alloc(ctx, P, &lv.b, (long long)ell * g.N));
     AAC_TRY(sp_alloc(ctx, P, &lv.x, (long long)ell * g.N));
@@ -961,7 +976,7 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     const Geo& gcl = gat ? c.gl : c.g;                     // this rank's part of the coarse level
     const dim3 gf(grid1d(a.g.N, SP_T), ell), gc(grid1d(gcl.N, SP_T), ell);
     LAUNCH(ctx, KID_SP_MG, 16.0 * ell * a.g.N,
-           k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.cnt, P->K, io, bl, a.x, st));
+           k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.dinv, P->K, io, bl, a.x, st));
     if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
     if (gat) CUDA_TRY(ctx, cudaMemsetAsync(c.b, 0, (size_t)ell * c.g.N * sizeof(double), ctx->stream));
     LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
@@ -979,6 +994,7 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
       const SpLevel& L = P->lev[tl + i];
       T.g[i] = L.g;
       T.cnt[i] = L.cnt;
+      T.dinv[i] = L.dinv;
       T.b[i] = L.b;
       T.x[i] = L.x;
       T.x2[i] = L.x2;
@@ -1004,11 +1020,11 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
                                                              gat ? c.goff : 0));
       AAC_TRY(sp_halo(ctx, a.g, a.x));
       LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-             k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
+             k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
                                                           hlo, hhi));
     } else {                                               // x, x_c, b in; x2 out (+ C)
       LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
-             k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, c.g, io, bl, a.x, c.x2, a.x2, S,
+             k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2, a.x2, S,
                                                                   l == 0 ? 1 : 0));
     }
   }
