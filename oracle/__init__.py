@@ -19,10 +19,11 @@ Modules (each function cites the passage it follows):
   chebyshev  Chebyshev semi-iteration, sigma bound, p*, Algorithm 1, NC apply
   saddle     saddle-point form, MINRES, PCG, multigrid V-cycle, SP apply
   gmres      flexible GMRES with CGS2 (north_star; not in the paper)
+  outer      the paper's outer solver: CI on the left-preconditioned system
   paper      the paper's own Dirichlet test operator + Appendix A bounds
 
 Parity status: every function here is pinned by tests/test_oracle_*.py against
 values the paper prints, closed forms, dense linear algebra or brute force,
 except where a docstring says "parity unpinned".
 """
-from . import operator, circulant, chebyshev, saddle, gmres, paper  # noqa: F401
+from . import operator, circulant, chebyshev, saddle, gmres, paper, outer  # noqa: F401

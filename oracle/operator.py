@@ -18,14 +18,19 @@ import scipy.sparse.linalg as spla
 
 
 class Weights:
-    """Face weights w_f = c*kappa_f*n_a^2 in natural interior layout."""
+    """Face weights w_f = c*kappa_f*n_a^2 in natural interior layout.
 
-    def __init__(self, shape, c, kx, ky, kz):
+    bd = (bx, by, bz): Dirichlet boundary-face weights per axis (the paper's own operator,
+    PAPER.md:630-637 Eq. IminusLap: a boundary face to a zero ghost value adds bd_a * u_P to
+    (A u)_P); (0, 0, 0) -- the default -- is the BASELINE zero-flux Neumann operator."""
+
+    def __init__(self, shape, c, kx, ky, kz, bd=(0.0, 0.0, 0.0)):
         nz, ny, nx = shape
         self.shape = (nz, ny, nx)
         self.wx = c * float(nx) ** 2 * np.asarray(kx, dtype=np.float64).reshape(nz, ny, nx - 1)
         self.wy = c * float(ny) ** 2 * np.asarray(ky, dtype=np.float64).reshape(nz, ny - 1, nx)
         self.wz = c * float(nz) ** 2 * np.asarray(kz, dtype=np.float64).reshape(nz - 1, ny, nx)
+        self.bd = tuple(float(v) for v in bd)
 
     @property
     def N(self):
@@ -34,7 +39,25 @@ class Weights:
 
 
 def weights(prob) -> Weights:
-    return Weights(prob.shape, prob.c, prob.kx, prob.ky, prob.kz)
+    return Weights(prob.shape, prob.c, prob.kx, prob.ky, prob.kz, getattr(prob, "bd", (0.0, 0.0, 0.0)))
+
+
+def boundary_diag(w: Weights) -> np.ndarray:
+    """Per-cell Dirichlet term: sum of bd_a over the cell's faces on the domain boundary
+    (zero for the Neumann operator)."""
+    d = np.zeros(w.shape)
+    bx, by, bz = getattr(w, "bd", (0.0, 0.0, 0.0))
+    nz, ny, nx = w.shape
+    for axis, b, n in ((2, bx, nx), (1, by, ny), (0, bz, nz)):
+        if b == 0.0 or n == 1:
+            continue
+        lo = [slice(None)] * 3
+        hi = [slice(None)] * 3
+        lo[axis] = 0
+        hi[axis] = n - 1
+        d[tuple(lo)] += b
+        d[tuple(hi)] += b
+    return d
 
 
 def apply_A(w: Weights, u):
@@ -50,6 +73,8 @@ def apply_A(w: Weights, u):
     d = u[1:, :, :] - u[:-1, :, :]            # across z-faces
     out[:-1, :, :] -= w.wz * d
     out[1:, :, :] += w.wz * d
+    if any(getattr(w, "bd", (0.0, 0.0, 0.0))):  # Dirichlet faces: zero ghost values
+        out = out + boundary_diag(w) * u
     return out
 
 
@@ -62,7 +87,7 @@ def gershgorin_max(w: Weights) -> float:
     s[:, 1:, :] += w.wy
     s[:-1, :, :] += w.wz
     s[1:, :, :] += w.wz
-    return float(np.max(1.0 + 2.0 * s))
+    return float(np.max(1.0 + 2.0 * s + boundary_diag(w)))
 
 
 def incidence(shape):
@@ -89,7 +114,8 @@ def sparse_A(w: Weights) -> sp.csr_matrix:
     """Independent assembly A = I + G^T diag(w) G (graph Laplacian form)."""
     G = incidence(w.shape)
     wf = np.concatenate([w.wx.ravel(), w.wy.ravel(), w.wz.ravel()])
-    return (sp.identity(w.N, format="csr") + G.T @ sp.diags(wf) @ G).tocsr()
+    return (sp.identity(w.N, format="csr") + G.T @ sp.diags(wf) @ G
+            + sp.diags(boundary_diag(w).ravel())).tocsr()
 
 
 def dense_A(w: Weights) -> np.ndarray:

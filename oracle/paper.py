@@ -15,6 +15,8 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
+from . import operator as op
+
 
 def nu(ell: int, D: float = 0.2) -> float:
     return D * D / (2.0 * ell - 4.0)
@@ -42,3 +44,16 @@ def sparse_A(nx: int, ell: int, D: float = 0.2) -> sp.csr_matrix:
     T = sp.diags([np.ones(nx - 1), -2.0 * np.ones(nx), np.ones(nx - 1)], [-1, 0, 1])
     L = sp.kron(sp.identity(nx), T) + sp.kron(T, sp.identity(nx))
     return (sp.identity(nx * nx) - (nu(ell, D) / (h * h)) * L).tocsr()
+
+
+def weights(nx: int, ell: int, D: float = 0.2) -> op.Weights:
+    """Eq. (IminusLap) in face-weight form: every interior face and every boundary face
+    (to a zero Dirichlet ghost) of the n_x x n_x vertex grid carries nu/h^2, h = 1/(n_x+1)."""
+    w = op.Weights.__new__(op.Weights)
+    w.shape = (1, nx, nx)
+    f = nu(ell, D) * (nx + 1) ** 2
+    w.wx = np.full((1, nx, nx - 1), f)
+    w.wy = np.full((1, nx - 1, nx), f)
+    w.wz = np.zeros((0, nx, nx))
+    w.bd = (f, f, 0.0)
+    return w
