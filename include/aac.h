@@ -52,7 +52,7 @@ enum {
   AAC_ENOMEM = -4    /* device or host allocation failed                           */
 };
 
-enum { AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3 };
+enum { AAC_NONE = 0, AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3 };
 
 typedef struct {
   int dim;          /* 1, 2 or 3                                                     */
@@ -84,14 +84,16 @@ int aac_slab_weights(const aac_grid* g, const double* kx, const double* ky, cons
  *  c          : diffusion coefficient; face weight w_f = c * kappa_f * n_a^2
  *               (h_a = 1/n_a), so A = I + c(-div kappa grad)_h (BASELINE.json).
  *  ell        : number of time blocks, even, 2 <= ell <= 16.
- *  alpha      : 0 < alpha < 1 (Lemma lemma:Zalpha needs alpha != mu_j^ell and
- *               mu_min(A) = 1 exactly under Neumann BCs).
+ *  alpha      : > 0. Every call that applies P_alpha then needs alpha^{1/ell} < mu_min
+ *               (Lemma lemma:Zalpha; AAC_EINVAL otherwise): alpha < 1 for
+ *               the Neumann operator (mu_min = 1 exactly), alpha <= 1 allowed for the
+ *               paper's Dirichlet operator once aac_set_bounds gives its mu_min > 1.
  *  max_krylov : Krylov storage for aac_gmres (maxit <= max_krylov).
  *  cuda_stream: cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  *               NULL = legacy default stream.
  *  nccl_id    : HOST pointer to a 128-byte ncclUniqueId shared by all ranks;
  *               ignored (may be NULL) when nranks == 1.
- * Errors: AAC_EINVAL (odd/small ell, alpha outside (0,1), c < 0, kappa <= 0 or
+ * Errors: AAC_EINVAL (odd/small ell, alpha <= 0, c < 0, kappa <= 0 or
  * non-finite, n < 2 on a used axis, bad slab), AAC_ENOMEM, AAC_ECUDA, AAC_ENCCL. */
 int aac_setup(const aac_grid* g, const double* kx, const double* ky, const double* kz,
               double c, int ell, double alpha, int max_krylov, void* cuda_stream,
@@ -168,6 +170,31 @@ int aac_profile_enable(aac_ctx* ctx, int enable);
 int aac_profile_count(void);
 int aac_profile_read(aac_ctx* ctx, int id, const char** name, double* ms, long long* launches,
                      double* model_bytes);
+/* ---- paper-reproduction mode ------------------------------------- */
+
+/* Dirichlet boundary faces: (A u)_P += b_a u_P for every face of P on the physical boundary
+ * along axis a (a zero ghost value), the paper's operator A = I - (nu/h^2) L (PAPER.md:630-637,
+ * Eq. IminusLap: interior AND boundary faces carry nu/h^2). b = 0 restores the BASELINE
+ * zero-flux operator. Recomputes the Gershgorin mu_max (mu_min resets to 1: set the true bound
+ * with aac_set_bounds), drops cached plans and graphs. Collective. AAC_SP then returns
+ * AAC_EINVAL (its multigrid hierarchy has no boundary terms).                            */
+int aac_set_boundary(aac_ctx* ctx, double bx, double by, double bz);
+
+/* Spectral bounds of A used by the inner Chebyshev solves and Algorithm 1 (default: 1 and the
+ * Gershgorin max, reading R5), e.g. the exact Appendix A bounds of the paper's operator
+ * (PAPER.md:998-1020). Needs 0 < mu_min <= mu_max and alpha^{1/ell} < mu_min.           */
+int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max);
+
+/* The paper's outer solver: Chebyshev semi-iteration on P^{-1} calA x = P^{-1} b (PAPER.md:
+ * 102-107 Eq. eq:precondsystem) with foci [lmin, lmax] -- Cor. cor:extremeevals gives
+ * [1, mu_min^ell/(mu_min^ell - alpha)] -- from x_0 = 0, stopping when ||b - calA x_p|| <
+ * tol ||b|| (the paper uses tol = 1e-6). method AAC_NONE: unpreconditioned, foci
+ * = the extreme eigenvalues of A. info->iters = p (preconditioner applications); info->
+ * matvecs_paper_units = p (ell + inner budget) (Table 1). b, x: device [ell][n_local], b != x.
+ * Uses the Krylov workspace (max_krylov >= 1). Returns AAC_OK or AAC_ENOCONV.             */
+int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* x, double lmin, double lmax,
+           double tol, int maxit, aac_gmres_info* info);
+
 /* Model (algorithmic) fp64 flops accumulated by kernel class `id` -- non-zero only for the
  * classes whose roofline is arithmetic (the wavefront Chebyshev kernel).                 */
 int aac_profile_flops(aac_ctx* ctx, int id, double* model_flops);

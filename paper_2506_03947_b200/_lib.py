@@ -14,13 +14,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libaac.so")
 
 AAC_OK, AAC_ENOCONV, AAC_EINVAL, AAC_ECUDA, AAC_ENCCL, AAC_ENOMEM = 0, 1, -1, -2, -3, -4
-AAC_NC1, AAC_NC2, AAC_SP = 1, 2, 3
-METHODS = {"nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
+AAC_NONE, AAC_NC1, AAC_NC2, AAC_SP = 0, 1, 2, 3
+METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",
            "aac_gmres_host", "aac_query", "aac_profile_enable", "aac_profile_count",
-           "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_launch_count", "aac_last_error",
+           "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_set_boundary",
+           "aac_set_bounds", "aac_ci", "aac_launch_count", "aac_last_error",
            "aac_destroy"]
 
 
@@ -82,6 +83,9 @@ def _load():
                                  ctypes.POINTER(L), dp]),
         "aac_profile_flops": (I, [P, I, dp]),
         "aac_profile_reset": (I, [P]),
+        "aac_set_boundary": (I, [P, D, D, D]),
+        "aac_set_bounds": (I, [P, D, D]),
+        "aac_ci": (I, [P, I, I, P, P, D, D, D, I, ctypes.POINTER(aac_gmres_info)]),
         "aac_launch_count": (L, [P]),
         "aac_last_error": (ctypes.c_char_p, [P]),
         "aac_destroy": (None, [P]),

@@ -11,6 +11,7 @@
 
 #include "aac_internal.cuh"
 #include "arnoldi.cuh"
+#include "ci.cuh"
 #include "comm.cuh"
 #include "krylov.cuh"
 #include "nc.cuh"
@@ -213,10 +214,8 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   if (g->dim < 1 || g->dim > 3) return aac_fail(nullptr, AAC_EINVAL, "dim must be 1, 2 or 3");
   if (ell < 2 || ell > AAC_MAX_ELL || (ell & 1))
     return aac_fail(nullptr, AAC_EINVAL, "ell must be even, 2 <= ell <= %d (PAPER.md:47)", AAC_MAX_ELL);
-  if (!(alpha > 0.0 && alpha < 1.0))
-    return aac_fail(nullptr, AAC_EINVAL,
-                    "alpha must lie in (0,1): mu_min(A) = 1 under Neumann BCs and P_alpha is "
-                    "singular at alpha = mu^ell (Lemma lemma:Zalpha, PAPER.md:120)");
+  if (!(alpha > 0.0) || !std::isfinite(alpha))
+    return aac_fail(nullptr, AAC_EINVAL, "alpha must be finite and > 0");
   if (!(c >= 0.0) || !std::isfinite(c)) return aac_fail(nullptr, AAC_EINVAL, "c must be finite and >= 0");
   if (max_krylov < 1) return aac_fail(nullptr, AAC_EINVAL, "max_krylov must be >= 1");
   const long long nx = g->n[0], ny = g->dim >= 2 ? g->n[1] : 1, nz = g->dim >= 3 ? g->n[2] : 1;
@@ -265,6 +264,9 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
     return aac_fail(nullptr, AAC_EINVAL, "kappa must be finite and > 0 on every interior face");
   }
   const long long lenx = lens[0], leny = lens[1];
+  ctx->wlen[0] = lens[0];
+  ctx->wlen[1] = lens[1];
+  ctx->wlen[2] = lens[2];
 
   if (tr) {
     ctx->host_tr = true;
@@ -411,6 +413,17 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   comm_destroy(ctx);
   delete ctx;
+}
+
+// Lemma lemma:Zalpha: P_alpha is invertible for alpha != mu_j^ell; with the
+// shifts |Lambda_k| = alpha^{1/ell} the block problems (A - Lambda_k) stay definite iff
+// alpha^{1/ell} < mu_min -- for the Neumann operator (mu_min = 1) that is alpha < 1.
+static int check_alpha(aac_ctx* ctx) {
+  if (pow(ctx->alpha, 1.0 / ctx->ell) < ctx->mu_min) return AAC_OK;
+  return aac_fail(ctx, AAC_EINVAL,
+                  "alpha must lie in (0, mu_min^ell) = (0, %g): mu_min(A) = 1 under Neumann BCs and "
+                  "P_alpha is singular at alpha = mu^ell (Lemma lemma:Zalpha, PAPER.md:120)",
+                  pow(ctx->mu_min, (double)ctx->ell));
 }
 
 extern "C" const char* aac_last_error(const aac_ctx* ctx) {
@@ -680,7 +693,8 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   const long long N = g.N, L = (long long)ell * N;
   const double C = 8.0 * ctx->dim * N;
   const Dft D = make_dft(ctx);
-  AAC_TRY(smem_optin(ctx, k_wave<H, NT>, WG::SMEM));
+  AAC_TRY(smem_optin(ctx, k_wave<H, NT, false>, WG::SMEM));
+  AAC_TRY(smem_optin(ctx, k_wave<H, NT, true>, WG::SMEM));
   const int nstrip = (g.nx + WG::TX - 1) / WG::TX;
   // rows per chunk: AAC_WAVE_LY overrides the default below
   const int ly_env = getenv("AAC_WAVE_LY") ? atoi(getenv("AAC_WAVE_LY")) : 0;
@@ -754,7 +768,7 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       ly0 = (int)std::max<long long>(10LL * H, (g.ny + want - 1) / want);
     }
     const int ncta = layout(ly0);
-    WSlab sl{g.wx, g.wy, 0, g.ny, nullptr, nullptr, 0};
+    WSlab sl{g.wx, g.wy, 0, g.ny, nullptr, nullptr, 0, (int)ctx->lo, (int)ctx->n[1]};
     if (ctx->nranks > 1) {                             // hd rows of hat w from each neighbour
       const int hd = ctx->wave_hd;
       Geo gh = g;
@@ -768,11 +782,14 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       double* hl = ctx->d_whalo;
       double* hh = ctx->d_whalo + (long long)ell * hd * g.nx;
       AAC_TRY(comm_halo_ex(ctx, gh, planes, qs, ell, hl, hh));
-      sl = WSlab{ctx->d_wext, ctx->d_wext + ctx->wext_x, ctx->wext_off, ctx->wext_rows, hl, hh, hd};
+      sl = WSlab{ctx->d_wext, ctx->d_wext + ctx->wext_x, ctx->wext_off, ctx->wext_rows, hl, hh, hd,
+                 (int)ctx->lo, (int)ctx->n[1]};
     }
     ctx->next_flops = flops;
     LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
-           (k_wave<H, NT><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
+           ((g.dir || ctx->nranks > 1)
+                ? k_wave<H, NT, true><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)
+                : k_wave<H, NT, false><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
   }
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
@@ -934,6 +951,7 @@ static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z,
 extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
   if (k < 1) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
+  AAC_TRY(check_alpha(ctx));
   StreamScope ss(ctx);
   if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z, false);
   if (method == AAC_SP) {
@@ -1072,6 +1090,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   if (k < 1) return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
   if (method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP)
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
+  AAC_TRY(check_alpha(ctx));
   const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
   const int ldh = ctx->max_krylov + 1;
   const long long sweeps0 = ctx->sweeps;
@@ -1232,3 +1251,158 @@ extern "C" int aac_profile_reset(aac_ctx* ctx) {
   return AAC_OK;
 }
 extern "C" long long aac_launch_count(const aac_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------------------------------------
+// Paper-reproduction mode: Dirichlet boundary faces, explicit spectral
+// bounds, the paper's outer CI.
+static void invalidate_plans(aac_ctx* ctx) {
+  for (auto& P : ctx->nc) P.method = 0;
+  for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
+  ctx->graphs.clear();
+  sp_destroy(ctx);
+}
+
+extern "C" int aac_set_boundary(aac_ctx* ctx, double bx, double by, double bz) {
+  if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_boundary: NULL ctx");
+  if (!(bx >= 0.0 && by >= 0.0 && bz >= 0.0) || !std::isfinite(bx + by + bz))
+    return aac_fail(ctx, AAC_EINVAL, "boundary face weights must be finite and >= 0");
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  Geo& g = ctx->geo;
+  g.bdx = bx;
+  g.bdy = ctx->dim >= 2 ? by : 0.0;
+  g.bdz = ctx->dim >= 3 ? bz : 0.0;
+  g.dir = (g.bdx != 0.0 || g.bdy != 0.0 || g.bdz != 0.0) ? 1 : 0;
+  // Gershgorin bound with the boundary terms: max_P (1 + 2 sum_f w_f + sum_boundary bd)
+  const long long tot = ctx->wlen[0] + ctx->wlen[1] + ctx->wlen[2];
+  std::vector<double> hw(tot);
+  CUDA_TRY(ctx, cudaMemcpy(hw.data(), ctx->d_w, tot * sizeof(double), cudaMemcpyDeviceToHost));
+  const double* wx = hw.data();
+  const double* wy = wx + ctx->wlen[0];
+  const double* wz = wy + ctx->wlen[1];
+  double gmax = 1.0;
+  for (int z = 0; z < g.nz; ++z)
+    for (int y = 0; y < g.ny; ++y)
+      for (int x = 0; x < g.nx; ++x) {
+        const long long p = ((long long)z * g.ny + y) * g.nx + x;
+        double sum = wx[p] + wx[p + 1];
+        if (ctx->dim >= 2) sum += wy[p] + wy[p + g.nx];
+        if (ctx->dim >= 3) sum += wz[p] + wz[p + g.S];
+        double d = g.bdx * ((x == 0) + (x == g.nx - 1));
+        if (ctx->dim == 2) d += g.bdy * ((y == 0 && !g.has_lo) + (y == g.ny - 1 && !g.has_hi));
+        if (ctx->dim == 3)
+          d += g.bdy * ((y == 0) + (y == g.ny - 1)) + g.bdz * ((z == 0 && !g.has_lo) + (z == g.nz - 1 && !g.has_hi));
+        gmax = fmax(gmax, 1.0 + 2.0 * sum + d);
+      }
+  if (ctx->nranks > 1) {
+    ctx->h_stat[0] = gmax;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_stat, ctx->h_stat, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclMax));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    gmax = ctx->h_stat[0];
+  }
+  ctx->mu_min = 1.0;          // (a Dirichlet operator's mu_min is > 1: set it with aac_set_bounds)
+  ctx->mu_max = gmax;
+  invalidate_plans(ctx);
+  return AAC_OK;
+}
+
+extern "C" int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max) {
+  if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_bounds: NULL ctx");
+  if (!(mu_min > 0.0 && mu_max >= mu_min) || !std::isfinite(mu_max))
+    return aac_fail(ctx, AAC_EINVAL, "need 0 < mu_min <= mu_max");
+  if (!(pow(ctx->alpha, 1.0 / ctx->ell) < mu_min))
+    return aac_fail(ctx, AAC_EINVAL, "alpha^{1/ell} must be below mu_min (Lemma lemma:Zalpha)");
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->mu_min = mu_min;
+  ctx->mu_max = mu_max;
+  invalidate_plans(ctx);
+  return AAC_OK;
+}
+
+extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* x, double lmin,
+                      double lmax, double tol, int maxit, aac_gmres_info* info) {
+  if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_ci: bad pointers");
+  if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP)
+    return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
+  if (method != AAC_NONE && k < 1) return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
+  if (!(lmin > 0.0 && lmax >= lmin) || !std::isfinite(lmax))
+    return aac_fail(ctx, AAC_EINVAL, "need 0 < lmin <= lmax");
+  if (!(tol >= 0.0) || maxit < 1) return aac_fail(ctx, AAC_EINVAL, "need tol >= 0, maxit >= 1");
+  if (method == AAC_SP && ctx->geo.dir) return aac_fail(ctx, AAC_EINVAL, "AAC_SP needs the Neumann operator");
+  if (method != AAC_NONE) AAC_TRY(check_alpha(ctx));
+  StreamScope ss(ctx);
+  const long long L = (long long)ctx->ell * ctx->geo.N;
+  const long long sweeps0 = ctx->sweeps;
+  double* xp = ctx->d_V;            // chi_{p-1}
+  double* r = ctx->d_V + L;         // b - calA chi_p
+  double* z = ctx->d_Z;             // P^{-1} r
+  double* y = ctx->d_W;             // calA chi_p
+  const unsigned nb = (unsigned)std::min<long long>(ctx->num_sms * 4, grid1d(L, 256));
+  CUDA_TRY(ctx, cudaMemsetAsync(x, 0, L * sizeof(double), ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(xp, 0, L * sizeof(double), ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(y, 0, L * sizeof(double), ctx->stream));
+  auto resid = [&](double* out) -> int {        // r = b - y, ||r||^2 -> host
+    LAUNCH(ctx, KID_AXPY, 24.0 * L, k_ci_resid<<<nb, 256, 0, ctx->stream>>>(b, y, r, L, ctx->d_part));
+    LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
+    AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    *out = sqrt(ctx->h_stat[0]);
+    return AAC_OK;
+  };
+  double bn = 0.0, rn = 0.0;
+  AAC_TRY(resid(&bn));                           // r_0 = b
+  if (method == AAC_SP) AAC_TRY(sp_prepare(ctx, k));
+  int alloc_sum = 0;
+  if (method != AAC_NONE) {
+    int al[AAC_MAX_ELL];
+    allocation(ctx, method, k, al);
+    for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
+  }
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+  double rho = 0.0;
+  int p = 0;
+  rn = bn;
+  bool conv = bn == 0.0;
+  for (; p < maxit && !conv; ++p) {
+    const double* zp = r;
+    if (method == AAC_NC1 || method == AAC_NC2) {
+      AAC_TRY(nc_apply(ctx, method, k, r, z, false));
+      zp = z;
+    } else if (method == AAC_SP) {
+      const Dft D = make_dft(ctx);
+      const long long N = ctx->geo.N;
+      if (ctx->ell <= 10)
+        LAUNCH(ctx, KID_FWD, 16.0 * L, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+      else
+        LAUNCH(ctx, KID_FWD, 16.0 * L, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+      AAC_TRY(sp_solve(ctx, k, z, 0, nullptr));
+      zp = z;
+    }
+    double a, c;
+    if (p == 0 || delta == 0.0) {
+      a = 0.0;
+      c = 1.0 / theta;
+      rho = delta / theta;
+    } else {
+      const double rho_new = 1.0 / (2.0 * theta / delta - rho);
+      a = rho_new * rho;
+      c = 2.0 * rho_new / delta;
+      rho = rho_new;
+    }
+    LAUNCH(ctx, KID_AXPY, 32.0 * L, k_ci_update<<<nb, 256, 0, ctx->stream>>>(x, xp, zp, a, c, L));
+    AAC_TRY(matvec_impl(ctx, x, y));
+    AAC_TRY(resid(&rn));
+    conv = rn < tol * bn;
+  }
+  if (info) {
+    info->iters = p;
+    info->converged = conv ? 1 : 0;
+    info->relres_est = bn > 0.0 ? rn / bn : 0.0;
+    info->relres_true = info->relres_est;
+    info->matvecs_paper_units = (long long)p * (ctx->ell + (method == AAC_SP ? sp_paper_matvecs(ctx, k) : alloc_sum));
+    info->stencil_sweeps = ctx->sweeps - sweeps0;
+  }
+  return conv ? AAC_OK : AAC_ENOCONV;
+}

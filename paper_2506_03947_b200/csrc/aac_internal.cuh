@@ -30,6 +30,8 @@ struct Geo {
   long long N;           // nx*ny*nz
   long long S;           // layer size across the slab axis
   int has_lo, has_hi;    // neighbour ranks below / above along the slab axis
+  int dir;               // 1: Dirichlet boundary faces (paper operator, aac_set_boundary)
+  double bdx, bdy, bdz;  // Dirichlet boundary-face weights per axis: (A u)_P += bd u_P per face
   const double* wx;
   const double* wy;
   const double* wz;
@@ -91,6 +93,7 @@ struct aac_ctx {
   int ka_grid = 0;                     // persistent grid of k_arnoldi
   // device memory (library-owned)
   double* d_w = nullptr;               // wx | wy | wz
+  long long wlen[3] = {0, 0, 0};       // their padded lengths
   double* d_what = nullptr;            // [ell][N] packed half-complex DFT of the input
   double* d_X = nullptr;               // [3][ell][N] Chebyshev iterate slots
   double* d_tmp = nullptr;             // [ell][N] scratch (true residual, SP)

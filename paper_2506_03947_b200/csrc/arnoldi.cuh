@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
             const int pl = g0 + k;
             if (pl < ell) {
               double a[1];
-              stencil_sv<DIM, 1>(q, sv[k], a);
+              stencil_sv<DIM, 1>(g, q, sv[k], a);
               w[pl] = a[0];
               if (pl > 0) w[pl] -= (k > 0) ? sv[0].c[0] : z[(long long)(pl - 1) * N + p];
             }

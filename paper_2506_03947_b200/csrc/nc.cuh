@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(LAST ? SW_TX * AAC_MAX_BLK : SW_FX, LAST ? 2 :
       ldv<VEC>(wr + N, p, w1);
     }
     double a0[VEC], a1[VEC];
-    stencil_sv<DIM, VEC>(q, v0, a0);
+    stencil_sv<DIM, VEC>(g, q, v0, a0);
     if (!B.cplx) {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(LAST ? SW_TX * AAC_MAX_BLK : SW_FX, LAST ? 2 :
       }
       if (!LAST) stv<VEC>(B.xo, p, out_r);
     } else {
-      stencil_sv<DIM, VEC>(q, v1, a1);
+      stencil_sv<DIM, VEC>(g, q, v1, a1);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const double c0 = v0.c[e], c1 = v1.c[e];

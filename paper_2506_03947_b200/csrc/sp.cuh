@@ -726,6 +726,8 @@ static void shift_of_block(const aac_ctx* ctx, int kb, double* lr, double* li);
 static int sp_prepare(aac_ctx* ctx, int k) {
   (void)k;
   if (ctx->sp) return AAC_OK;
+  if (ctx->geo.dir)   // the aggregation hierarchy carries no Dirichlet boundary terms
+    return aac_fail(ctx, AAC_EINVAL, "AAC_SP needs the Neumann operator (no aac_set_boundary)");
   SpPlan* P = new SpPlan();
   ctx->sp = P;
   const int ell = ctx->ell, h = ell / 2, dim = ctx->dim;

@@ -51,7 +51,21 @@ struct PtV {
   int x, y, z;
   double wx[VEC + 1];             // lower x-faces of the VEC points, then the last upper face
   double wym[VEC], wyp[VEC], wzm[VEC], wzp[VEC];
+  double dbd[VEC];                // Dirichlet boundary-face diagonal (0 for Neumann)
 };
+
+// Dirichlet boundary faces of the point (x, y, z) on the physical boundary (paper operator,
+// PAPER.md:630-637 Eq. IminusLap): sum of bd_a over its faces to a zero ghost value.
+template <int DIM>
+__device__ __forceinline__ double dirichlet_diag(const Geo& g, int x, int y, int z) {
+  double d = g.bdx * ((x == 0) + (x == g.nx - 1));
+  if constexpr (DIM == 2) d += g.bdy * ((y == 0 && !g.has_lo) + (y == g.ny - 1 && !g.has_hi));
+  if constexpr (DIM == 3) {
+    d += g.bdy * ((y == 0) + (y == g.ny - 1));
+    d += g.bdz * ((z == 0 && !g.has_lo) + (z == g.nz - 1 && !g.has_hi));
+  }
+  return d;
+}
 
 // Face weights of the VEC-point group at (x, y, z) (local slab coordinates).
 template <int DIM, int VEC>
@@ -72,6 +86,12 @@ __device__ __forceinline__ void load_ptv_xyz(const Geo& g, int x, int y, int z, 
   if constexpr (DIM >= 3) {
     ldv<VEC>(g.wz, p, q.wzm);
     ldv<VEC>(g.wz, p + g.S, q.wzp);
+  }
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) q.dbd[e] = 0.0;
+  if (g.dir) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) q.dbd[e] = dirichlet_diag<DIM>(g, x + e, y, z);
   }
 }
 
@@ -144,7 +164,7 @@ __device__ __forceinline__ void load_sv(const Geo& g, const PtV<DIM, VEC>& q, co
 
 // out[e] = (A u)_{p+e} from loaded operands
 template <int DIM, int VEC>
-__device__ __forceinline__ void stencil_sv(const PtV<DIM, VEC>& q, const SV<VEC>& v, double* out) {
+__device__ __forceinline__ void stencil_sv(const Geo& g, const PtV<DIM, VEC>& q, const SV<VEC>& v, double* out) {
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
     const double l = e == 0 ? v.w : v.c[e - 1];
@@ -161,6 +181,7 @@ __device__ __forceinline__ void stencil_sv(const PtV<DIM, VEC>& q, const SV<VEC>
       acc = fma(q.wzm[e], c - v.d[e], acc);
       acc = fma(q.wzp[e], c - v.u[e], acc);
     }
+    acc = fma(q.dbd[e], c, acc);                   // Dirichlet boundary faces (0: Neumann)
     out[e] = acc;
   }
 }
@@ -172,7 +193,7 @@ __device__ __forceinline__ void apply_Av(const Geo& g, const PtV<DIM, VEC>& q, c
                                          double* centre) {
   SV<VEC> v;
   load_sv<DIM, VEC>(g, q, u, hlo, hhi, v);
-  stencil_sv<DIM, VEC>(q, v, out);
+  stencil_sv<DIM, VEC>(g, q, v, out);
 #pragma unroll
   for (int e = 0; e < VEC; ++e) centre[e] = v.c[e];
 }
@@ -204,12 +225,12 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
     load_sv<DIM, VEC>(g, q, x + (long long)j * g.N, hlo + j * g.S, hhi + j * g.S, v0);
     if (two) load_sv<DIM, VEC>(g, q, x + (long long)(j + 1) * g.N, hlo + (j + 1) * g.S, hhi + (j + 1) * g.S, v1);
     double a0[VEC], a1[VEC];
-    stencil_sv<DIM, VEC>(q, v0, a0);
+    stencil_sv<DIM, VEC>(g, q, v0, a0);
 #pragma unroll
     for (int e = 0; e < VEC; ++e) a0[e] -= prev[e];
     stv<VEC>(y + (long long)j * g.N, p, a0);
     if (two) {
-      stencil_sv<DIM, VEC>(q, v1, a1);
+      stencil_sv<DIM, VEC>(g, q, v1, a1);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         a1[e] -= v0.c[e];

@@ -50,6 +50,7 @@ struct WSlab {
   const double* whlo;        // [ell][hd][nx] rows -hd .. -1 of hat w (NULL: none)
   const double* whhi;        // [ell][hd][nx] rows ny .. ny+hd-1
   int hd;
+  int lo, nyg;               // global row of local row 0, global rows (Dirichlet faces)
 };
 
 struct WSweep {
@@ -94,10 +95,31 @@ struct WCtx {                      // per-CTA constants
 
 struct WRow { double w0, w1, s0, s1, m0, m1, fxl, fyl; };
 
-template <int H, int NT, bool CPLX>
+template <int H, int NT, bool CPLX, bool GEN>
 __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow& R) {
   R.w0 = R.w1 = R.s0 = R.s1 = R.m0 = R.m1 = R.fxl = R.fyl = 0.0;
   const Geo& g = C.g;
+  if constexpr (!GEN) {                                  // one rank, Neumann: the slab itself
+    if (C.colin && r >= 0 && r < g.ny) {
+      const long long p = (long long)r * g.nx + C.x;
+      const double* wq = C.what + (long long)C.B->q * g.N + p;
+      R.w0 = __ldg(wq);
+      if (CPLX) R.w1 = __ldg(wq + g.N);
+      R.fxl = __ldg(g.wx + p);
+      R.fyl = __ldg(g.wy + p);
+      if (!C.B->virt) {
+        R.s0 = C.B->ps[p];
+        R.m0 = C.B->pm[p];
+        if (CPLX) {
+          R.s1 = C.B->ps[g.N + p];
+          R.m1 = C.B->pm[g.N + p];
+        }
+      }
+    } else if (C.colin && r == g.ny) {
+      R.fyl = __ldg(g.wy + (long long)r * g.nx + C.x);
+    }
+    return;
+  }
   const int er = r + C.sl.eoff;                          // row of the extended weight arrays
   if (C.colin && er >= 0 && er < C.sl.ne) {
     const long long p = (long long)r * g.nx + C.x;
@@ -131,7 +153,7 @@ __device__ __forceinline__ void wave_load_row(const WCtx<H, NT>& C, int r, WRow&
   }
 }
 
-template <int H, int NT, int ns, bool CPLX>
+template <int H, int NT, int ns, bool CPLX, bool GEN>
 __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, int tau, int slot,
                                           WRow& nxt, int tau1) {
   using G = WGeom<H, NT>;
@@ -147,7 +169,7 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, in
   }
   // (2) row tau enters: history, L_0, L_1; prefetch row tau + 1
   const WRow cur = nxt;
-  if (tau + 1 < tau1) wave_load_row<H, NT, CPLX>(C, tau + 1, nxt);
+  if (tau + 1 < tau1) wave_load_row<H, NT, CPLX, GEN>(C, tau + 1, nxt);
   {
     double* hs = C.hist + slot * (4 * G::HW);
     hs[0] = cur.w0;
@@ -194,15 +216,21 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, in
     // step) is folded first; the serial chain through the levels is 4 operations deep:
     //   x_new = c + a (c - m) + b (w - (A - Lambda) c) = Q - b Ap,  Ap = fyh (c - dn) + Bp.
     const double c0 = S.L[i][1][0];
-    const double B0 = fma(fyl, c0 - S.L[i][2][0], fma(fxh, c0 - xl[1], fma(fxl, c0 - xl[-1], c0)));
+    double B0 = fma(fyl, c0 - S.L[i][2][0], fma(fxh, c0 - xl[1], fma(fxl, c0 - xl[-1], c0)));
+    double dB = 0.0;                                    // Dirichlet boundary faces (paper mode)
+    if (GEN && C.g.dir) {
+      const int rg = tau - i + C.sl.lo;
+      dB = C.g.bdx * ((C.x == 0) + (C.x == C.g.nx - 1)) + C.g.bdy * ((rg == 0) + (rg == C.sl.nyg - 1));
+      B0 = fma(dB, c0, B0);
+    }
     const double m0 = i == 1 ? S.L[0][1][0] : S.L[i - 1][2][0];
     const double ar = B.ar[i - 1], br = B.br[i - 1];
     double o0, o1 = 0.0;
     if (CPLX) {
       const double w1 = hr[G::HW];
       const double c1 = S.L[i][1][1];
-      const double B1 = fma(fyl, c1 - S.L[i][2][1],
-                            fma(fxh, c1 - xl[G::XW + 1], fma(fxl, c1 - xl[G::XW - 1], c1)));
+      const double B1 = fma(dB, c1, fma(fyl, c1 - S.L[i][2][1],
+                                        fma(fxh, c1 - xl[G::XW + 1], fma(fxl, c1 - xl[G::XW - 1], c1))));
       const double m1 = i == 1 ? S.L[0][1][1] : S.L[i - 1][2][1];
       const double ai = B.ai[i - 1], bi = B.bi[i - 1];
       const double P0 = fma(-li, c1, fma(lr, c0, w0));      // w + Lambda c (r = P - Ap)
@@ -247,7 +275,7 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, in
   }
 }
 
-template <int H, int NT, int ns, bool CPLX>
+template <int H, int NT, int ns, bool CPLX, bool GEN>
 __device__ __forceinline__ void wave_block(const WCtx<H, NT>& C) {
   using G = WGeom<H, NT>;
   WState<H> S;
@@ -257,28 +285,30 @@ __device__ __forceinline__ void wave_block(const WCtx<H, NT>& C) {
     for (int a = 0; a < 3; ++a) S.L[i][a][0] = S.L[i][a][1] = 0.0;
   const int tau0 = C.y0 - ns, tau1 = C.y1 + ns;         // L_1 rows tau0 .. tau1-1
   WRow nxt;
-  wave_load_row<H, NT, CPLX>(C, tau0, nxt);
+  wave_load_row<H, NT, CPLX, GEN>(C, tau0, nxt);
   int slot = (tau0 % G::NSLOT + G::NSLOT) % G::NSLOT;   // history slot of row tau
   for (int tau = tau0; tau < tau1; ++tau) {
-    wave_step<H, NT, ns, CPLX>(C, S, tau, slot, nxt, tau1);
+    wave_step<H, NT, ns, CPLX, GEN>(C, S, tau, slot, nxt, tau1);
     slot = slot + 1 == G::NSLOT ? 0 : slot + 1;
   }
 }
 
 // one compact specialised loop per (steps, real/complex): no level guards in the loop
-template <int H, int NT, int NS>
+template <int H, int NT, int NS, bool GEN>
 __device__ __forceinline__ void wave_dispatch_ns(const WCtx<H, NT>& C, int ns, bool cplx) {
   if constexpr (NS >= 1) {
     if (ns == NS) {
-      if (cplx) wave_block<H, NT, NS, true>(C);
-      else wave_block<H, NT, NS, false>(C);
+      if (cplx) wave_block<H, NT, NS, true, GEN>(C);
+      else wave_block<H, NT, NS, false, GEN>(C);
       return;
     }
-    wave_dispatch_ns<H, NT, NS - 1>(C, ns, cplx);
+    wave_dispatch_ns<H, NT, NS - 1, GEN>(C, ns, cplx);
   }
 }
 
-template <int H, int NT>
+// GEN: the general variant (Dirichlet boundary faces of paper mode, halo rows of a slab);
+// GEN = false is the one-rank Neumann path with neither compiled in
+template <int H, int NT, bool GEN>
 __global__ void __launch_bounds__(NT, NT > 128 ? 2 : 3) k_wave(Geo g, WSweep W, const double* __restrict__ what,
                                                             const IterState* st, WSlab sl) {
   using G = WGeom<H, NT>;
@@ -307,5 +337,5 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 2 : 3) k_wave(Geo g, WSweep W, 
     wsm[k * G::XW + G::XW - 1] = 0.0;
   }
   for (int k = threadIdx.x; k < G::NSLOT * 4; k += NT) wsm[G::XCH + k * G::HW + NT] = 0.0;
-  wave_dispatch_ns<H, NT, H>(C, C.B->ns, C.B->np == 2);
+  wave_dispatch_ns<H, NT, H, GEN>(C, C.B->ns, C.B->np == 2);
 }

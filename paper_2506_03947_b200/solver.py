@@ -171,6 +171,27 @@ class Solver:
         return list(al)
 
     # -- profiling -----------------------------------------------------------------------
+    # -- paper-reproduction mode (aac_set_boundary / aac_set_bounds / aac_ci) -------------
+    def set_boundary(self, bx=0.0, by=0.0, bz=0.0):
+        check(lib.aac_set_boundary(self.ctx, float(bx), float(by), float(bz)), self.ctx)
+        mu0, mu1 = ctypes.c_double(), ctypes.c_double()
+        check(lib.aac_query(self.ctx, 1, 1, ctypes.byref(mu0), ctypes.byref(mu1), None, None), self.ctx)
+        self.mu_min, self.mu_max = mu0.value, mu1.value
+
+    def set_bounds(self, mu_min, mu_max):
+        check(lib.aac_set_bounds(self.ctx, float(mu_min), float(mu_max)), self.ctx)
+        self.mu_min, self.mu_max = float(mu_min), float(mu_max)
+
+    def ci(self, method, k, b, x=None, *, lmin, lmax, tol=1e-6, maxit=1000):
+        """The paper's outer CI (aac_ci): returns (x, info dict)."""
+        b = self._vec(b)
+        x = self.empty() if x is None else self._vec(x)
+        info = aac_gmres_info()
+        check(lib.aac_ci(self.ctx, _method(method), int(k), ctypes.c_void_p(b.data_ptr()),
+                         ctypes.c_void_p(x.data_ptr()), float(lmin), float(lmax), float(tol),
+                         int(maxit), ctypes.byref(info)), self.ctx, ok=(0, 1))
+        return x, info.asdict()
+
     def profile(self, enable=True):
         check(lib.aac_profile_enable(self.ctx, int(enable)), self.ctx)
 
@@ -210,6 +231,13 @@ class Solver:
 def from_problem(prob, *, rank=0, nranks=1, nccl_id=None, max_krylov=64, **kw) -> Solver:
     """Construct a Solver from a synth.Problem-like object (dim, shape, c, ell, alpha, kx..)."""
     nz, ny, nx = prob.shape
-    return Solver(prob.dim, (nx, ny, nz), prob.kx, prob.ky if prob.dim >= 2 else None,
-                  prob.kz if prob.dim >= 3 else None, prob.c, prob.ell, prob.alpha,
-                  rank=rank, nranks=nranks, nccl_id=nccl_id, max_krylov=max_krylov, **kw)
+    s = Solver(prob.dim, (nx, ny, nz), prob.kx, prob.ky if prob.dim >= 2 else None,
+               prob.kz if prob.dim >= 3 else None, prob.c, prob.ell, prob.alpha,
+               rank=rank, nranks=nranks, nccl_id=nccl_id, max_krylov=max_krylov, **kw)
+    bd = getattr(prob, "bd", (0.0, 0.0, 0.0))
+    if any(bd):                                  # the paper's Dirichlet operator
+        s.set_boundary(*bd)
+    mb = getattr(prob, "mu_bounds", None)
+    if mb is not None:
+        s.set_bounds(*mb)
+    return s

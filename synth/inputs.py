@@ -75,6 +75,8 @@ class Problem:
     rtol: float
     name: str = ""
     seed: int = 0
+    bd: tuple = (0.0, 0.0, 0.0)   # Dirichlet boundary-face weights (paper mode), else Neumann
+    mu_bounds: tuple = None       # exact spectral bounds of A when known (paper mode)
 
     @property
     def N(self) -> int:
@@ -146,3 +148,29 @@ def make_problem(name: str = "headline", *, n=None, shape=None, seed: int = 0,
                    kz=np.ascontiguousarray(kz), b=b,
                    method=spec.method if method is None else method,
                    k=spec.k if k is None else k, rtol=spec.rtol, name=name, seed=seed)
+
+
+def make_paper_problem(nx: int, ell: int = 10, alpha: float = 0.01, *, D: float = 0.2,
+                       seed: int = 0, method: str = "nc2", eta: float = 0.2) -> Problem:
+    """The paper's own test problem (§5): A = I - (nu/h^2) L,
+    2D Dirichlet 5-point Laplacian on the n_x x n_x interior vertices, h = 1/(n_x+1),
+    nu = D^2/(2 ell - 4), D = 0.2; b = (b_1, 0, ..., 0), b_1 ~ N(0,1) (seeded); inner budget
+    ell n_x eta per preconditioner apply (k = n_x eta per block). In face-weight form every
+    interior and boundary face carries nu/h^2: kappa = nu (n_x+1)^2 / n_x^2 with c = 1 (the
+    library's w_f = c kappa n^2), boundary weights bd = nu/h^2. mu_bounds: Appendix A
+    (PAPER.md:998-1020), mu = 1 + (4 nu/h^2)(sin^2(i pi/(2(n_x+1))) + sin^2(j pi/(2(n_x+1)))).
+    """
+    nu = D * D / (2.0 * ell - 4.0)
+    f = nu * (nx + 1) ** 2
+    kap = f / float(nx * nx)
+    s1 = math.sin(math.pi / (2 * (nx + 1))) ** 2
+    sn = math.sin(nx * math.pi / (2 * (nx + 1))) ** 2
+    mu_min, mu_max = 1.0 + 4.0 * f * 2 * s1, 1.0 + 4.0 * f * 2 * sn
+    rng = np.random.default_rng(seed)
+    b = np.zeros((ell, 1, nx, nx))
+    b[0] = rng.standard_normal(nx * nx).reshape(1, nx, nx)
+    return Problem(dim=2, shape=(1, nx, nx), ell=ell, alpha=alpha, c=1.0,
+                   kx=np.full((1, nx, nx - 1), kap), ky=np.full((1, nx - 1, nx), kap),
+                   kz=np.zeros((0, nx, nx)), b=b, method=method, k=max(1, round(nx * eta)),
+                   rtol=1e-6, name=f"paper{nx}", seed=seed, bd=(f, f, 0.0),
+                   mu_bounds=(mu_min, mu_max))

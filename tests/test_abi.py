@@ -68,7 +68,7 @@ def _setup(dim=2, n=(8, 6, 1), ell=4, alpha=0.1, c=0.01, kx=None, ky=None, kz=No
 
 @pytest.mark.parametrize("kw,frag", [
     (dict(ell=5), "ell must be even"), (dict(ell=0), "ell must be even"),
-    (dict(ell=18), "ell must be even"), (dict(alpha=1.0), "alpha must lie in (0,1)"),
+    (dict(ell=18), "ell must be even"), (dict(alpha=-0.5), "alpha must be finite and > 0"),
     (dict(alpha=0.0), "alpha"), (dict(c=-1.0), "c must be"), (dict(max_krylov=0), "max_krylov"),
     (dict(dim=4), "dim"), (dict(n=(1, 6, 1)), "n >= 2"),
     (dict(kx=-np.ones((1, 6, 7))), "kappa must be finite"),

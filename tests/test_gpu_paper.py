@@ -1,0 +1,108 @@
+"""GPU paper-reproduction mode vs the oracle: the paper's own Dirichlet
+operator through aac_set_boundary / aac_set_bounds, and the paper's outer
+solver, CI on the left-preconditioned system (aac_ci)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import synth  # noqa: E402
+from oracle import chebyshev as ch  # noqa: E402
+from oracle import operator as op  # noqa: E402
+from oracle import outer  # noqa: E402
+from oracle import paper  # noqa: E402
+
+HERE = os.path.dirname(__file__)
+
+
+def _dev(a, ell):
+    return torch.from_numpy(np.ascontiguousarray(a).reshape(ell, -1)).cuda()
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b))
+
+
+def _solver(p, **kw):
+    from paper_2506_03947_b200 import from_problem
+    return from_problem(p, max_krylov=kw.pop("max_krylov", 8), **kw)
+
+
+@pytest.mark.parametrize("nx,ell,alpha,eta,h", [(50, 10, 0.01, 0.2, "8"), (50, 10, 1.0, 0.1, "8"),
+                                                (37, 6, 0.5, 0.3, "8"), (37, 6, 0.5, 0.3, "0"),
+                                                (50, 10, 0.01, 0.3, "4")])
+def test_paper_operator_apply_parity(monkeypatch, nx, ell, alpha, eta, h):
+    monkeypatch.setenv("AAC_WAVE_H", h)
+    p = synth.make_paper_problem(nx, ell, alpha, eta=eta)
+    s = _solver(p)
+    w = paper.weights(nx, ell)
+    mu0, mu1 = paper.bounds(nx, ell)
+    assert s.mu_min == pytest.approx(mu0, rel=1e-14) and s.mu_max == pytest.approx(mu1, rel=1e-14)
+    r = np.random.default_rng(2).standard_normal((ell, 1, nx, nx))
+    assert _rel(s.matvec(_dev(r, ell)).cpu().numpy(), op.apply_allatonce(w, r)) <= 1e-12
+    for m in ("nc1", "nc2"):
+        al = ch.allocate(ell, mu0, mu1, alpha, ell * nx * eta, m, p.k)
+        assert s.allocation(m, p.k) == al
+        z = s.precond_apply(m, p.k, _dev(r, ell)).cpu().numpy()
+        assert _rel(z, ch.nc_apply(w, r, ell, alpha, mu0, mu1, al)) <= 1e-12, m
+    s.close()
+
+
+def test_gershgorin_with_dirichlet_faces():
+    p = synth.make_paper_problem(30, 10, 0.01)
+    from paper_2506_03947_b200 import Solver
+    s = Solver(2, (30, 30), p.kx, p.ky, None, p.c, p.ell, p.alpha, max_krylov=4)
+    s.set_boundary(*p.bd)
+    assert s.mu_max == pytest.approx(op.gershgorin_max(paper.weights(30, 10)), rel=1e-14)
+    from paper_2506_03947_b200 import AacError
+    with pytest.raises(AacError):                      # SP has no Dirichlet multigrid
+        s.precond_apply("sp", 2, _dev(np.ones((p.ell, 900)), p.ell))
+    s.close()
+
+
+@pytest.mark.parametrize("method,alpha,eta", [("none", 0.01, 0.2), ("nc1", 0.01, 0.1), ("nc2", 0.01, 0.2),
+                                              ("nc2", 1.0, 0.2), ("nc1", 0.01, 0.3)])
+def test_outer_ci_parity(method, alpha, eta):
+    """GPU outer CI vs the oracle's (same foci: Cor 2.4, or A's bounds unpreconditioned):
+    iteration counts equal within 1, iterates agree far below the 1e-6 stopping level."""
+    nx, ell = 50, 10
+    p = synth.make_paper_problem(nx, ell, alpha, eta=eta)
+    s = _solver(p)
+    w = paper.weights(nx, ell)
+    mu0, mu1 = paper.bounds(nx, ell)
+    if method == "none":
+        lo, hi, prec = mu0, mu1, None
+    else:
+        lo, hi = outer.extreme_eigs(mu0, ell, alpha)
+        al = ch.allocate(ell, mu0, mu1, alpha, ell * nx * eta, method, p.k)
+        prec = lambda r: ch.nc_apply(w, r, ell, alpha, mu0, mu1, al)  # noqa: E731
+    ro = outer.ci_outer(lambda x: op.apply_allatonce(w, x), prec, p.b, lo, hi, tol=1e-6, maxit=3000)
+    x, info = s.ci(method, p.k, _dev(p.b, ell), lmin=lo, lmax=hi, tol=1e-6, maxit=3000)
+    assert ro.converged and info["converged"] == 1
+    assert abs(info["iters"] - ro.iters) <= 1
+    if info["iters"] == ro.iters:
+        assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    budget = 0 if method == "none" else sum(s.allocation(method, p.k))
+    assert info["matvecs_paper_units"] == info["iters"] * (ell + budget)
+    s.close()
+
+
+def test_outer_ci_unpreconditioned_paper500():
+    """n_x = 500, ell = 10, unpreconditioned CI (1282 iterations) vs the oracle's
+    stored run (scripts/make_oracle_golden.py paper500, oracle only)."""
+    g = json.load(open(os.path.join(HERE, "golden", "oracle_paper500.json")))
+    p = synth.make_paper_problem(500, 10, 0.01)
+    s = _solver(p)
+    x, info = s.ci("none", 1, _dev(p.b, 10), lmin=g["lmin"], lmax=g["lmax"], tol=1e-6, maxit=3000)
+    assert info["converged"] == 1 and abs(info["iters"] - g["iters"]) <= 1
+    assert abs(info["iters"] - 1282) <= 0.02 * 1282
+    xs = x.cpu().numpy().ravel()
+    idx = np.array(g["sample_idx"])
+    if info["iters"] == g["iters"]:
+        assert np.linalg.norm(xs[idx] - np.array(g["sample_x"])) <= 1e-9 * np.linalg.norm(g["sample_x"])
+    s.close()

@@ -178,6 +178,21 @@ def test_gmres_zero_rhs_and_enoconv():
     s.close()
 
 
+def test_alpha_at_or_above_mu_min_pow_ell_is_rejected():
+    """Neumann: mu_min = 1 exactly, so alpha >= 1 makes P_alpha singular (Lemma lemma:Zalpha)
+    -- setup accepts it (the paper's Dirichlet operator allows alpha = 1), every apply refuses."""
+    from paper_2506_03947_b200 import AacError
+    p = synth.make_problem("headline", shape=(1, 8, 8), alpha=1.0)
+    s = _solver(p, max_krylov=4)
+    r = _dev(np.ones((p.ell, p.N)), p.ell)
+    for m in ("nc1", "nc2", "sp"):
+        with pytest.raises(AacError, match="Lemma"):
+            s.precond_apply(m, 2, r)
+    with pytest.raises(AacError, match="Lemma"):
+        s.gmres("nc2", 2, r, maxit=4)
+    s.close()
+
+
 def test_bad_arguments_raise():
     from paper_2506_03947_b200 import AacError
     p = synth.make_problem("headline", shape=(1, 8, 8))
