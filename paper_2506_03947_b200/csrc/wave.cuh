@@ -79,6 +79,7 @@ struct WGeom {
 template <int H>
 struct WState {
   double L[H + 1][3][2];           // L[0] = x_{s0-1}, L[i] = L_i (i = 1..ns): [age][plane]
+  double co[H][4];                 // step coefficients a_r, b_r, a_i, b_i held in registers
 };
 
 template <int H, int NT>
@@ -224,7 +225,7 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, in
       B0 = fma(dB, c0, B0);
     }
     const double m0 = i == 1 ? S.L[0][1][0] : S.L[i - 1][2][0];
-    const double ar = B.ar[i - 1], br = B.br[i - 1];
+    const double ar = S.co[i - 1][0], br = S.co[i - 1][1];
     double o0, o1 = 0.0;
     if (CPLX) {
       const double w1 = hr[G::HW];
@@ -232,7 +233,7 @@ __device__ __forceinline__ void wave_step(const WCtx<H, NT>& C, WState<H>& S, in
       const double B1 = fma(dB, c1, fma(fyl, c1 - S.L[i][2][1],
                                         fma(fxh, c1 - xl[G::XW + 1], fma(fxl, c1 - xl[G::XW - 1], c1))));
       const double m1 = i == 1 ? S.L[0][1][1] : S.L[i - 1][2][1];
-      const double ai = B.ai[i - 1], bi = B.bi[i - 1];
+      const double ai = S.co[i - 1][2], bi = S.co[i - 1][3];
       const double P0 = fma(-li, c1, fma(lr, c0, w0));      // w + Lambda c (r = P - Ap)
       const double P1 = fma(li, c0, fma(lr, c1, w1));
       const double dr = c0 - m0, di = c1 - m1;
@@ -283,6 +284,13 @@ __device__ __forceinline__ void wave_block(const WCtx<H, NT>& C) {
   for (int i = 0; i <= H; ++i)
 #pragma unroll
     for (int a = 0; a < 3; ++a) S.L[i][a][0] = S.L[i][a][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < ns; ++i) {
+    S.co[i][0] = C.B->ar[i];
+    S.co[i][1] = C.B->br[i];
+    S.co[i][2] = CPLX ? C.B->ai[i] : 0.0;
+    S.co[i][3] = CPLX ? C.B->bi[i] : 0.0;
+  }
   const int tau0 = C.y0 - ns, tau1 = C.y1 + ns;         // L_1 rows tau0 .. tau1-1
   WRow nxt;
   wave_load_row<H, NT, CPLX, GEN>(C, tau0, nxt);
