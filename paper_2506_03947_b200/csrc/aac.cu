@@ -766,6 +766,14 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       const long long slots = (long long)(NT > 128 ? 2 : 3) * ctx->num_sms;
       const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb));
       ly0 = (int)std::max<long long>(10LL * H, (g.ny + want - 1) / want);
+      // small grids: 10 H rows per chunk would leave most SMs idle -- fill the resident slots
+      // instead (at least 2 ns rows, the warm-up, per chunk)
+      const long long cols = (long long)g.ny * nstrip * nb;
+      if (cols / ly0 < slots) {
+        int ns_max = 1;
+        for (int i = 0; i < nb; ++i) ns_max = std::max(ns_max, S.b[i].ns);
+        ly0 = (int)std::max<long long>(2LL * ns_max, (cols + slots - 1) / slots);
+      }
     }
     const int ncta = layout(ly0);
     WSlab sl{g.wx, g.wy, 0, g.ny, nullptr, nullptr, 0, (int)ctx->lo, (int)ctx->n[1]};
