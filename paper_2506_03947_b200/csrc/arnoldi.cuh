@@ -50,11 +50,22 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
   // row-aligned tiles: (row, chunk of AT points within the row) -> no per-point index division
   const unsigned cpr = (unsigned)((g.nx + AT - 1) / AT), nrow = (unsigned)g.ny * (unsigned)g.nz;
   const long long ntile = (long long)cpr * nrow;
-  const long long my_tiles = blockIdx.x < ntile ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const long long nitems = my_tiles * nv;       // item k -> (tile r = k / nv, basis vector i = k % nv)
-  struct Tile { long long base; int x0, y, z, len; };
+  // Work units = (tile, group of basis vectors). Large grids: one group (a CTA streams all
+  // j+1 vectors of its tiles). Small grids have fewer tiles than CTAs, so the vectors are split
+  // into ng groups over more CTAs (each re-reads its tile of W and V_j; the partial sums of a
+  // CTA are zero outside its groups) -- the per-tile chain of j+1 dependent stages is the
+  // latency that bounds a small problem.
+  long long ngl = (2LL * gridDim.x + ntile - 1) / ntile;
+  ngl = ngl < 1 ? 1 : (ngl > nv ? nv : ngl);
+  const int ng = FUSED ? 1 : (int)ngl;
+  const int gsz = (nv + ng - 1) / ng;
+  const long long nunit = ntile * ng;
+  const long long my_tiles = blockIdx.x < nunit ? (nunit - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  struct Tile { long long base; int x0, y, z, len, i0, i1; };
   auto tile_of = [&](long long r) {
-    const unsigned tix = (unsigned)(blockIdx.x + r * gridDim.x);
+    const long long u = blockIdx.x + r * gridDim.x;
+    const unsigned tix = (unsigned)(u / ng);
+    const int gi = (int)(u - (long long)tix * ng);
     const unsigned row = tix / cpr, ch = tix - row * cpr;
     Tile T;
     T.x0 = (int)(ch * AT);
@@ -62,6 +73,8 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
     T.z = (int)(row / (unsigned)g.ny);
     T.base = (long long)row * g.nx + T.x0;
     T.len = g.nx - T.x0 < AT ? g.nx - T.x0 : AT;
+    T.i0 = gi * gsz;
+    T.i1 = min(nv, T.i0 + gsz);
     return T;
   };
   if (TMA && t == 0) {
@@ -74,17 +87,20 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
   __syncthreads();
   if (warp == AW) {                             // ---- producer warp
     if (TMA && lane == 0) {
-      for (long long k = 0; k < nitems; ++k) {
-        const int s = (int)(k % AS);
-        if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
-        const Tile T = tile_of(k / nv);
-        const int i = (int)(k % nv);
-        bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s]);
+      long long k = 0;                          // item counter (ring stage / phase)
+      for (long long r = 0; r < my_tiles; ++r) {
+        const Tile T = tile_of(r);
+        for (int i = T.i0; i < T.i1; ++i, ++k) {
+          const int s = (int)(k % AS);
+          if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
+          bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s]);
+        }
       }
     }
   } else {                                      // ---- consumer warps
     const double* z = P.Z + (long long)j * P.L;
     const double* vj = P.V + (long long)j * P.L;
+    long long k = 0;                            // item counter (matches the producer's)
     for (long long r = 0; r < my_tiles; ++r) {
       const Tile T = tile_of(r);
       const long long b = T.base;
@@ -131,8 +147,7 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
           }
         }
       }
-      for (int i = 0; i < nv; ++i) {
-        const long long k = r * nv + i;
+      for (int i = T.i0; i < T.i1; ++i, ++k) {
         const int s = (int)(k % AS);
         if constexpr (TMA) mbar_wait(&full[s], (uint32_t)((k / AS) & 1));
         double sa = 0.0, ga = 0.0;
