@@ -327,6 +327,82 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_paper(args):
+    """--config paper500 (one GPU): the paper's own operator (n_x = 500, ell = 10,
+    Dirichlet, Appendix A bounds) solved by the paper's outer CI with P_NC2 (eta = 0.2, alpha =
+    0.01) to 1e-6. A step = one outer-CI solve; metric = outer iterations/s."""
+    import torch
+
+    from paper_2506_03947_b200 import from_problem
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    nx, ell, alpha, eta = 500, 10, 0.01, 0.2
+    p = synth.make_paper_problem(nx, ell, alpha, eta=eta, method="nc2")
+    s = from_problem(p, max_krylov=4)
+    mu0 = p.mu_bounds[0]
+    lmin, lmax = 1.0, mu0 ** ell / (mu0 ** ell - alpha)          # Cor. cor:extremeevals
+    b_host = np.ascontiguousarray(p.b.reshape(ell, -1))
+    b = torch.from_numpy(b_host).to(dev)
+    x = torch.empty_like(b)
+    for _ in range(args.warmup):
+        _, info = s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = 0
+    for _ in range(args.steps):
+        _, info = s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+        its += info["iters"]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    bh = torch.from_numpy(b_host).pin_memory()
+    xh = torch.empty_like(bh).pin_memory()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    e_its = 0
+    for _ in range(args.steps):
+        bd = bh.to(dev, non_blocking=True)
+        xd, inf2 = s.ci("nc2", p.k, bd, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+        xh.copy_(xd, non_blocking=True)
+        e_its += inf2["iters"]
+    f1.record()
+    torch.cuda.synchronize()
+    s.profile_reset()
+    s.profile(True)
+    s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+    prof = s.profile_read()
+    s.profile(False)
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    tot = sum(v["ms"] for v in prof.values())
+    rl = None
+    if dom[1].get("model_flops", 0) > 0:
+        ach = dom[1]["model_flops"] / (dom[1]["ms"] / 1e3) / 1e12
+        rl = {"bound": "alu", "kernel": dom[0], "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+              "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+              "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz", "share_of_step": dom[1]["ms"] / tot}
+    line = {
+        "metric": "paper-mode outer CI its/s (fp64, n_x=500, ell=10, P_NC2 eta=0.2, alpha=0.01, tol 1e-6)",
+        "value": its / (ms / 1e3), "unit": "its/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "paper500: the paper's Dirichlet operator I - (nu/h^2) L (PAPER.md:630-637), "
+                               "outer CI on P_NC2^{-1} calA (PAPER.md:102-107, 647); SURVEY N1",
+                   "outer_iters_per_solve": info["iters"], "alloc": s.allocation("nc2", p.k),
+                   "matvecs_paper_units_per_solve": info["matvecs_paper_units"],
+                   "paper_table3_context": "n_x=500 alpha=0.01 eta=0.2: 7 outer its (7035 matvecs), PAPER.md:813"},
+        "e2e": {"value": e_its / (f0.elapsed_time(f1) / 1e3), "unit": "its/s",
+                "h2d_bytes_per_step": int(b_host.nbytes), "d2h_bytes_per_step": int(b_host.nbytes)},
+        "gpu_launches": None, "clocks": clk, "roofline": rl, "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+    s.close()
+
+
 def _nccl_unique_id() -> bytes:
     import ctypes
     import glob
@@ -360,14 +436,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="headline", choices=list(synth.CONFIGS))
+    ap.add_argument("--config", default="headline", choices=list(synth.CONFIGS) + ["paper500"])
     ap.add_argument("--method", default=None, choices=[None, "nc1", "nc2", "sp"])
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--maxit", type=int, default=60)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.config == "paper500":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "paper500 is a paper-mode extra, no reference arm"}))
+        else:
+            run_paper(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -11,6 +11,7 @@ for c in saddle 2d256 1d; do
 done
 timeout 900 python bench.py --config 3d --maxit 20 --steps 2 --no-cpu-baseline > $O/b_3d.json 2> $O/b_3d.err; echo "3d rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 > $O/b_ref.json 2> $O/b_ref.err; echo "ref rc=$?"
+timeout 600 python bench.py --config paper500 --steps 3 > $O/b_paper500.json 2> $O/b_paper500.err; echo "paper500 rc=$?"
 CMD="python scripts/one_solve.py headline 2"
 timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv $CMD > $O/ncu1.log 2>&1; echo "ncu launches rc=$?"

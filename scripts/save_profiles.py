@@ -17,7 +17,7 @@ src, ver = sys.argv[1], sys.argv[2]
 note = sys.argv[3] if len(sys.argv) > 3 else ""
 dst = os.path.join(ROOT, "profiles", f"r01_bench_{ver}")
 os.makedirs(dst, exist_ok=True)
-for f in ("b_head", "b_saddle", "b_2d256", "b_1d", "b_3d", "b_ref"):
+for f in ("b_head", "b_saddle", "b_2d256", "b_1d", "b_3d", "b_ref", "b_paper500"):
     p = os.path.join(src, f + ".json")
     if os.path.exists(p) and os.path.getsize(p):
         shutil.copy(p, dst)
