@@ -363,7 +363,8 @@ def run_paper(args):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     nx, ell, alpha, eta = 500, 10, 0.01, 0.2
-    p = synth.make_paper_problem(nx, ell, alpha, eta=eta, method="nc2")
+    meth = args.method if args.method in ("nc1", "nc2", "exact") else "nc2"
+    p = synth.make_paper_problem(nx, ell, alpha, eta=eta, method=meth)
     s = from_problem(p, max_krylov=4)
     mu0 = p.mu_bounds[0]
     lmin, lmax = 1.0, mu0 ** ell / (mu0 ** ell - alpha)          # Cor. cor:extremeevals
@@ -371,7 +372,7 @@ def run_paper(args):
     b = torch.from_numpy(b_host).to(dev)
     x = torch.empty_like(b)
     for _ in range(args.warmup):
-        _, info = s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+        _, info = s.ci(meth, p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
     clocks = ClockSampler(0)
     clocks.start()
     torch.cuda.synchronize()
@@ -379,7 +380,7 @@ def run_paper(args):
     e0.record()
     its = 0
     for _ in range(args.steps):
-        _, info = s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+        _, info = s.ci(meth, p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
         its += info["iters"]
     e1.record()
     torch.cuda.synchronize()
@@ -393,14 +394,14 @@ def run_paper(args):
     e_its = 0
     for _ in range(args.steps):
         bd = bh.to(dev, non_blocking=True)
-        xd, inf2 = s.ci("nc2", p.k, bd, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+        xd, inf2 = s.ci(meth, p.k, bd, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
         xh.copy_(xd, non_blocking=True)
         e_its += inf2["iters"]
     f1.record()
     torch.cuda.synchronize()
     s.profile_reset()
     s.profile(True)
-    s.ci("nc2", p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
+    s.ci(meth, p.k, b, x, lmin=lmin, lmax=lmax, tol=1e-6, maxit=200)
     prof = s.profile_read()
     s.profile(False)
     dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
@@ -412,13 +413,15 @@ def run_paper(args):
               "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
               "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz", "share_of_step": dom[1]["ms"] / tot}
     line = {
-        "metric": "paper-mode outer CI its/s (fp64, n_x=500, ell=10, P_NC2 eta=0.2, alpha=0.01, tol 1e-6)",
+        "metric": f"paper-mode outer CI its/s (fp64, n_x=500, ell=10, P={meth} eta=0.2, alpha=0.01, tol 1e-6)",
         "value": its / (ms / 1e3), "unit": "its/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "paper500: the paper's Dirichlet operator I - (nu/h^2) L (PAPER.md:630-637), "
-                               "outer CI on P_NC2^{-1} calA (PAPER.md:102-107, 647); SURVEY N1",
-                   "outer_iters_per_solve": info["iters"], "alloc": s.allocation("nc2", p.k),
+                               f"outer CI on P_{meth}^{{-1}} calA (PAPER.md:102-107, 647); SURVEY N1"
+                               + (" / N3 (exact P_alpha by DST-diagonalised block solves)" if meth == "exact" else ""),
+                   "outer_iters_per_solve": info["iters"], "method": meth,
+                   "alloc": s.allocation(meth, p.k) if meth != "exact" else None,
                    "matvecs_paper_units_per_solve": info["matvecs_paper_units"],
                    "paper_table3_context": "n_x=500 alpha=0.01 eta=0.2: 7 outer its (7035 matvecs), PAPER.md:813"},
         "e2e": {"value": e_its / (f0.elapsed_time(f1) / 1e3), "unit": "its/s",
@@ -463,7 +466,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="headline", choices=list(synth.CONFIGS) + ["paper500"])
-    ap.add_argument("--method", default=None, choices=[None, "nc1", "nc2", "sp"])
+    ap.add_argument("--method", default=None, choices=[None, "nc1", "nc2", "sp", "exact"])
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--maxit", type=int, default=60)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

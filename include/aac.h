@@ -52,7 +52,7 @@ enum {
   AAC_ENOMEM = -4    /* device or host allocation failed                           */
 };
 
-enum { AAC_NONE = 0, AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3 };
+enum { AAC_NONE = 0, AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3, AAC_EXACT = 4 };
 
 typedef struct {
   int dim;          /* 1, 2 or 3                                                     */
@@ -184,6 +184,14 @@ int aac_set_boundary(aac_ctx* ctx, double bx, double by, double bz);
  * Gershgorin max, reading R5), e.g. the exact Appendix A bounds of the paper's operator
  * (PAPER.md:998-1020). Needs 0 < mu_min <= mu_max and alpha^{1/ell} < mu_min.           */
 int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max);
+
+/* method AAC_EXACT, for aac_precond_apply / aac_gmres / aac_ci: the exact
+ * P_alpha^{-1} (PAPER.md:229-275 with exact block solves) for the paper's operator only -- 2D,
+ * square n x n, one rank, every interior face and the Dirichlet boundary faces of both axes
+ * carrying the same weight w (aac_set_boundary(w, w, 0)): A is then diagonalised by the
+ * orthonormal DST-I (Appendix A) and every block solve is two-sided DST
+ * products (batched fp64 GEMMs through cuBLAS, loaded at run time) and a spectral division.
+ * AAC_EINVAL for any other operator; k is ignored.                                       */
 
 /* The paper's outer solver: Chebyshev semi-iteration on P^{-1} calA x = P^{-1} b (PAPER.md:
  * 102-107 Eq. eq:precondsystem) with foci [lmin, lmax] -- Cor. cor:extremeevals gives

@@ -14,8 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libaac.so")
 
 AAC_OK, AAC_ENOCONV, AAC_EINVAL, AAC_ECUDA, AAC_ENCCL, AAC_ENOMEM = 0, 1, -1, -2, -3, -4
-AAC_NONE, AAC_NC1, AAC_NC2, AAC_SP = 0, 1, 2, 3
-METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP}
+AAC_NONE, AAC_NC1, AAC_NC2, AAC_SP, AAC_EXACT = 0, 1, 2, 3, 4
+METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP, "exact": AAC_EXACT}
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",

@@ -12,6 +12,7 @@
 #include "aac_internal.cuh"
 #include "arnoldi.cuh"
 #include "ci.cuh"
+#include "exact.cuh"
 #include "comm.cuh"
 #include "krylov.cuh"
 #include "nc.cuh"
@@ -399,6 +400,9 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   if (ctx->d_st) cudaFree(ctx->d_st);
   if (ctx->d_grp) cudaFree(ctx->d_grp);
   if (ctx->d_wext) cudaFree(ctx->d_wext);
+  if (ctx->d_S) cudaFree(ctx->d_S);
+  if (ctx->d_lam1) cudaFree(ctx->d_lam1);
+  if (ctx->d_T) cudaFree(ctx->d_T);
   if (ctx->d_whalo) cudaFree(ctx->d_whalo);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
@@ -956,12 +960,122 @@ static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z,
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Exact P_alpha for the paper's operator (exact.cuh).
+static CublasApi g_cublas;
+
+static int cublas_load(aac_ctx* ctx) {
+  if (g_cublas.h) return AAC_OK;
+  void* h = nullptr;
+  for (const char* nm : {"libcublas.so.12", "libcublas.so"})
+    if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return aac_fail(ctx, AAC_ECUDA, "dlopen libcublas failed: %s", dlerror());
+  *(void**)(&g_cublas.Create) = dlsym(h, "cublasCreate_v2");
+  *(void**)(&g_cublas.Destroy) = dlsym(h, "cublasDestroy_v2");
+  *(void**)(&g_cublas.SetStream) = dlsym(h, "cublasSetStream_v2");
+  *(void**)(&g_cublas.DgemmStridedBatched) = dlsym(h, "cublasDgemmStridedBatched");
+  if (!g_cublas.Create || !g_cublas.SetStream || !g_cublas.DgemmStridedBatched)
+    return aac_fail(ctx, AAC_ECUDA, "cuBLAS symbols missing");
+  if (g_cublas.Create(&g_cublas.handle) != 0) return aac_fail(ctx, AAC_ECUDA, "cublasCreate failed");
+  g_cublas.h = h;
+  return AAC_OK;
+}
+
+static int exact_prepare(aac_ctx* ctx) {
+  if (ctx->exact_n > 0) return AAC_OK;
+  const Geo& g = ctx->geo;
+  if (ctx->dim != 2 || ctx->nranks != 1 || g.nx != g.ny || !g.dir)
+    return aac_fail(ctx, AAC_EINVAL, "AAC_EXACT needs the paper's operator: 2D, square, one rank, Dirichlet faces");
+  const int n = g.nx;
+  const long long tot = ctx->wlen[0] + ctx->wlen[1];
+  std::vector<double> hw(tot);
+  CUDA_TRY(ctx, cudaMemcpy(hw.data(), ctx->d_w, tot * sizeof(double), cudaMemcpyDeviceToHost));
+  const double w = hw[1];                       // wx of (x=1, y=0): an interior face
+  auto same = [&](double v) { return fabs(v - w) <= 1e-12 * fabs(w); };
+  bool ok = same(g.bdx) && same(g.bdy);
+  for (int y = 0; y < n && ok; ++y)
+    for (int x = 0; x < n && ok; ++x) {
+      const long long p = (long long)y * n + x;
+      if (x > 0) ok = ok && same(hw[p]);
+      if (y > 0) ok = ok && same(hw[ctx->wlen[0] + p]);
+    }
+  if (!ok)
+    return aac_fail(ctx, AAC_EINVAL,
+                    "AAC_EXACT needs a constant face weight w on every interior and Dirichlet boundary face");
+  AAC_TRY(cublas_load(ctx));
+  std::vector<double> S((size_t)n * n), lam(n);
+  const double sc = sqrt(2.0 / (n + 1));
+  for (int i = 0; i < n; ++i) {
+    const double si = sin(M_PI * (i + 1) / (2.0 * (n + 1)));
+    lam[i] = w * 4.0 * si * si;
+    for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = sc * sin(M_PI * (double)(i + 1) * (j + 1) / (n + 1));
+  }
+  const long long L = (long long)ctx->ell * n * n;
+  if (cudaMalloc((void**)&ctx->d_S, (size_t)n * n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->d_lam1, (size_t)n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->d_T, (size_t)L * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return aac_fail(ctx, AAC_ENOMEM, "AAC_EXACT workspace allocation failed");
+  }
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_S, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_lam1, lam.data(), lam.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  ctx->exact_n = n;
+  return AAC_OK;
+}
+
+// C_q = op(A) op(B) for the ell planes (column-major views of the row-major planes; S = S^T)
+static int gemm_planes(aac_ctx* ctx, const double* A, long long sa, const double* B, long long sb, double* C) {
+  const int n = ctx->exact_n;
+  const double one = 1.0, zero = 0.0;
+  g_cublas.SetStream(g_cublas.handle, ctx->stream);
+  LaunchScope ls(ctx, KID_SWEEP, 8.0 * ctx->ell * 3.0 * n * n);
+  ctx->prof_flops[KID_SWEEP] += 2.0 * ctx->ell * (double)n * n * n;
+  if (g_cublas.DgemmStridedBatched(g_cublas.handle, 0, 0, n, n, n, &one, A, n, sa, B, n, sb, &zero, C, n,
+                                   (long long)n * n, ctx->ell) != 0)
+    return aac_fail(ctx, AAC_ECUDA, "cublasDgemmStridedBatched failed");
+  return ls.end();
+}
+
+static int exact_apply(aac_ctx* ctx, const double* r, double* zbase, bool gmres_mode, int host_j) {
+  AAC_TRY(exact_prepare(ctx));
+  const int n = ctx->exact_n, ell = ctx->ell, h = ell / 2;
+  const long long N = ctx->geo.N, L = (long long)ell * N, NN = (long long)n * n;
+  const double V = 8.0 * L;
+  const Dft D = make_dft(ctx);
+  const IterState* st = gmres_mode ? ctx->d_st : nullptr;
+  if (gmres_mode) {
+    AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
+  } else if (ell <= 10) {
+    LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+  } else {
+    LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
+  }
+  double* X = ctx->d_X;
+  // DST both sides: T = S W, X = T S; divide by mu - Lambda_k; back: T = S X, X = T S
+  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, ctx->d_what, NN, ctx->d_T));
+  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
+  ExactShifts Sh{};
+  for (int kb = 0; kb <= h; ++kb) shift_of_block(ctx, kb, &Sh.lr[kb], &Sh.li[kb]);
+  LAUNCH(ctx, KID_SWEEP, 2 * V, k_exact_scale<<<grid1d(NN, 256), 256, 0, ctx->stream>>>(n, ell, ctx->d_lam1, X, Sh));
+  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, X, NN, ctx->d_T));
+  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
+  NcFinal F{};
+  for (int kb = 0; kb <= h; ++kb) {
+    F.src[kb] = X + (long long)plane_of_block(ell, kb) * N;
+    F.tr[kb] = 1.0;
+    F.ti[kb] = 0.0;
+  }
+  return run_inverse(ctx, D, F, zbase, gmres_mode ? L : 0, st);
+}
+
 extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
-  if (k < 1) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
+  if (k < 1 && method != AAC_EXACT) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
   AAC_TRY(check_alpha(ctx));
   StreamScope ss(ctx);
   if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z, false);
+  if (method == AAC_EXACT) return exact_apply(ctx, r, z, false, 0);
   if (method == AAC_SP) {
     AAC_TRY(sp_prepare(ctx, k));
     const long long N = ctx->geo.N;
@@ -1051,6 +1165,8 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
     AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
+  } else if (method == AAC_EXACT) {
+    AAC_TRY(exact_apply(ctx, nullptr, ctx->d_Z, true, host_j));
   } else {
     AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j));
   }
@@ -1095,10 +1211,11 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   if (maxit < 1 || maxit > ctx->max_krylov)
     return aac_fail(ctx, AAC_EINVAL, "maxit must be in [1, max_krylov=%d]", ctx->max_krylov);
   if (!(rtol >= 0.0)) return aac_fail(ctx, AAC_EINVAL, "rtol must be >= 0");
-  if (k < 1) return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
-  if (method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP)
+  if (method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP && method != AAC_EXACT)
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
+  if (k < 1 && method != AAC_EXACT) return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
   AAC_TRY(check_alpha(ctx));
+  if (method == AAC_EXACT) AAC_TRY(exact_prepare(ctx));
   const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
   const int ldh = ctx->max_krylov + 1;
   const long long sweeps0 = ctx->sweeps;
@@ -1112,13 +1229,13 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_V, b, L * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_giv, 0, 6LL * ldh * sizeof(double), ctx->stream));
   int alloc_sum = 0;
-  {
+  if (method != AAC_EXACT) {
     int al[AAC_MAX_ELL];
     allocation(ctx, method, k, al);
     for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
   }
   GraphEntry* ge = nullptr;
-  const bool graphs = ctx->use_graphs && !ctx->prof;
+  const bool graphs = ctx->use_graphs && !ctx->prof && method != AAC_EXACT;   // (cuBLAS: eager)
   if (graphs) AAC_TRY(get_graph(ctx, method, k, &ge));
   // Arnoldi steps. Graph path: replay one captured step per iteration and poll the state of
   // the PREVIOUS step (speculative: a step launched after convergence returns at once).
@@ -1265,6 +1382,13 @@ extern "C" long long aac_launch_count(const aac_ctx* ctx) { return ctx ? ctx->la
 // bounds, the paper's outer CI.
 static void invalidate_plans(aac_ctx* ctx) {
   for (auto& P : ctx->nc) P.method = 0;
+  if (ctx->exact_n > 0) {                       // the DST factorisation belongs to the old operator
+    cudaFree(ctx->d_S);
+    cudaFree(ctx->d_lam1);
+    cudaFree(ctx->d_T);
+    ctx->d_S = ctx->d_lam1 = ctx->d_T = nullptr;
+    ctx->exact_n = 0;
+  }
   for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
   ctx->graphs.clear();
   sp_destroy(ctx);
@@ -1331,9 +1455,10 @@ extern "C" int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max) {
 extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* x, double lmin,
                       double lmax, double tol, int maxit, aac_gmres_info* info) {
   if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_ci: bad pointers");
-  if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP)
+  if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP && method != AAC_EXACT)
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
-  if (method != AAC_NONE && k < 1) return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
+  if ((method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) && k < 1)
+    return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
   if (!(lmin > 0.0 && lmax >= lmin) || !std::isfinite(lmax))
     return aac_fail(ctx, AAC_EINVAL, "need 0 < lmin <= lmax");
   if (!(tol >= 0.0) || maxit < 1) return aac_fail(ctx, AAC_EINVAL, "need tol >= 0, maxit >= 1");
@@ -1362,8 +1487,9 @@ extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* 
   double bn = 0.0, rn = 0.0;
   AAC_TRY(resid(&bn));                           // r_0 = b
   if (method == AAC_SP) AAC_TRY(sp_prepare(ctx, k));
+  if (method == AAC_EXACT) AAC_TRY(exact_prepare(ctx));
   int alloc_sum = 0;
-  if (method != AAC_NONE) {
+  if (method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) {
     int al[AAC_MAX_ELL];
     allocation(ctx, method, k, al);
     for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
@@ -1377,6 +1503,9 @@ extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* 
     const double* zp = r;
     if (method == AAC_NC1 || method == AAC_NC2) {
       AAC_TRY(nc_apply(ctx, method, k, r, z, false));
+      zp = z;
+    } else if (method == AAC_EXACT) {
+      AAC_TRY(exact_apply(ctx, r, z, false, 0));
       zp = z;
     } else if (method == AAC_SP) {
       const Dft D = make_dft(ctx);

@@ -127,6 +127,11 @@ struct aac_ctx {
   NcPlan nc[2];                        // cached NC plans
   int nc_next = 0;
   SpPlan* sp = nullptr;
+  // exact P_alpha (N3, exact.cuh): DST-I matrix, 1D eigenvalues, GEMM workspace
+  double* d_S = nullptr;               // [n][n] orthonormal DST-I
+  double* d_lam1 = nullptr;            // [n] w * 4 sin^2(pi (i+1) / (2 (n+1)))
+  double* d_T = nullptr;               // [ell][n][n] GEMM intermediate
+  int exact_n = 0;                     // > 0 once prepared
   // NCCL (dlopen'ed), or the host-staged transport
   void* nccl_comm = nullptr;
   bool host_tr = false;

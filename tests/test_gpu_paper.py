@@ -106,3 +106,56 @@ def test_outer_ci_unpreconditioned_paper500():
     if info["iters"] == g["iters"]:
         assert np.linalg.norm(xs[idx] - np.array(g["sample_x"])) <= 1e-9 * np.linalg.norm(g["sample_x"])
     s.close()
+
+
+# ---------------------------------------------------------------- exact P_alpha
+@pytest.mark.parametrize("nx,ell,alpha", [(50, 10, 1.0), (50, 10, 0.01), (37, 6, 1e-4), (64, 16, 0.3)])
+def test_exact_precond_parity(nx, ell, alpha):
+    """AAC_EXACT (DST-diagonalised block solves) vs the oracle's exact P_alpha^{-1} (sparse LU per
+    Fourier block); rounding grows with kappa(Gamma_alpha) (reading R18)."""
+    from oracle import circulant as circ
+    p = synth.make_paper_problem(nx, ell, alpha)
+    s = _solver(p)
+    w = paper.weights(nx, ell)
+    r = np.random.default_rng(4).standard_normal((ell, 1, nx, nx))
+    z = s.precond_apply("exact", 1, _dev(r, ell)).cpu().numpy()
+    zo = circ.exact_apply(w, r, ell, alpha)
+    assert _rel(z, zo) <= 1e-12 * max(1.0, circ.gamma_condition(ell, alpha))
+    s.close()
+
+
+def test_exact_rejects_other_operators():
+    from paper_2506_03947_b200 import AacError
+    p = synth.make_problem("headline", shape=(1, 16, 16))          # Neumann, variable kappa
+    s = _solver(p)
+    with pytest.raises(AacError, match="AAC_EXACT"):
+        s.precond_apply("exact", 1, _dev(np.ones((p.ell, 256)), p.ell))
+    s.close()
+
+
+@pytest.mark.parametrize("alpha", [1.0, 1e-2, 1e-4, 1e-6])
+def test_exact_outer_ci_and_gmres(alpha):
+    """Outer CI and GMRES with the exact P_alpha: counts = the oracle's +-1 (Fig. 2 left: the count
+    falls with alpha); for small alpha the spectrum of P^{-1} calA clusters at 1
+    (Thm 2.2) and GMRES needs only a few steps."""
+    from oracle import circulant as circ
+    nx, ell = 40, 10
+    p = synth.make_paper_problem(nx, ell, alpha)
+    s = _solver(p, max_krylov=40)
+    w = paper.weights(nx, ell)
+    mu0 = paper.bounds(nx, ell)[0]
+    lo, hi = outer.extreme_eigs(mu0, ell, alpha)
+    ro = outer.ci_outer(lambda x: op.apply_allatonce(w, x), lambda r: circ.exact_apply(w, r, ell, alpha),
+                        p.b, lo, hi, tol=1e-6, maxit=200)
+    x, info = s.ci("exact", 1, _dev(p.b, ell), lmin=lo, lmax=hi, tol=1e-6, maxit=200)
+    assert info["converged"] == 1 and abs(info["iters"] - ro.iters) <= 1
+    from oracle import gmres as og
+    rg = og.fgmres(lambda v: op.apply_allatonce(w, v), lambda v: circ.exact_apply(w, v, ell, alpha), p.b,
+                   1e-10, 40)
+    xg, ig = s.gmres("exact", 1, _dev(p.b, ell), rtol=1e-10, maxit=40)
+    assert ig["converged"] == 1 and abs(ig["iters"] - rg.iters) <= 1
+    if ig["iters"] == rg.iters:
+        assert _rel(xg.cpu().numpy(), rg.x) <= 1e-9
+    if alpha <= 1e-2:                     # spectrum {1} u {mu^ell/(mu^ell - alpha)} clusters at 1
+        assert ig["iters"] <= 4
+    s.close()
