@@ -960,114 +960,7 @@ static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z,
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// Exact P_alpha for the paper's operator (exact.cuh).
-static CublasApi g_cublas;
-
-static int cublas_load(aac_ctx* ctx) {
-  if (g_cublas.h) return AAC_OK;
-  void* h = nullptr;
-  for (const char* nm : {"libcublas.so.12", "libcublas.so"})
-    if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
-  if (!h) return aac_fail(ctx, AAC_ECUDA, "dlopen libcublas failed: %s", dlerror());
-  *(void**)(&g_cublas.Create) = dlsym(h, "cublasCreate_v2");
-  *(void**)(&g_cublas.Destroy) = dlsym(h, "cublasDestroy_v2");
-  *(void**)(&g_cublas.SetStream) = dlsym(h, "cublasSetStream_v2");
-  *(void**)(&g_cublas.DgemmStridedBatched) = dlsym(h, "cublasDgemmStridedBatched");
-  if (!g_cublas.Create || !g_cublas.SetStream || !g_cublas.DgemmStridedBatched)
-    return aac_fail(ctx, AAC_ECUDA, "cuBLAS symbols missing");
-  if (g_cublas.Create(&g_cublas.handle) != 0) return aac_fail(ctx, AAC_ECUDA, "cublasCreate failed");
-  g_cublas.h = h;
-  return AAC_OK;
-}
-
-static int exact_prepare(aac_ctx* ctx) {
-  if (ctx->exact_n > 0) return AAC_OK;
-  const Geo& g = ctx->geo;
-  if (ctx->dim != 2 || ctx->nranks != 1 || g.nx != g.ny || !g.dir)
-    return aac_fail(ctx, AAC_EINVAL, "AAC_EXACT needs the paper's operator: 2D, square, one rank, Dirichlet faces");
-  const int n = g.nx;
-  const long long tot = ctx->wlen[0] + ctx->wlen[1];
-  std::vector<double> hw(tot);
-  CUDA_TRY(ctx, cudaMemcpy(hw.data(), ctx->d_w, tot * sizeof(double), cudaMemcpyDeviceToHost));
-  const double w = hw[1];                       // wx of (x=1, y=0): an interior face
-  auto same = [&](double v) { return fabs(v - w) <= 1e-12 * fabs(w); };
-  bool ok = same(g.bdx) && same(g.bdy);
-  for (int y = 0; y < n && ok; ++y)
-    for (int x = 0; x < n && ok; ++x) {
-      const long long p = (long long)y * n + x;
-      if (x > 0) ok = ok && same(hw[p]);
-      if (y > 0) ok = ok && same(hw[ctx->wlen[0] + p]);
-    }
-  if (!ok)
-    return aac_fail(ctx, AAC_EINVAL,
-                    "AAC_EXACT needs a constant face weight w on every interior and Dirichlet boundary face");
-  AAC_TRY(cublas_load(ctx));
-  std::vector<double> S((size_t)n * n), lam(n);
-  const double sc = sqrt(2.0 / (n + 1));
-  for (int i = 0; i < n; ++i) {
-    const double si = sin(M_PI * (i + 1) / (2.0 * (n + 1)));
-    lam[i] = w * 4.0 * si * si;
-    for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = sc * sin(M_PI * (double)(i + 1) * (j + 1) / (n + 1));
-  }
-  const long long L = (long long)ctx->ell * n * n;
-  if (cudaMalloc((void**)&ctx->d_S, (size_t)n * n * sizeof(double)) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->d_lam1, (size_t)n * sizeof(double)) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->d_T, (size_t)L * sizeof(double)) != cudaSuccess) {
-    cudaGetLastError();
-    return aac_fail(ctx, AAC_ENOMEM, "AAC_EXACT workspace allocation failed");
-  }
-  CUDA_TRY(ctx, cudaMemcpy(ctx->d_S, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(ctx->d_lam1, lam.data(), lam.size() * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaDeviceSynchronize());
-  ctx->exact_n = n;
-  return AAC_OK;
-}
-
-// C_q = op(A) op(B) for the ell planes (column-major views of the row-major planes; S = S^T)
-static int gemm_planes(aac_ctx* ctx, const double* A, long long sa, const double* B, long long sb, double* C) {
-  const int n = ctx->exact_n;
-  const double one = 1.0, zero = 0.0;
-  g_cublas.SetStream(g_cublas.handle, ctx->stream);
-  LaunchScope ls(ctx, KID_SWEEP, 8.0 * ctx->ell * 3.0 * n * n);
-  ctx->prof_flops[KID_SWEEP] += 2.0 * ctx->ell * (double)n * n * n;
-  if (g_cublas.DgemmStridedBatched(g_cublas.handle, 0, 0, n, n, n, &one, A, n, sa, B, n, sb, &zero, C, n,
-                                   (long long)n * n, ctx->ell) != 0)
-    return aac_fail(ctx, AAC_ECUDA, "cublasDgemmStridedBatched failed");
-  return ls.end();
-}
-
-static int exact_apply(aac_ctx* ctx, const double* r, double* zbase, bool gmres_mode, int host_j) {
-  AAC_TRY(exact_prepare(ctx));
-  const int n = ctx->exact_n, ell = ctx->ell, h = ell / 2;
-  const long long N = ctx->geo.N, L = (long long)ell * N, NN = (long long)n * n;
-  const double V = 8.0 * L;
-  const Dft D = make_dft(ctx);
-  const IterState* st = gmres_mode ? ctx->d_st : nullptr;
-  if (gmres_mode) {
-    AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
-  } else if (ell <= 10) {
-    LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
-  } else {
-    LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
-  }
-  double* X = ctx->d_X;
-  // DST both sides: T = S W, X = T S; divide by mu - Lambda_k; back: T = S X, X = T S
-  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, ctx->d_what, NN, ctx->d_T));
-  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
-  ExactShifts Sh{};
-  for (int kb = 0; kb <= h; ++kb) shift_of_block(ctx, kb, &Sh.lr[kb], &Sh.li[kb]);
-  LAUNCH(ctx, KID_SWEEP, 2 * V, k_exact_scale<<<grid1d(NN, 256), 256, 0, ctx->stream>>>(n, ell, ctx->d_lam1, X, Sh));
-  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, X, NN, ctx->d_T));
-  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
-  NcFinal F{};
-  for (int kb = 0; kb <= h; ++kb) {
-    F.src[kb] = X + (long long)plane_of_block(ell, kb) * N;
-    F.tr[kb] = 1.0;
-    F.ti[kb] = 0.0;
-  }
-  return run_inverse(ctx, D, F, zbase, gmres_mode ? L : 0, st);
-}
+#include "exact_host.cuh"   // exact P_alpha for the paper operator (N3): host side
 
 extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
@@ -1377,169 +1270,4 @@ extern "C" int aac_profile_reset(aac_ctx* ctx) {
 }
 extern "C" long long aac_launch_count(const aac_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-// ------------------------------------------------------------------------------------------
-// Paper-reproduction mode: Dirichlet boundary faces, explicit spectral
-// bounds, the paper's outer CI.
-static void invalidate_plans(aac_ctx* ctx) {
-  for (auto& P : ctx->nc) P.method = 0;
-  if (ctx->exact_n > 0) {                       // the DST factorisation belongs to the old operator
-    cudaFree(ctx->d_S);
-    cudaFree(ctx->d_lam1);
-    cudaFree(ctx->d_T);
-    ctx->d_S = ctx->d_lam1 = ctx->d_T = nullptr;
-    ctx->exact_n = 0;
-  }
-  for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
-  ctx->graphs.clear();
-  sp_destroy(ctx);
-}
-
-extern "C" int aac_set_boundary(aac_ctx* ctx, double bx, double by, double bz) {
-  if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_boundary: NULL ctx");
-  if (!(bx >= 0.0 && by >= 0.0 && bz >= 0.0) || !std::isfinite(bx + by + bz))
-    return aac_fail(ctx, AAC_EINVAL, "boundary face weights must be finite and >= 0");
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  Geo& g = ctx->geo;
-  g.bdx = bx;
-  g.bdy = ctx->dim >= 2 ? by : 0.0;
-  g.bdz = ctx->dim >= 3 ? bz : 0.0;
-  g.dir = (g.bdx != 0.0 || g.bdy != 0.0 || g.bdz != 0.0) ? 1 : 0;
-  // Gershgorin bound with the boundary terms: max_P (1 + 2 sum_f w_f + sum_boundary bd)
-  const long long tot = ctx->wlen[0] + ctx->wlen[1] + ctx->wlen[2];
-  std::vector<double> hw(tot);
-  CUDA_TRY(ctx, cudaMemcpy(hw.data(), ctx->d_w, tot * sizeof(double), cudaMemcpyDeviceToHost));
-  const double* wx = hw.data();
-  const double* wy = wx + ctx->wlen[0];
-  const double* wz = wy + ctx->wlen[1];
-  double gmax = 1.0;
-  for (int z = 0; z < g.nz; ++z)
-    for (int y = 0; y < g.ny; ++y)
-      for (int x = 0; x < g.nx; ++x) {
-        const long long p = ((long long)z * g.ny + y) * g.nx + x;
-        double sum = wx[p] + wx[p + 1];
-        if (ctx->dim >= 2) sum += wy[p] + wy[p + g.nx];
-        if (ctx->dim >= 3) sum += wz[p] + wz[p + g.S];
-        double d = g.bdx * ((x == 0) + (x == g.nx - 1));
-        if (ctx->dim == 2) d += g.bdy * ((y == 0 && !g.has_lo) + (y == g.ny - 1 && !g.has_hi));
-        if (ctx->dim == 3)
-          d += g.bdy * ((y == 0) + (y == g.ny - 1)) + g.bdz * ((z == 0 && !g.has_lo) + (z == g.nz - 1 && !g.has_hi));
-        gmax = fmax(gmax, 1.0 + 2.0 * sum + d);
-      }
-  if (ctx->nranks > 1) {
-    ctx->h_stat[0] = gmax;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_stat, ctx->h_stat, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclMax));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    gmax = ctx->h_stat[0];
-  }
-  ctx->mu_min = 1.0;          // (a Dirichlet operator's mu_min is > 1: set it with aac_set_bounds)
-  ctx->mu_max = gmax;
-  invalidate_plans(ctx);
-  return AAC_OK;
-}
-
-extern "C" int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max) {
-  if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_bounds: NULL ctx");
-  if (!(mu_min > 0.0 && mu_max >= mu_min) || !std::isfinite(mu_max))
-    return aac_fail(ctx, AAC_EINVAL, "need 0 < mu_min <= mu_max");
-  if (!(pow(ctx->alpha, 1.0 / ctx->ell) < mu_min))
-    return aac_fail(ctx, AAC_EINVAL, "alpha^{1/ell} must be below mu_min (Lemma lemma:Zalpha)");
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->mu_min = mu_min;
-  ctx->mu_max = mu_max;
-  invalidate_plans(ctx);
-  return AAC_OK;
-}
-
-extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* x, double lmin,
-                      double lmax, double tol, int maxit, aac_gmres_info* info) {
-  if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_ci: bad pointers");
-  if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP && method != AAC_EXACT)
-    return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
-  if ((method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) && k < 1)
-    return aac_fail(ctx, AAC_EINVAL, "k must be >= 1");
-  if (!(lmin > 0.0 && lmax >= lmin) || !std::isfinite(lmax))
-    return aac_fail(ctx, AAC_EINVAL, "need 0 < lmin <= lmax");
-  if (!(tol >= 0.0) || maxit < 1) return aac_fail(ctx, AAC_EINVAL, "need tol >= 0, maxit >= 1");
-  if (method == AAC_SP && ctx->geo.dir) return aac_fail(ctx, AAC_EINVAL, "AAC_SP needs the Neumann operator");
-  if (method != AAC_NONE) AAC_TRY(check_alpha(ctx));
-  StreamScope ss(ctx);
-  const long long L = (long long)ctx->ell * ctx->geo.N;
-  const long long sweeps0 = ctx->sweeps;
-  double* xp = ctx->d_V;            // chi_{p-1}
-  double* r = ctx->d_V + L;         // b - calA chi_p
-  double* z = ctx->d_Z;             // P^{-1} r
-  double* y = ctx->d_W;             // calA chi_p
-  const unsigned nb = (unsigned)std::min<long long>(ctx->num_sms * 4, grid1d(L, 256));
-  CUDA_TRY(ctx, cudaMemsetAsync(x, 0, L * sizeof(double), ctx->stream));
-  CUDA_TRY(ctx, cudaMemsetAsync(xp, 0, L * sizeof(double), ctx->stream));
-  CUDA_TRY(ctx, cudaMemsetAsync(y, 0, L * sizeof(double), ctx->stream));
-  auto resid = [&](double* out) -> int {        // r = b - y, ||r||^2 -> host
-    LAUNCH(ctx, KID_AXPY, 24.0 * L, k_ci_resid<<<nb, 256, 0, ctx->stream>>>(b, y, r, L, ctx->d_part));
-    LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
-    AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    *out = sqrt(ctx->h_stat[0]);
-    return AAC_OK;
-  };
-  double bn = 0.0, rn = 0.0;
-  AAC_TRY(resid(&bn));                           // r_0 = b
-  if (method == AAC_SP) AAC_TRY(sp_prepare(ctx, k));
-  if (method == AAC_EXACT) AAC_TRY(exact_prepare(ctx));
-  int alloc_sum = 0;
-  if (method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) {
-    int al[AAC_MAX_ELL];
-    allocation(ctx, method, k, al);
-    for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
-  }
-  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
-  double rho = 0.0;
-  int p = 0;
-  rn = bn;
-  bool conv = bn == 0.0;
-  for (; p < maxit && !conv; ++p) {
-    const double* zp = r;
-    if (method == AAC_NC1 || method == AAC_NC2) {
-      AAC_TRY(nc_apply(ctx, method, k, r, z, false));
-      zp = z;
-    } else if (method == AAC_EXACT) {
-      AAC_TRY(exact_apply(ctx, r, z, false, 0));
-      zp = z;
-    } else if (method == AAC_SP) {
-      const Dft D = make_dft(ctx);
-      const long long N = ctx->geo.N;
-      if (ctx->ell <= 10)
-        LAUNCH(ctx, KID_FWD, 16.0 * L, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
-      else
-        LAUNCH(ctx, KID_FWD, 16.0 * L, (k_forward<16><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
-      AAC_TRY(sp_solve(ctx, k, z, 0, nullptr));
-      zp = z;
-    }
-    double a, c;
-    if (p == 0 || delta == 0.0) {
-      a = 0.0;
-      c = 1.0 / theta;
-      rho = delta / theta;
-    } else {
-      const double rho_new = 1.0 / (2.0 * theta / delta - rho);
-      a = rho_new * rho;
-      c = 2.0 * rho_new / delta;
-      rho = rho_new;
-    }
-    LAUNCH(ctx, KID_AXPY, 32.0 * L, k_ci_update<<<nb, 256, 0, ctx->stream>>>(x, xp, zp, a, c, L));
-    AAC_TRY(matvec_impl(ctx, x, y));
-    AAC_TRY(resid(&rn));
-    conv = rn < tol * bn;
-  }
-  if (info) {
-    info->iters = p;
-    info->converged = conv ? 1 : 0;
-    info->relres_est = bn > 0.0 ? rn / bn : 0.0;
-    info->relres_true = info->relres_est;
-    info->matvecs_paper_units = (long long)p * (ctx->ell + (method == AAC_SP ? sp_paper_matvecs(ctx, k) : alloc_sum));
-    info->stencil_sweeps = ctx->sweeps - sweeps0;
-  }
-  return conv ? AAC_OK : AAC_ENOCONV;
-}
+#include "paper_mode.cuh"   // aac_set_boundary / aac_set_bounds / aac_ci (N1)
