@@ -285,6 +285,167 @@ __global__ void __launch_bounds__(SP_T) k_mg_restrict(Geo g, const double* __res
   bc[(long long)pl * cstride + coff + pc] = acc;
 }
 
+// ---- plane-pair variants: one CTA per (tile, plane pair) -- the pair shares the point's face
+// weights, aggregate count and index arithmetic (loaded once for both planes) and gives each
+// thread two independent chains. Pair 0 = planes (0, ell-1) (the real blocks), pair k = the
+// (Re, Im) planes of complex block k.
+__device__ __forceinline__ void sp_pair(int ell, int pi, int& p0, int& p1) {
+  p0 = pi == 0 ? 0 : 2 * pi - 1;
+  p1 = pi == 0 ? ell - 1 : 2 * pi;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_restrict_pair(Geo g, const double* __restrict__ cnt, Geo gc,
+                                                           SpConst K, MgIo io, const double* bl,
+                                                           const double* xl, double* bc,
+                                                           const IterState* st, const double* hlo,
+                                                           const double* hhi, long long cstride,
+                                                           long long coff) {
+  if (st && st->done) return;
+  int pa, pb;
+  sp_pair(K.ell, blockIdx.y, pa, pb);
+  const long long pc = (long long)blockIdx.x * SP_T + threadIdx.x;
+  if (pc >= gc.N) return;
+  const int X = (int)(pc % gc.nx);
+  const long long rr = pc / gc.nx;
+  const int Y = (int)(rr % gc.ny), Z = (int)(rr / gc.ny);
+  const double sa = K.s[pa], sb = K.s[pb];
+  const double* ba = bl ? bl + (long long)pa * g.N : io.in[pa];
+  const double* bb = bl ? bl + (long long)pb * g.N : io.in[pb];
+  const double* xa = xl + (long long)pa * g.N;
+  const double* xb = xl + (long long)pb * g.N;
+  double acca = 0.0, accb = 0.0;
+  for (int dz = 0; dz < (DIM >= 3 ? 2 : 1); ++dz)
+    for (int dy = 0; dy < (DIM >= 2 ? 2 : 1); ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int fx = 2 * X + dx, fy = DIM >= 2 ? 2 * Y + dy : 0, fz = DIM >= 3 ? 2 * Z + dz : 0;
+        if (fx >= g.nx || fy >= g.ny || fz >= g.nz) continue;
+        PtV<DIM, 1> q;
+        load_ptv_xyz<DIM, 1>(g, fx, fy, fz, q);
+        const long long p = q.p;
+        const double c = cnt[p];
+        acca += ba[p] - mg_apply<DIM>(g, q, xa, (1.0 + sa) * c, hlo + (long long)pa * g.S, hhi + (long long)pa * g.S);
+        accb += bb[p] - mg_apply<DIM>(g, q, xb, (1.0 + sb) * c, hlo + (long long)pb * g.S, hhi + (long long)pb * g.S);
+      }
+  bc[(long long)pa * cstride + coff + pc] = acca;
+  bc[(long long)pb * cstride + coff + pc] = accb;
+}
+
+// per-(plane, CTA) partials of a pair kernel; the last CTA sums every plane in a fixed order
+__device__ __forceinline__ void sp_reduce_pair(const SpStepCtx& S, double va, double vb, int pa, int pb) {
+  __shared__ double red[2][SP_T / 32];
+  __shared__ bool last;
+  __shared__ double tot[AAC_MAX_ELL];
+  va = warp_sum(va);
+  vb = warp_sum(vb);
+  const int t = threadIdx.x;
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = va;
+    red[1][t >> 5] = vb;
+  }
+  __syncthreads();
+  const int ntile = gridDim.x;
+  if (t == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < SP_T / 32; ++w) {
+      sa += red[0][w];
+      sb += red[1][w];
+    }
+    S.part[(long long)pa * ntile + blockIdx.x] = sa;
+    S.part[(long long)pb * ntile + blockIdx.x] = sb;
+    __threadfence();
+    const unsigned tk = atomicAdd(S.tick, 1u);
+    last = (tk == gridDim.x * gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int ell = S.K.ell;
+  for (int q = 0; q < ell; ++q) {
+    const double sum = block_sum_fixed(S.part + (long long)q * ntile, ntile);
+    if (t == 0) tot[q] = sum;
+  }
+  if (t == 0) {
+    *S.tick = 0;
+    if (S.red) {
+      for (int q = 0; q < ell; ++q) S.red[q] = tot[q];
+    } else {
+      sp_scalar_B(S, tot);
+    }
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair(Geo g, const double* __restrict__ cnt,
+                                                               const double* __restrict__ dinv, Geo gc,
+                                                               MgIo io, const double* bl, const double* xl,
+                                                               const double* __restrict__ xc, double* x2l,
+                                                               SpStepCtx S, int level0) {
+  if (S.st && S.st->done) return;
+  int pa, pb;
+  sp_pair(S.K.ell, blockIdx.y, pa, pb);
+  double dota = 0.0, dotb = 0.0;
+  const double* xa = xl + (long long)pa * g.N;
+  const double* xb = xl + (long long)pb * g.N;
+  const double* ca = xc + (long long)pa * gc.N;
+  const double* cb = xc + (long long)pb * gc.N;
+  const double* ba = bl ? bl + (long long)pa * g.N : io.in[pa];
+  const double* bb = bl ? bl + (long long)pb * g.N : io.in[pb];
+  const double* da = dinv + (long long)sp_block_of(S.K.ell, pa) * g.N;
+  const double* db = dinv + (long long)sp_block_of(S.K.ell, pb) * g.N;
+  const double sa = S.K.s[pa], sb = S.K.s[pb];
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < g.N; p += (long long)gridDim.x * SP_T) {
+    PtV<DIM, 1> q;
+    load_ptv<DIM, 1>(g, p, q);
+    // neighbour offsets and aggregates (a boundary neighbour aliases the point)
+    auto agg = [&](int xx, int yy, int zz) { return ((long long)(zz / 2) * gc.ny + yy / 2) * gc.nx + xx / 2; };
+    const long long ac = agg(q.x, q.y, q.z);
+    const long long ow = q.x > 0 ? -1 : 0, oe = q.x < g.nx - 1 ? 1 : 0;
+    const long long aw = ow ? agg(q.x - 1, q.y, q.z) : ac, ae = oe ? agg(q.x + 1, q.y, q.z) : ac;
+    long long on = 0, os = 0, od = 0, ou = 0, an = ac, as = ac, ad = ac, au = ac;
+    if constexpr (DIM >= 2) {
+      on = q.y > 0 ? -(long long)g.nx : 0;
+      os = q.y < g.ny - 1 ? (long long)g.nx : 0;
+      an = on ? agg(q.x, q.y - 1, q.z) : ac;
+      as = os ? agg(q.x, q.y + 1, q.z) : ac;
+    }
+    if constexpr (DIM >= 3) {
+      od = q.z > 0 ? -g.S : 0;
+      ou = q.z < g.nz - 1 ? g.S : 0;
+      ad = od ? agg(q.x, q.y, q.z - 1) : ac;
+      au = ou ? agg(q.x, q.y, q.z + 1) : ac;
+    }
+    const double c = cnt ? cnt[p] : 1.0;
+    auto one = [&](const double* x, const double* xcp, const double* b, const double* di, double s,
+                   double& dot, int pl) {
+      const double u0 = x[p] + xcp[ac];
+      const double m = (1.0 + s) * c;
+      double a = m * u0;
+      a = fma(q.wx[0], u0 - (x[p + ow] + xcp[aw]), a);
+      a = fma(q.wx[1], u0 - (x[p + oe] + xcp[ae]), a);
+      if constexpr (DIM >= 2) {
+        a = fma(q.wym[0], u0 - (x[p + on] + xcp[an]), a);
+        a = fma(q.wyp[0], u0 - (x[p + os] + xcp[as]), a);
+      }
+      if constexpr (DIM >= 3) {
+        a = fma(q.wzm[0], u0 - (x[p + od] + xcp[ad]), a);
+        a = fma(q.wzp[0], u0 - (x[p + ou] + xcp[au]), a);
+      }
+      const double bp = b[p];
+      const double xn = u0 + SP_OMEGA * (bp - a) * di[p];
+      if (level0) {
+        io.out[pl][p] = xn;
+        dot = fma(xn, bp, dot);
+      } else {
+        x2l[(long long)pl * g.N + p] = xn;
+      }
+    };
+    one(xa, ca, ba, da, sa, dota, pa);
+    one(xb, cb, bb, db, sb, dotb, pb);
+  }
+  if (level0) sp_reduce_pair(S, dota, dotb, pa, pb);
+}
+
 // x_c = A_c(s)^{-1} b_c with the precomputed dense inverse of the plane's block (CTA per plane)
 __global__ void __launch_bounds__(SP_T) k_mg_coarse(int nc, const double* __restrict__ minv, int ell,
                                                     const double* bc, double* xc, const IterState* st) {
@@ -981,9 +1142,15 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
            k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.dinv, P->K, io, bl, a.x, st));
     if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
     if (gat) CUDA_TRY(ctx, cudaMemsetAsync(c.b, 0, (size_t)ell * c.g.N * sizeof(double), ctx->stream));
-    LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
-           k_mg_restrict<DIM><<<gc, SP_T, 0, ctx->stream>>>(a.g, a.cnt, gcl, P->K, io, bl, a.x, c.b, st, hlo,
-                                                            hhi, c.g.N, gat ? c.goff : 0));
+    static const bool no_pair = getenv("AAC_SP_PAIR") && atoi(getenv("AAC_SP_PAIR")) == 0;
+    if (no_pair)
+      LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+             k_mg_restrict<DIM><<<gc, SP_T, 0, ctx->stream>>>(a.g, a.cnt, gcl, P->K, io, bl, a.x, c.b, st, hlo,
+                                                              hhi, c.g.N, gat ? c.goff : 0));
+    else
+      LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
+             k_mg_restrict_pair<DIM><<<dim3(gc.x, ell / 2), SP_T, 0, ctx->stream>>>(
+                 a.g, a.cnt, gcl, P->K, io, bl, a.x, c.b, st, hlo, hhi, c.g.N, gat ? c.goff : 0));
     if (gat) AAC_TRY(comm_allreduce(ctx, c.b, (int)(ell * c.g.N), ncclSum));
   }
   SpLevel& cl = P->lev[nl - 1];
@@ -1025,9 +1192,15 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
              k_mg_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, io, bl, a.x, a.x2, S, l == 0 ? 1 : 0,
                                                           hlo, hhi));
     } else {                                               // x, x_c, b in; x2 out (+ C)
-      LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
-             k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2, a.x2, S,
-                                                                  l == 0 ? 1 : 0));
+      static const bool no_pair = getenv("AAC_SP_PAIR") && atoi(getenv("AAC_SP_PAIR")) == 0;
+      if (no_pair)
+        LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
+               k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2,
+                                                                    a.x2, S, l == 0 ? 1 : 0));
+      else
+        LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
+               k_mg_prolong_post_pair<DIM><<<dim3(gp.x, ell / 2), SP_T, 0, ctx->stream>>>(
+                   a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2, a.x2, S, l == 0 ? 1 : 0));
     }
   }
   return AAC_OK;
