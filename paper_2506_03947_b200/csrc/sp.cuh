@@ -690,9 +690,12 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
   if (S.st && S.st->done) return;
   const int kb = blockIdx.y, ell = S.K.ell, h = ell / 2;
   const long long N = g.N;
-  const SpBlk& b = S.blk[kb];
+  // block scalars read once (SZ stores may alias S.blk as far as the compiler knows, which
+  // would re-load them after every store and serialise the loop)
+  const bool stopped = S.blk[kb].stop != 0;
+  const double invg = stopped ? 0.0 : 1.0 / S.blk[kb].gamma;
   double dotp = 0.0;
-  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N && !b.stop;
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N && !stopped;
        p += (long long)gridDim.x * SP_T) {     // grid-stride: few reducing CTAs (see k_mg_post)
     PtV<DIM, 1> q;
     load_ptv<DIM, 1>(g, p, q);
@@ -705,7 +708,6 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
       dotp = fma(pp[p], a, dotp);
     } else {
       const int qu = 2 * kb - 1, qv = qu + 1;
-      const double invg = 1.0 / b.gamma;
       double azu[1], azv[1], zu[1], zv[1];
       apply_Av<DIM, 1>(g, q, v.Zc + (long long)qu * N, S.hlo + (long long)qu * g.S, S.hhi + (long long)qu * g.S,
                        azu, zu);
