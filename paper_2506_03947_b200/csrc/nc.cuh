@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(256) k_forward(long long N, Dft D, const doubl
 }
 
 constexpr int FT = 256;        // tile points per CTA (one per consumer thread)
+#define AAC_FWD_MAXC 128       // update coefficients staged in shared memory (more: global loads)
 constexpr int FS = 3;          // bulk-copy pipeline stages
 constexpr int FW = FT / 32;    // consumer warps; warp FW is the TMA producer
 
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   extern __shared__ __align__(16) double sm[];      // [FS][ELLC][FT]
   __shared__ __align__(8) uint64_t full[FS], empty[FS];
   __shared__ double red[FW];
+  __shared__ double coefs[AAC_FWD_MAXC];       // update coefficients, loaded once per CTA
   __shared__ bool last;
   IterState* st = U.ac.st;
   if (st->done) return;
@@ -152,6 +154,10 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
     }
     fence_mbar_init();
   }
+  // the item coefficients are read by every consumer thread for every item: one parallel load
+  // into shared memory instead of a dependent global load per item
+  for (int k = t; k < nitems && k < AAC_FWD_MAXC; k += blockDim.x)
+    coefs[k] = k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1];
   __syncthreads();
   double nrm = 0.0;
   if (warp == FW) {                                 // ---- producer warp
@@ -168,7 +174,8 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
     FOR_PL(pl) w[pl] = 0.0;
     for (int k = 0; k < nitems; ++k) {
       const int s = k % FS;
-      const double coef = k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1];
+      const double coef = k < AAC_FWD_MAXC ? coefs[k]
+                          : (k == 0 ? (j == 0 ? 1.0 : U.ac.sigma[j - 1]) : -U.ac.c[k - 1] * U.ac.sigma[k - 1]);
       const double* src = src_of(k) + base;
       if constexpr (TMA) mbar_wait(&full[s], (uint32_t)((k / FS) & 1));
       if (valid) {
