@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -30,3 +32,24 @@ def test_paper500_reference_arm_is_declared_unavailable():
     assert r.returncode == 0
     d = json.loads(r.stdout.strip())
     assert d["impl"] == "reference" and "unavailable" in d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["headline", "1d"])
+def test_bench_gpu_json_line(config):
+    """The driver's bench command on the GPU: one JSON line with the contract's keys, the
+    roofline and clocks objects, device-measured its/s and an end-to-end figure."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--steps", "2",
+                        "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "clocks", "roofline"):
+        assert k in d, k
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    rl = d["roofline"]
+    assert rl["bound"] in ("hbm", "alu") and 0 < rl["frac"] and rl["peak"] > 0
+    assert d["config"]["relres_true"] <= 1.5e-10
