@@ -732,16 +732,21 @@ __global__ void __launch_bounds__(SP_T) k_sp_upd1(long long N, int ell, SpVec v,
                                                   const IterState* st) {
   if (st && st->done) return;
   const int pl = blockIdx.y, h = ell / 2, kb = sp_block_of(ell, pl);
-  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
-  if (p >= N) return;
-  const long long o = (long long)pl * N + p;
   const SpBlk& b = blk[kb];
   if (b.stop == 1) return;
-  if (kb == 0 || kb == h) {
-    v.X[o] = fma(b.alpha, v.P[o], v.X[o]);
-    v.R[o] = fma(-b.alpha, v.SZ[o], v.R[o]);
-  } else {
-    v.Vn[o] = v.SZ[o] - b.dcoef * v.Vc[o] - b.vcoef * v.Vp[o];
+  // block scalars once per thread; grid-stride over the plane (the vectors are not aliased with
+  // blk, but the compiler cannot know: loading the scalars inside the loop would re-load them)
+  const double alpha = b.alpha, dcoef = b.dcoef, vcoef = b.vcoef;
+  const bool real = kb == 0 || kb == h;
+  const long long o0 = (long long)pl * N;
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N; p += (long long)gridDim.x * SP_T) {
+    const long long o = o0 + p;
+    if (real) {
+      v.X[o] = fma(alpha, v.P[o], v.X[o]);
+      v.R[o] = fma(-alpha, v.SZ[o], v.R[o]);
+    } else {
+      v.Vn[o] = v.SZ[o] - dcoef * v.Vc[o] - vcoef * v.Vp[o];
+    }
   }
 }
 
@@ -751,18 +756,21 @@ __global__ void __launch_bounds__(SP_T) k_sp_upd2(long long N, int ell, SpVec v,
                                                   const IterState* st) {
   if (st && st->done) return;
   const int pl = blockIdx.y, h = ell / 2, kb = sp_block_of(ell, pl);
-  const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
-  if (p >= N) return;
-  const long long o = (long long)pl * N + p;
   const SpBlk& b = blk[kb];
   if (b.stop == 1) return;
-  if (kb == 0 || kb == h) {
-    v.P[o] = fma(b.beta, v.P[o], v.Zr[o]);
-  } else {
-    const double zs = v.Zc[o] / b.gamma_prev;
-    const double wn = (zs - b.a3 * v.Wp[o] - b.a2 * v.Wc[o]) / b.a1;
-    v.Wn[o] = wn;
-    v.X[o] = fma(b.xcoef, wn, v.X[o]);
+  const double beta = b.beta, gp = b.gamma_prev, a1 = b.a1, a2 = b.a2, a3 = b.a3, xcoef = b.xcoef;
+  const bool real = kb == 0 || kb == h;
+  const long long o0 = (long long)pl * N;
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N; p += (long long)gridDim.x * SP_T) {
+    const long long o = o0 + p;
+    if (real) {
+      v.P[o] = fma(beta, v.P[o], v.Zr[o]);
+    } else {
+      const double zs = v.Zc[o] / gp;
+      const double wn = (zs - a3 * v.Wp[o] - a2 * v.Wc[o]) / a1;
+      v.Wn[o] = wn;
+      v.X[o] = fma(xcoef, wn, v.X[o]);
+    }
   }
 }
 
@@ -1269,11 +1277,13 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
                               ctx->stream>>>(ctx->geo, vecs(), S));
     AAC_TRY(finish(h + 1, 0));
     LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
-           k_sp_upd1<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
+           k_sp_upd1<<<dim3(std::min<unsigned>(gt, 16 * ctx->num_sms / ell + 1), ell), SP_T, 0, ctx->stream>>>(
+               N, ell, vecs(), P->blk, st));
     AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
     AAC_TRY(finish(ell, 1));
     LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
-           k_sp_upd2<<<dim3(gt, ell), SP_T, 0, ctx->stream>>>(N, ell, vecs(), P->blk, st));
+           k_sp_upd2<<<dim3(std::min<unsigned>(gt, 16 * ctx->num_sms / ell + 1), ell), SP_T, 0, ctx->stream>>>(
+               N, ell, vecs(), P->blk, st));
     // rotate: v_prev <- v <- v_next, z <- z_next, w_prev <- w <- w_next
     double* t = Vp; Vp = Vc; Vc = Vn; Vn = t;
     t = Zc; Zc = Zn; Zn = t;
