@@ -46,12 +46,13 @@ def _peaks():
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
-def _ncu_traffic(kernel):
+def _ncu_traffic(config, kernel):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of a kernel class
-    from the committed ncu --set full summary (profiles/ncu_traffic.json), or None."""
+    on this workload from the committed ncu --set full summary (profiles/ncu_traffic.json,
+    keyed by config then kernel class), or None when that workload was not captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f)[kernel]["dram_bytes_per_launch"]
+            return json.load(f)[config][kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -272,7 +273,7 @@ def run_ours(args):
     if dom[1]["ms"] > 0:
         nl = max(1, dom[1]["launches"])
         ach_hbm = dom[1]["model_bytes"] / (dom[1]["ms"] / 1e3) / 1e9
-        tr = _ncu_traffic(dom[0])
+        tr = _ncu_traffic(args.config, dom[0])
         if dom[1].get("model_flops", 0.0) > 0:
             # arithmetic-bound kernel (the wavefront Chebyshev solve): fp64 flops vs the
             # derived fp64 peak; its HBM view is reported beside it

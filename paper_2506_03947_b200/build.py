@@ -33,7 +33,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp", SRC, "-ldl"]
+    extra = os.environ.get("AAC_EXTRA_NVCC", "").split()    # experiments only (-D overrides)
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-o", LIB + ".tmp", SRC, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -48,7 +48,7 @@ for r in rr[2:]:
                      "dram_read": val(r, "dram__bytes_read.sum"), "dram_write": val(r, "dram__bytes_write.sum"),
                      "kernel": name.split("(")[0],
                      "source": f"profiles/r01_ncu_summary.md ({ver} capture, one GMRES step of the headline)"}
-json.dump(tr, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+json.dump({"headline": tr}, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 head = json.load(open(os.path.join(dst, "b_head.json")))
 with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.md"), "a") as f:
     f.write(f"\n## {ver}: headline 1024², ℓ=10, NC2 k=8 — {head['value']:.1f} its/s device, "
