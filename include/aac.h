@@ -155,6 +155,18 @@ int aac_gmres(aac_ctx* ctx, int method, int k, const double* b, double* x,
 int aac_gmres_host(aac_ctx* ctx, int method, int k, const double* b_host, double* x_host,
                    double rtol, int maxit, aac_gmres_info* info);
 
+/* aac_gmres_host for nrhs independent systems (BASELINE.json north_star: one
+ * solve per right-hand side), pipelined: while system i is solved on the
+ * context stream, b_{i+1} is copied in and x_{i-1} copied out on a second
+ * stream (two device slots each; pinned host memory makes the copies
+ * asynchronous, pageable memory still works but stages through the driver).
+ * b_host[i], x_host[i]: host [ell][n_local] each (x_host[i] may repeat a
+ * buffer: the copies out are ordered). info: NULL or nrhs entries. Returns
+ * the worst code over the systems (AAC_ENOCONV if any reached maxit); on an
+ * error (< 0) the systems after the failing one are not solved.               */
+int aac_gmres_host_batch(aac_ctx* ctx, int method, int k, int nrhs, const double* const* b_host,
+                         double* const* x_host, double rtol, int maxit, aac_gmres_info* info);
+
 /* Spectral bounds used by the inner solvers (mu_min = 1 exactly, mu_max =
  * global Gershgorin max) and the per-block inner iteration counts for
  * (method, k), block k = 0..ell-1 (alloc may be NULL). n_local may be NULL.      */

@@ -19,7 +19,7 @@ METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP, "exac
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",
-           "aac_gmres_host", "aac_query", "aac_profile_enable", "aac_profile_count",
+           "aac_gmres_host", "aac_gmres_host_batch", "aac_query", "aac_profile_enable", "aac_profile_count",
            "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_set_boundary",
            "aac_set_bounds", "aac_ci", "aac_launch_count", "aac_last_error",
            "aac_destroy"]
@@ -76,6 +76,8 @@ def _load():
         "aac_precond_apply": (I, [P, I, I, P, P]),
         "aac_gmres": (I, [P, I, I, P, P, D, I, ctypes.POINTER(aac_gmres_info)]),
         "aac_gmres_host": (I, [P, I, I, dp, dp, D, I, ctypes.POINTER(aac_gmres_info)]),
+        "aac_gmres_host_batch": (I, [P, I, I, I, ctypes.POINTER(dp), ctypes.POINTER(dp), D, I,
+                                     ctypes.POINTER(aac_gmres_info)]),
         "aac_query": (I, [P, I, I, dp, dp, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_int64)]),
         "aac_profile_enable": (I, [P, I]),
         "aac_profile_count": (I, []),

@@ -393,7 +393,7 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   sp_destroy(ctx);
   for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
   double* ptrs[] = {ctx->d_w, ctx->d_what, ctx->d_X, ctx->d_tmp, ctx->d_V, ctx->d_Z,
-                    ctx->d_W, ctx->d_bx, ctx->d_halo, ctx->d_part, ctx->d_red, ctx->d_H,
+                    ctx->d_W, ctx->d_bx, ctx->d_bb, ctx->d_halo, ctx->d_part, ctx->d_red, ctx->d_H,
                     ctx->d_G, ctx->d_giv, ctx->d_stat};
   for (double* p : ptrs)
     if (p) cudaFree(p);
@@ -409,6 +409,9 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
+  for (auto e : ctx->ev_cp)
+    if (e) cudaEventDestroy(e);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto& r : ctx->prof_recs) {
     cudaEventDestroy(r.a);
@@ -1217,6 +1220,62 @@ extern "C" int aac_gmres_host(aac_ctx* ctx, int method, int k, const double* b_h
   CUDA_TRY(ctx, cudaMemcpyAsync(x_host, ctx->d_bx + L, L * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return rc;
+}
+
+// Several right-hand sides from the host, copies overlapped with the solves: the H2D copy of
+// b_{i+1} and the D2H copy of x_{i-1} run on a copy stream while system i is solved (two device
+// slots each for b and x; events order every reuse of a slot).
+extern "C" int aac_gmres_host_batch(aac_ctx* ctx, int method, int k, int nrhs, const double* const* b_host,
+                                    double* const* x_host, double rtol, int maxit, aac_gmres_info* info) {
+  if (!ctx || nrhs < 0 || (nrhs > 0 && (!b_host || !x_host)))
+    return aac_fail(ctx, AAC_EINVAL, "aac_gmres_host_batch: bad arguments");
+  for (int i = 0; i < nrhs; ++i)
+    if (!b_host[i] || !x_host[i]) return aac_fail(ctx, AAC_EINVAL, "aac_gmres_host_batch: NULL vector %d", i);
+  if (nrhs == 0) return AAC_OK;
+  const long long L = (long long)ctx->ell * ctx->geo.N;
+  const size_t bytes = L * sizeof(double);
+  if (!ctx->d_bb && cudaMalloc((void**)&ctx->d_bb, 4 * bytes) != cudaSuccess) {
+    ctx->d_bb = nullptr;
+    cudaGetLastError();
+    return aac_fail(ctx, AAC_ENOMEM, "batch staging allocation failed");
+  }
+  if (!ctx->cstream) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_cp) CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* ev_in = ctx->ev_cp;
+  cudaEvent_t* ev_done = ctx->ev_cp + 2;
+  cudaEvent_t* ev_out = ctx->ev_cp + 4;
+  auto B = [&](int s) { return ctx->d_bb + (long long)s * L; };
+  auto X = [&](int s) { return ctx->d_bb + (long long)(2 + s) * L; };
+  StreamScope ss(ctx);
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->cstream, ctx->ev_in, 0));   // after the caller's work
+  CUDA_TRY(ctx, cudaMemcpyAsync(B(0), b_host[0], bytes, cudaMemcpyHostToDevice, ctx->cstream));
+  CUDA_TRY(ctx, cudaEventRecord(ev_in[0], ctx->cstream));
+  int worst = AAC_OK;
+  for (int i = 0; i < nrhs; ++i) {
+    const int s = i & 1;
+    if (i + 1 < nrhs) {                          // prefetch b_{i+1} into the other slot
+      const int s1 = (i + 1) & 1;
+      if (i >= 1) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->cstream, ev_done[s1], 0));   // solve i-1 done with it
+      CUDA_TRY(ctx, cudaMemcpyAsync(B(s1), b_host[i + 1], bytes, cudaMemcpyHostToDevice, ctx->cstream));
+      CUDA_TRY(ctx, cudaEventRecord(ev_in[s1], ctx->cstream));
+    }
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ev_in[s], 0));
+    if (i >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ev_out[s], 0));       // x_{i-2} copied out
+    const int rc = gmres_impl(ctx, method, k, B(s), X(s), rtol, maxit, info ? info + i : nullptr);
+    if (rc < 0) {
+      cudaStreamSynchronize(ctx->cstream);
+      return rc;
+    }
+    worst = std::max(worst, rc);
+    CUDA_TRY(ctx, cudaEventRecord(ev_done[s], ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->cstream, ev_done[s], 0));
+    CUDA_TRY(ctx, cudaMemcpyAsync(x_host[i], X(s), bytes, cudaMemcpyDeviceToHost, ctx->cstream));
+    CUDA_TRY(ctx, cudaEventRecord(ev_out[s], ctx->cstream));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->cstream));
+  return worst;
 }
 
 extern "C" int aac_query(aac_ctx* ctx, int method, int k, double* mu_min, double* mu_max, int* alloc,

@@ -101,6 +101,9 @@ struct aac_ctx {
   double* d_Z = nullptr;               // [max_krylov][ell][N]
   double* d_W = nullptr;               // [ell][N] Arnoldi work vector
   double* d_bx = nullptr;              // [2][ell][N] staging for aac_gmres_host
+  double* d_bb = nullptr;              // [4][ell][N] b | b | x | x for aac_gmres_host_batch
+  cudaStream_t cstream = nullptr;      // copy stream of aac_gmres_host_batch
+  cudaEvent_t ev_cp[6] = {};           // in[2] | done[2] | out[2]
   double* d_halo = nullptr;            // [2][ell][S]  lo | hi
   double* d_part = nullptr;            // per-CTA partial sums
   unsigned* d_grp = nullptr;           // two-level ticket counters (zeroed)

@@ -397,27 +397,30 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair(Geo g, const doub
   for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < g.N; p += (long long)gridDim.x * SP_T) {
     PtV<DIM, 1> q;
     load_ptv<DIM, 1>(g, p, q);
-    // neighbour offsets and aggregates (a boundary neighbour aliases the point)
-    auto agg = [&](int xx, int yy, int zz) { return ((long long)(zz / 2) * gc.ny + yy / 2) * gc.nx + xx / 2; };
-    const long long ac = agg(q.x, q.y, q.z);
+    // neighbour offsets and aggregates (a boundary neighbour aliases the point); a neighbour's
+    // aggregate differs from the point's only across an aggregate edge (coordinate parity)
+    const long long ac = ((long long)(q.z / 2) * gc.ny + q.y / 2) * gc.nx + q.x / 2;
     const long long ow = q.x > 0 ? -1 : 0, oe = q.x < g.nx - 1 ? 1 : 0;
-    const long long aw = ow ? agg(q.x - 1, q.y, q.z) : ac, ae = oe ? agg(q.x + 1, q.y, q.z) : ac;
+    const long long aw = ac - (ow != 0 && !(q.x & 1)), ae = ac + (oe != 0 && (q.x & 1));
     long long on = 0, os = 0, od = 0, ou = 0, an = ac, as = ac, ad = ac, au = ac;
     if constexpr (DIM >= 2) {
       on = q.y > 0 ? -(long long)g.nx : 0;
       os = q.y < g.ny - 1 ? (long long)g.nx : 0;
-      an = on ? agg(q.x, q.y - 1, q.z) : ac;
-      as = os ? agg(q.x, q.y + 1, q.z) : ac;
+      an = ac - (on != 0 && !(q.y & 1)) * (long long)gc.nx;
+      as = ac + (os != 0 && (q.y & 1)) * (long long)gc.nx;
     }
     if constexpr (DIM >= 3) {
+      const long long cS = (long long)gc.nx * gc.ny;
       od = q.z > 0 ? -g.S : 0;
       ou = q.z < g.nz - 1 ? g.S : 0;
-      ad = od ? agg(q.x, q.y, q.z - 1) : ac;
-      au = ou ? agg(q.x, q.y, q.z + 1) : ac;
+      ad = ac - (od != 0 && !(q.z & 1)) * cS;
+      au = ac + (ou != 0 && (q.z & 1)) * cS;
     }
     const double c = cnt ? cnt[p] : 1.0;
+    // both planes computed before either is stored (the stores may alias the inputs as far as
+    // the compiler knows: storing between them would serialise the two planes' loads)
     auto one = [&](const double* x, const double* xcp, const double* b, const double* di, double s,
-                   double& dot, int pl) {
+                   double& bp) -> double {
       const double u0 = x[p] + xcp[ac];
       const double m = (1.0 + s) * c;
       double a = m * u0;
@@ -431,17 +434,21 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair(Geo g, const doub
         a = fma(q.wzm[0], u0 - (x[p + od] + xcp[ad]), a);
         a = fma(q.wzp[0], u0 - (x[p + ou] + xcp[au]), a);
       }
-      const double bp = b[p];
-      const double xn = u0 + SP_OMEGA * (bp - a) * di[p];
-      if (level0) {
-        io.out[pl][p] = xn;
-        dot = fma(xn, bp, dot);
-      } else {
-        x2l[(long long)pl * g.N + p] = xn;
-      }
+      bp = b[p];
+      return u0 + SP_OMEGA * (bp - a) * di[p];
     };
-    one(xa, ca, ba, da, sa, dota, pa);
-    one(xb, cb, bb, db, sb, dotb, pb);
+    double bpa, bpb;
+    const double xna = one(xa, ca, ba, da, sa, bpa);
+    const double xnb = one(xb, cb, bb, db, sb, bpb);
+    if (level0) {
+      io.out[pa][p] = xna;
+      io.out[pb][p] = xnb;
+      dota = fma(xna, bpa, dota);
+      dotb = fma(xnb, bpb, dotb);
+    } else {
+      x2l[(long long)pa * g.N + p] = xna;
+      x2l[(long long)pb * g.N + p] = xnb;
+    }
   }
   if (level0) sp_reduce_pair(S, dota, dotb, pa, pb);
 }

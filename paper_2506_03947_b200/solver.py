@@ -5,6 +5,7 @@
     z = s.precond_apply("nc2", 8, r)                     # aac_precond_apply    (z ~ P^{-1} r)
     x, info = s.gmres("nc2", 8, b, rtol=1e-10)           # aac_gmres            (device tensors)
     x, info = s.gmres_host("nc2", 8, b_numpy)            # aac_gmres_host       (host arrays)
+    xs, infos = s.gmres_host_batch("nc2", 8, [b0, b1])  # aac_gmres_host_batch (pipelined copies)
 
 Block vectors are torch.float64 CUDA tensors of shape [ell, n_local] (or anything that
 reshapes to it) holding this rank's slab; see include/aac.h for the layout.
@@ -164,6 +165,28 @@ class Solver:
                                 int(maxit or self.max_krylov), ctypes.byref(info))
         check(rc, self.ctx, ok=(_lib.AAC_OK, _lib.AAC_ENOCONV))
         return x, info.asdict()
+
+    def gmres_host_batch(self, method, k, bs, xs=None, rtol=1e-10, maxit=None):
+        """aac_gmres_host_batch: one solve per host right-hand side in `bs`, the copies in and
+        out overlapped with the solves. Returns (xs, [info, ...])."""
+        bs = [np.ascontiguousarray(b, dtype=np.float64) for b in bs]
+        for b in bs:
+            if b.size != self.ell * self.n_local:
+                raise ValueError("b has the wrong size")
+        xs = [np.empty_like(b) for b in bs] if xs is None else list(xs)
+        if len(xs) != len(bs):
+            raise ValueError("xs and bs differ in length")
+        for x in xs:
+            if x.dtype != np.float64 or not x.flags.c_contiguous or x.size != self.ell * self.n_local:
+                raise ValueError("x must be a C-contiguous float64 array of ell * n_local values")
+        n = len(bs)
+        bp = (ctypes.POINTER(ctypes.c_double) * max(n, 1))(*[_dptr(b) for b in bs])
+        xp = (ctypes.POINTER(ctypes.c_double) * max(n, 1))(*[_dptr(x) for x in xs])
+        infos = (aac_gmres_info * max(n, 1))()
+        rc = lib.aac_gmres_host_batch(self.ctx, _method(method), int(k), n, bp, xp, float(rtol),
+                                      int(maxit or self.max_krylov), infos)
+        check(rc, self.ctx, ok=(_lib.AAC_OK, _lib.AAC_ENOCONV))
+        return xs, [infos[i].asdict() for i in range(n)]
 
     def allocation(self, method, k):
         al = (ctypes.c_int * self.ell)()

@@ -78,3 +78,13 @@ def _setup(dim=2, n=(8, 6, 1), ell=4, alpha=0.1, c=0.01, kx=None, ky=None, kz=No
 def test_setup_validation(kw, frag):
     rc, msg = _setup(**kw)
     assert rc == -1 and frag in msg
+
+
+def test_null_context_calls_fail_cleanly():
+    """Every ctx-taking entry point returns AAC_EINVAL on a NULL context (no CUDA work)."""
+    from paper_2506_03947_b200 import _lib
+    L = _lib.lib
+    assert L.aac_gmres_host_batch(None, 2, 8, 1, None, None, 1e-10, 10, None) == -1
+    assert L.aac_gmres_host(None, 2, 8, None, None, 1e-10, 10, None) == -1
+    assert L.aac_gmres(None, 2, 8, None, None, 1e-10, 10, None) == -1
+    assert L.aac_matvec(None, None, None) == -1
