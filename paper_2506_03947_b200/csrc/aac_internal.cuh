@@ -119,6 +119,8 @@ struct aac_ctx {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   int wave_h = 8;                      // wavefront depth (wave.cuh; 0 = per-step sweeps)
+  bool wave_forced = false;            // AAC_WAVE_H given: no automatic choice (wave_pays)
+  int l2_bytes = 0;                    // L2 size (the wave / per-step choice)
   // slab-decomposed wavefront (2D, several ranks): face weights of rows [elo, ehi) of the
   // global grid (this slab +- WAVE halo rows) and halo rows of hat w
   double* d_wext = nullptr;            // wx | wy of the extended row range

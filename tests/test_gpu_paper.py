@@ -159,3 +159,29 @@ def test_exact_outer_ci_and_gmres(alpha):
     if alpha <= 1e-2:                     # spectrum {1} u {mu^ell/(mu^ell - alpha)} clusters at 1
         assert ig["iters"] <= 4
     s.close()
+
+
+def test_wave_policy_auto(monkeypatch):
+    """Without AAC_WAVE_H the library picks the organisation (aac.cu wave_pays): the wavefront
+    when every block's steps fit in one pass, per-step sweeps for many steps on an L2-resident
+    problem. Both choices stay parity-exact."""
+    monkeypatch.delenv("AAC_WAVE_H", raising=False)
+    cases = [(synth.make_paper_problem(50, 10, 0.01, eta=0.2), "nc2", False),   # 100 steps: sweeps
+             (synth.make_problem("headline", shape=(1, 40, 48)), "nc2", True)]  # 8 steps: one wave pass
+    for p, m, wave in cases:
+        s = _solver(p)
+        if p.name.startswith("paper"):
+            w = paper.weights(p.shape[-1], p.ell)
+            mu0, mu1 = paper.bounds(p.shape[-1], p.ell)
+        else:
+            w = op.weights(p)
+            mu0, mu1 = 1.0, op.gershgorin_max(w)
+        al = s.allocation(m, p.k)
+        r = np.random.default_rng(4).standard_normal((p.ell,) + p.shape)
+        s.profile(True)
+        z = s.precond_apply(m, p.k, _dev(r, p.ell)).cpu().numpy()
+        prof = s.profile_read()
+        s.profile(False)
+        assert (prof["cheb_sweep"]["model_flops"] > 0) == wave, (p.shape, prof["cheb_sweep"])
+        assert _rel(z, ch.nc_apply(w, r, p.ell, p.alpha, mu0, mu1, al)) <= 1e-12
+        s.close()
