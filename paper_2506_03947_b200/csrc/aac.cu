@@ -1088,16 +1088,23 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   return AAC_OK;
 }
 
+// IterState (or n doubles) device -> pinned host without a copy engine (k_publish)
+static int publish(aac_ctx* ctx, const void* dsrc, void* hdst, size_t bytes) {
+  void* hd = nullptr;
+  CUDA_TRY(ctx, cudaHostGetDevicePointer(&hd, hdst, 0));
+  const int n = (int)(bytes / sizeof(unsigned));
+  LAUNCH(ctx, KID_SCALAR, 0, k_publish<<<1, 32, 0, ctx->stream>>>(static_cast<const unsigned*>(dsrc),
+                                                                  static_cast<unsigned*>(hd), n));
+  return AAC_OK;
+}
+
 static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
   for (auto& ge : ctx->graphs)
     if (ge.method == method && ge.k == k) { *out = &ge; return AAC_OK; }
   const long long l0 = ctx->launches;
   CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   int rc = arnoldi_step(ctx, method, k, 0);
-  if (rc == AAC_OK) {
-    cudaError_t e = cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e != cudaSuccess) rc = aac_fail(ctx, AAC_ECUDA, "capture memcpy: %s", cudaGetErrorString(e));
-  }
+  if (rc == AAC_OK) rc = publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState));
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != AAC_OK) {
@@ -1134,8 +1141,11 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   init.maxit = maxit;
   init.rtol = rtol;
   *ctx->h_st = init;
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_st, ctx->h_st, sizeof(IterState), cudaMemcpyHostToDevice, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_V, b, L * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  // (kernels, not copy engines: a concurrent host transfer of aac_gmres_host_batch must not
+  // delay the solve)
+  LAUNCH(ctx, KID_SCALAR, 0, k_set_state<<<1, 1, 0, ctx->stream>>>(ctx->d_st, init));
+  LAUNCH(ctx, KID_AXPY, 16.0 * L,
+         k_copy<<<std::min<long long>(4LL * ctx->num_sms, grid1d(L, 256)), 256, 0, ctx->stream>>>(b, ctx->d_V, L));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_giv, 0, 6LL * ldh * sizeof(double), ctx->stream));
   int alloc_sum = 0;
   if (method != AAC_EXACT) {
@@ -1160,7 +1170,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
       }
     } else {
       AAC_TRY(arnoldi_step(ctx, method, k, it));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream));
+      AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
       CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       if (ctx->h_st->done) break;
     }
@@ -1177,7 +1187,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   double* yy = ctx->d_giv + 3 * ldh;
   LAUNCH(ctx, KID_SCALAR, 0,
          k_backsub<<<1, 1, 0, ctx->stream>>>(ctx->d_st, ldh, ctx->d_H, ctx->d_giv + 2 * ldh, ctx->d_giv + 4 * ldh, yy));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(IterState), cudaMemcpyDeviceToHost, ctx->stream));
+  AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   const IterState fin = *ctx->h_st;
   const int m = fin.m;
@@ -1195,7 +1205,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
     LAUNCH(ctx, KID_AXPY, 16.0 * L, k_diffnorm<<<nb, 256, 0, ctx->stream>>>(b, ctx->d_tmp, L, ctx->d_part));
     LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
     AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    AAC_TRY(publish(ctx, ctx->d_stat, ctx->h_stat, sizeof(double)));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     rtrue = sqrt(ctx->h_stat[0]) / fin.beta;
   }

@@ -29,6 +29,22 @@ struct IterState {
   double hn;        // last H[j+1, j]
 };
 
+// Publish n 32-bit words of device state into pinned (mapped) host memory from a kernel: the
+// host reads it after an event / stream sync. Unlike a D2H memcpy this needs no copy engine, so
+// the per-step poll never queues behind a large host transfer on another stream
+// (aac_gmres_host_batch moves whole vectors in and out while the solves run).
+__global__ void k_publish(const unsigned* __restrict__ src, unsigned* dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// Solve start without copy engines (see k_publish): the state from a kernel argument, V_0 = b.
+__global__ void k_set_state(IterState* st, IterState v) { *st = v; }
+__global__ void __launch_bounds__(256) k_copy(const double* __restrict__ src, double* __restrict__ dst,
+                                              long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 struct ArnoldiCtx {
   IterState* st;
   double* H;        // (ldh x max_krylov) column-major, ldh = max_krylov + 1

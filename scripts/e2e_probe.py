@@ -12,6 +12,7 @@ import synth  # noqa: E402
 from paper_2506_03947_b200 import from_problem  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "headline"
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 p = synth.make_problem(name)
 s = from_problem(p)
 b = np.ascontiguousarray(p.b.reshape(p.ell, -1))
@@ -30,16 +31,16 @@ bd = bh.cuda()
 for rep in range(3):
     torch.cuda.synchronize(); t = time.perf_counter()
     its = 0
-    for _ in range(5):
+    for _ in range(K):
         _, info = s.gmres(meth, k, bd, rtol=p.rtol)
         its += info["iters"]
     torch.cuda.synchronize(); dev = its / (time.perf_counter() - t)
     t = time.perf_counter()
-    _, infos = s.gmres_host_batch(meth, k, [bh.numpy()] * 5, [xh.numpy()] * 5, rtol=p.rtol)
+    _, infos = s.gmres_host_batch(meth, k, [bh.numpy()] * K, [xh.numpy()] * K, rtol=p.rtol)
     bat = sum(i["iters"] for i in infos) / (time.perf_counter() - t)
     t = time.perf_counter()
     its = 0
-    for _ in range(5):
+    for _ in range(K):
         _, info = s.gmres_host(meth, k, bh.numpy(), xh.numpy(), rtol=p.rtol)
         its += info["iters"]
     ser = its / (time.perf_counter() - t)
