@@ -104,7 +104,7 @@ extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* 
     LAUNCH(ctx, KID_AXPY, 24.0 * L, k_ci_resid<<<nb, 256, 0, ctx->stream>>>(b, y, r, L, ctx->d_part));
     LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
     AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stat, ctx->d_stat, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    AAC_TRY(publish(ctx, ctx->d_stat, ctx->h_stat, sizeof(double)));   // (no copy engine, as aac_gmres)
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     *out = sqrt(ctx->h_stat[0]);
     return AAC_OK;
