@@ -186,6 +186,12 @@ def test_gmres_host_batch_matches_device_path():
     xs2, _ = s.gmres_host_batch("nc2", 8, bs[:3], [xo] * 3, rtol=p.rtol, maxit=40)
     assert np.array_equal(xo, xs[2])
     assert s.gmres_host_batch("nc2", 8, [])[0] == []
+    # maxit reached on every system: AAC_ENOCONV is a completed call, each x is the last iterate
+    xs3, infos3 = s.gmres_host_batch("nc2", 8, bs[:2], rtol=p.rtol, maxit=3)
+    for b, x, info in zip(bs[:2], xs3, infos3):
+        xd, info_d = s.gmres("nc2", 8, torch.from_numpy(np.ascontiguousarray(b)).cuda(), rtol=p.rtol, maxit=3)
+        assert info["iters"] == info_d["iters"] == 3 and info["converged"] == 0
+        assert np.array_equal(xd.cpu().numpy(), x)
     s.close()
 
 
