@@ -453,6 +453,75 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair(Geo g, const doub
   if (level0) sp_reduce_pair(S, dota, dotb, pa, pb);
 }
 
+// 2D variant of k_mg_prolong_post_pair on a row grid (grid-stride over rows, threads over x):
+// the generic kernel spends ~70% of its ~310 instructions per point pair on flat-index and
+// aggregate arithmetic; here every neighbour is a row pointer fixed once per row plus the column,
+// and the aggregate of a neighbour follows from the coordinate parity. Same operations in the
+// same order: bit-identical results.
+__global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair2(Geo g, const double* __restrict__ cnt,
+                                                                const double* __restrict__ dinv, Geo gc,
+                                                                MgIo io, const double* bl, const double* xl,
+                                                                const double* __restrict__ xc, double* x2l,
+                                                                SpStepCtx S, int level0) {
+  if (S.st && S.st->done) return;
+  int pa, pb;
+  sp_pair(S.K.ell, blockIdx.y, pa, pb);
+  double dota = 0.0, dotb = 0.0;
+  const int nx = g.nx, ny = g.ny, cnx = gc.nx;
+  const double sa = S.K.s[pa], sb = S.K.s[pb];
+  const double* xa = xl + (long long)pa * g.N;
+  const double* xb = xl + (long long)pb * g.N;
+  const double* ca = xc + (long long)pa * gc.N;
+  const double* cb = xc + (long long)pb * gc.N;
+  const double* ba = bl ? bl + (long long)pa * g.N : io.in[pa];
+  const double* bb = bl ? bl + (long long)pb * g.N : io.in[pb];
+  const double* da = dinv + (long long)sp_block_of(S.K.ell, pa) * g.N;
+  const double* db = dinv + (long long)sp_block_of(S.K.ell, pb) * g.N;
+  double* oa = level0 ? io.out[pa] : x2l + (long long)pa * g.N;
+  double* ob = level0 ? io.out[pb] : x2l + (long long)pb * g.N;
+  for (int y = blockIdx.x; y < ny; y += gridDim.x) {
+    const long long r0 = (long long)y * nx;
+    const int on = y > 0 ? -nx : 0, os = y < ny - 1 ? nx : 0;   // boundary neighbour = the point
+    const long long cr = (long long)(y / 2) * cnx;
+    const int can = (on != 0 && !(y & 1)) ? -cnx : 0, cas = (os != 0 && (y & 1)) ? cnx : 0;
+    const double* wxr = g.wx + r0;
+    const double* wyr = g.wy + r0;
+    const double* cntr = cnt ? cnt + r0 : nullptr;
+    for (int x = threadIdx.x; x < nx; x += SP_T) {
+      const int ow = x > 0 ? -1 : 0, oe = x < nx - 1 ? 1 : 0;
+      const int cx = x >> 1;
+      const int caw = (ow != 0 && !(x & 1)) ? -1 : 0, cae = (oe != 0 && (x & 1)) ? 1 : 0;
+      const double wx0 = __ldg(wxr + x), wx1 = __ldg(wxr + x + 1);
+      const double wym = __ldg(wyr + x), wyp = __ldg(wyr + nx + x);
+      const double c = cntr ? cntr[x] : 1.0;
+      auto one = [&](const double* xp_, const double* cp_, const double* b_, const double* d_, double s,
+                     double& bp) -> double {
+        const double* xr = xp_ + r0 + x;
+        const double* cc = cp_ + cr + cx;
+        const double u0 = xr[0] + cc[0];
+        const double m = (1.0 + s) * c;
+        double a = m * u0;
+        a = fma(wx0, u0 - (xr[ow] + cc[caw]), a);
+        a = fma(wx1, u0 - (xr[oe] + cc[cae]), a);
+        a = fma(wym, u0 - (xr[on] + cc[can]), a);
+        a = fma(wyp, u0 - (xr[os] + cc[cas]), a);
+        bp = b_[r0 + x];
+        return u0 + SP_OMEGA * (bp - a) * d_[r0 + x];
+      };
+      double bpa, bpb;
+      const double xna = one(xa, ca, ba, da, sa, bpa);
+      const double xnb = one(xb, cb, bb, db, sb, bpb);
+      oa[r0 + x] = xna;
+      ob[r0 + x] = xnb;
+      if (level0) {
+        dota = fma(xna, bpa, dota);
+        dotb = fma(xnb, bpb, dotb);
+      }
+    }
+  }
+  if (level0) sp_reduce_pair(S, dota, dotb, pa, pb);
+}
+
 // x_c = A_c(s)^{-1} b_c with the precomputed dense inverse of the plane's block (CTA per plane)
 __global__ void __launch_bounds__(SP_T) k_mg_coarse(int nc, const double* __restrict__ minv, int ell,
                                                     const double* bc, double* xc, const IterState* st) {
@@ -1210,10 +1279,16 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
                                                           hlo, hhi));
     } else {                                               // x, x_c, b in; x2 out (+ C)
       static const bool no_pair = getenv("AAC_SP_PAIR") && atoi(getenv("AAC_SP_PAIR")) == 0;
+      static const bool no_row2d = getenv("AAC_SP_ROW2D") && atoi(getenv("AAC_SP_ROW2D")) == 0;
       if (no_pair)
         LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
                k_mg_prolong_post<DIM><<<gp, SP_T, 0, ctx->stream>>>(a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2,
                                                                     a.x2, S, l == 0 ? 1 : 0));
+      else if (DIM == 2 && !no_row2d)                      // row grid: grid-stride over rows
+        LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
+               k_mg_prolong_post_pair2<<<dim3(std::min<unsigned>(gp.x, (unsigned)a.g.ny), ell / 2), SP_T, 0,
+                                         ctx->stream>>>(a.g, a.cnt, a.dinv, c.g, io, bl, a.x, c.x2, a.x2, S,
+                                                        l == 0 ? 1 : 0));
       else
         LAUNCH(ctx, KID_SP_MG, 8.0 * ell * (3.0 * a.g.N + c.g.N) + 8.0 * DIM * a.g.N,
                k_mg_prolong_post_pair<DIM><<<dim3(gp.x, ell / 2), SP_T, 0, ctx->stream>>>(
