@@ -802,6 +802,77 @@ __global__ void __launch_bounds__(SP_T) k_sp_apply(Geo g, SpVec v, SpStepCtx S) 
   sp_reduce(S, dotp, false);
 }
 
+// 2D row-grid variant of k_sp_apply (grid-stride over rows, threads over x): row pointers for the
+// y-neighbours (slab halo rows at the ends), no flat-index arithmetic. Same operations in the same
+// order as apply_Av / mg_apply: bit-identical.
+__global__ void __launch_bounds__(SP_T) k_sp_apply2(Geo g, SpVec v, SpStepCtx S) {
+  if (S.st && S.st->done) return;
+  const int kb = blockIdx.y, ell = S.K.ell, h = ell / 2;
+  const long long N = g.N;
+  const int nx = g.nx, ny = g.ny;
+  const bool stopped = S.blk[kb].stop != 0;
+  const double invg = stopped ? 0.0 : 1.0 / S.blk[kb].gamma;
+  const bool real = kb == 0 || kb == h;
+  const int q0 = real ? (kb == 0 ? 0 : ell - 1) : 2 * kb - 1;
+  const double* u0p = real ? v.P + (long long)q0 * N : v.Zc + (long long)q0 * N;
+  const double* u1p = real ? u0p : v.Zc + (long long)(q0 + 1) * N;
+  const double* hl0 = S.hlo + (long long)q0 * g.S;
+  const double* hh0 = S.hhi + (long long)q0 * g.S;
+  const double* hl1 = S.hlo + (long long)(q0 + 1) * g.S;
+  const double* hh1 = S.hhi + (long long)(q0 + 1) * g.S;
+  const double m = 1.0 + S.K.s[q0];
+  const double lr = S.K.lre[kb], li = S.K.lim[kb];
+  double* sz0 = v.SZ + (long long)q0 * N;
+  double* sz1 = v.SZ + (long long)(q0 + 1) * N;
+  double dotp = 0.0;
+  for (int y = blockIdx.x; y < ny && !stopped; y += gridDim.x) {
+    const long long r0 = (long long)y * nx;
+    // y-neighbour rows: in the slab, a halo row (slab boundary), or the row itself (boundary)
+    const double* n0 = y > 0 ? u0p + r0 - nx : (g.has_lo ? hl0 : u0p + r0);
+    const double* s0 = y < ny - 1 ? u0p + r0 + nx : (g.has_hi ? hh0 : u0p + r0);
+    const double* n1 = y > 0 ? u1p + r0 - nx : (g.has_lo ? hl1 : u1p + r0);
+    const double* s1 = y < ny - 1 ? u1p + r0 + nx : (g.has_hi ? hh1 : u1p + r0);
+    const double* wxr = g.wx + r0;
+    const double* wyr = g.wy + r0;
+    for (int x = threadIdx.x; x < nx; x += SP_T) {
+      const int ow = x > 0 ? -1 : 0, oe = x < nx - 1 ? 1 : 0;
+      const double wx0 = __ldg(wxr + x), wx1 = __ldg(wxr + x + 1);
+      const double wym = __ldg(wyr + x), wyp = __ldg(wyr + nx + x);
+      const double dbd = g.dir ? dirichlet_diag<2>(g, x, y, 0) : 0.0;
+      auto av = [&](const double* u, const double* nr, const double* sr, double& c) {
+        const double* ur = u + r0 + x;
+        c = ur[0];
+        double acc = c;
+        acc = fma(wx0, c - ur[ow], acc);
+        acc = fma(wx1, c - ur[oe], acc);
+        acc = fma(wym, c - nr[x], acc);
+        acc = fma(wyp, c - sr[x], acc);
+        acc = fma(dbd, c, acc);
+        return acc;
+      };
+      if (real) {
+        double c;
+        const double a0 = av(u0p, n0, s0, c);
+        const double a = a0 + (m - 1.0) * c;                 // (A - Lambda) p
+        sz0[r0 + x] = a;
+        dotp = fma(c, a, dotp);
+      } else {
+        double zu, zv;
+        const double azu = av(u0p, n0, s0, zu);
+        const double azv = av(u1p, n1, s1, zv);
+        const double us = zu * invg, vs = zv * invg;
+        const double Au = azu * invg, Av = azv * invg;
+        const double Su = li * us + (Av - lr * vs);
+        const double Sv = (Au - lr * us) - li * vs;
+        sz0[r0 + x] = Su;
+        sz1[r0 + x] = Sv;
+        dotp = fma(Sv, vs, fma(Su, us, dotp));
+      }
+    }
+  }
+  sp_reduce(S, dotp, false);
+}
+
 // K3 (grid: tiles x planes): complex: Vn = SZ - (delta/gamma) Vc - (gamma/gamma_prev) Vp;
 // real: X += alpha P, R -= alpha Q.
 __global__ void __launch_bounds__(SP_T) k_sp_upd1(long long N, int ell, SpVec v, const SpBlk* blk,
@@ -1354,9 +1425,15 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
       }
       AAC_TRY(comm_halo(ctx, planes, qs, ell));
     }
-    LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
-           k_sp_apply<DIM><<<dim3(std::min<unsigned>(gt, std::max(1, 8 * ctx->num_sms / (h + 1))), h + 1), SP_T, 0,
-                              ctx->stream>>>(ctx->geo, vecs(), S));
+    static const bool no_row2d = getenv("AAC_SP_ROW2D") && atoi(getenv("AAC_SP_ROW2D")) == 0;
+    const unsigned gsa = std::min<unsigned>(gt, std::max(1, 8 * ctx->num_sms / (h + 1)));
+    if (DIM == 2 && !no_row2d)
+      LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+             k_sp_apply2<<<dim3(std::min<unsigned>(gsa, (unsigned)ctx->geo.ny), h + 1), SP_T, 0, ctx->stream>>>(
+                 ctx->geo, vecs(), S));
+    else
+      LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+             k_sp_apply<DIM><<<dim3(gsa, h + 1), SP_T, 0, ctx->stream>>>(ctx->geo, vecs(), S));
     AAC_TRY(finish(h + 1, 0));
     LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
            k_sp_upd1<<<dim3(std::min<unsigned>(gt, 16 * ctx->num_sms / ell + 1), ell), SP_T, 0, ctx->stream>>>(
