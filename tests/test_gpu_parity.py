@@ -286,6 +286,37 @@ def test_sp_precond_parity(name, kw, k):
     s.close()
 
 
+_SP_VARIANT = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth
+from oracle import operator as op, saddle
+from paper_2506_03947_b200 import from_problem
+p = synth.make_problem("saddle", shape=(1, 37, 53), ell=4, alpha=1e-2)
+s = from_problem(p, max_krylov=8)
+w = op.weights(p)
+r = np.random.default_rng(6).standard_normal((p.ell,) + p.shape)
+z = s.precond_apply("sp", 3, torch.from_numpy(r.reshape(p.ell, -1)).cuda()).cpu().numpy()
+zo = saddle.sp_apply(w, r, p.ell, p.alpha, 3).reshape(p.ell, -1)
+e = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+assert e <= 1e-12, e
+print("ok", e)
+"""
+
+
+@pytest.mark.parametrize("env", [dict(AAC_SP_ROW2D="0"), dict(AAC_SP_PAIR="0"), dict(AAC_SP_TAIL="0")])
+def test_sp_kernel_variants_parity(env):
+    """The non-default SP kernel organisations (generic flat-index kernels in 2D, one plane per
+    CTA, no fused coarse tail) against the oracle on a ragged grid. A fresh process each: the
+    library reads these switches once per process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SP_VARIANT.format(root=root)], capture_output=True, text=True,
+                       timeout=300, env={**os.environ, **env})
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
+
+
 def test_sp_gmres_parity():
     from oracle import saddle
     p = synth.make_problem("saddle", shape=(1, 64, 48))
