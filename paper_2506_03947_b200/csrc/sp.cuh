@@ -1435,13 +1435,17 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
       LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
              k_sp_apply<DIM><<<dim3(gsa, h + 1), SP_T, 0, ctx->stream>>>(ctx->geo, vecs(), S));
     AAC_TRY(finish(h + 1, 0));
+    // CTAs per plane of the vector updates (grid-stride): 4 x SMs per plane (measured: 237 -> 592
+    // took the saddle solve from 64.8 to 63.3 ms; a full one-element-per-thread grid was slower)
+    static const int upd_env = getenv("AAC_SP_UPD_CAP") ? atoi(getenv("AAC_SP_UPD_CAP")) : 0;
+    const unsigned upd_cap = upd_env > 0 ? (unsigned)upd_env : (unsigned)(4 * ctx->num_sms);
     LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
-           k_sp_upd1<<<dim3(std::min<unsigned>(gt, 16 * ctx->num_sms / ell + 1), ell), SP_T, 0, ctx->stream>>>(
+           k_sp_upd1<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(
                N, ell, vecs(), P->blk, st));
     AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
     AAC_TRY(finish(ell, 1));
     LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
-           k_sp_upd2<<<dim3(std::min<unsigned>(gt, 16 * ctx->num_sms / ell + 1), ell), SP_T, 0, ctx->stream>>>(
+           k_sp_upd2<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(
                N, ell, vecs(), P->blk, st));
     // rotate: v_prev <- v <- v_next, z <- z_next, w_prev <- w <- w_next
     double* t = Vp; Vp = Vc; Vc = Vn; Vn = t;
