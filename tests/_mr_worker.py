@@ -52,6 +52,11 @@ def main():
     out["x"] = xs.cpu().numpy()
     out["iters"] = info["iters"]
     out["relres_true"] = info["relres_true"]
+    # the pipelined host API on the slabs (SPMD): two systems, each bit-identical to aac_gmres
+    bl = local(p.b).cpu().numpy()
+    xsb, infb = s.gmres_host_batch(case["method"], case["k"], [bl, bl], rtol=p.rtol, maxit=60)
+    out["batch_same"] = int(all(np.array_equal(xb, out["x"]) for xb in xsb) and
+                            all(i["iters"] == info["iters"] for i in infb))
     try:                                           # SP needs even slab boundaries
         out["z_sp"] = s.precond_apply("sp", case["k_sp"], local(r)).cpu().numpy()
         xsp, isp = s.gmres("sp", case["k_sp"], local(p.b), rtol=p.rtol, maxit=60)

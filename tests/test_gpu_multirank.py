@@ -95,6 +95,7 @@ def test_multirank_slabs_match_oracle(tmp_path, world, case):
     assert len(its) == 1 and abs(its.pop() - ro.iters) <= 1
     assert _rel(_stitch(parts, "x", p), ro.x) <= 1e-9
     assert all(float(d["relres_true"]) <= 1.5 * p.rtol for d in parts)
+    assert all(int(d["batch_same"]) == 1 for d in parts)        # aac_gmres_host_batch, SPMD
     if not case["sp"]:
         assert all(int(d["sp_error"]) == 1 for d in parts)    # odd slab boundary: clean error
         return
