@@ -17,6 +17,7 @@
 #include "krylov.cuh"
 #include "nc.cuh"
 #include "wave.cuh"
+#include "wave_r.cuh"
 #include "stencil.cuh"
 
 // saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
@@ -414,6 +415,11 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   for (auto e : ctx->ev_cp)
     if (e) cudaEventDestroy(e);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (int a = 0; a < aac_ctx::NAUX; ++a) {
+    if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
+    if (ctx->ev_join[a]) cudaEventDestroy(ctx->ev_join[a]);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto& r : ctx->prof_recs) {
     cudaEventDestroy(r.a);
@@ -649,6 +655,20 @@ static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
   return ac;
 }
 
+// Eager GMRES (profiling, AAC_NO_GRAPH, host transport): after the forward step of an Arnoldi
+// step -- the kernel that forms V_j, its norm and the Givens update, so the step where the
+// solve converges -- read the state back; a converged solve then launches nothing more for
+// that step. (Graph replay instead runs the whole speculative step, whose kernels return at
+// once; profile counters are only collected in eager mode, so they count work that ran.)
+static constexpr int AAC_STEP_DONE = 100;              // internal: the solve finished
+static int publish(aac_ctx* ctx, const void* dsrc, void* hdst, size_t bytes);
+static int poll_after_forward(aac_ctx* ctx) {
+  if (!ctx->eager_poll) return AAC_OK;
+  AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return ctx->h_st->done ? AAC_STEP_DONE : AAC_OK;
+}
+
 // ------------------------------------------------------------------------------------------
 // Dynamic shared memory beyond 48 KB needs an explicit opt-in per kernel.
 // The opt-in is per kernel and process-wide: raise it whenever a launch needs more than any
@@ -688,6 +708,90 @@ static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Per-block wavefront launches (wave_r.cuh): one kernel instantiation per (steps, real/complex,
+// general, first pass), the active blocks of a pass forked over the auxiliary streams and joined
+// back into the library stream (a fork/join subgraph under graph capture).
+template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT>
+static int waver_launch_t(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
+                          cudaStream_t s) {
+  // one warp role per CTA (k_waver) by default; AAC_WAVE_ROLES=2: two roles for 5+ steps
+  // (k_waver2: measured slower at the headline, 9.51 vs 8.63 ms per solve -- barrier stalls and
+  // spills at the 128-register cap)
+  static const bool two_roles = getenv("AAC_WAVE_ROLES") && atoi(getenv("AAC_WAVE_ROLES")) == 2;
+  if constexpr (NS >= 5) {
+    if (two_roles) {
+      auto kern = k_waver2<H, NT, NS, CPLX, GEN, VIRT>;
+      const size_t smem = waver2_smem<NT>(NS, CPLX ? 2 : 1);
+      AAC_TRY(smem_optin(ctx, kern, smem));
+      kern<<<ncta, 2 * NT, smem, s>>>(ctx->geo, P, ctx->d_what, st, sl);
+      return AAC_OK;
+    }
+  }
+  auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT>;
+  const size_t smem = waver_smem<NT>(NS, CPLX ? 2 : 1);
+  AAC_TRY(smem_optin(ctx, kern, smem));
+  kern<<<ncta, NT, smem, s>>>(ctx->geo, P, ctx->d_what, st, sl);
+  return AAC_OK;
+}
+
+template <int H, int NT, int NS>
+static int waver_launch_ns(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
+                           cudaStream_t s, bool gen) {
+  if constexpr (NS >= 1) {
+    if (P.b.ns != NS) return waver_launch_ns<H, NT, NS - 1>(ctx, P, ncta, sl, st, s, gen);
+    const bool c = P.b.np == 2, v = P.b.virt != 0;
+    if (gen) {
+      if (c) return v ? waver_launch_t<H, NT, NS, true, true, true>(ctx, P, ncta, sl, st, s)
+                      : waver_launch_t<H, NT, NS, true, true, false>(ctx, P, ncta, sl, st, s);
+      return v ? waver_launch_t<H, NT, NS, false, true, true>(ctx, P, ncta, sl, st, s)
+               : waver_launch_t<H, NT, NS, false, true, false>(ctx, P, ncta, sl, st, s);
+    }
+    if (c) return v ? waver_launch_t<H, NT, NS, true, false, true>(ctx, P, ncta, sl, st, s)
+                    : waver_launch_t<H, NT, NS, true, false, false>(ctx, P, ncta, sl, st, s);
+    return v ? waver_launch_t<H, NT, NS, false, false, true>(ctx, P, ncta, sl, st, s)
+             : waver_launch_t<H, NT, NS, false, false, false>(ctx, P, ncta, sl, st, s);
+  }
+  return aac_fail(ctx, AAC_EINVAL, "wavefront: bad step count %d", P.b.ns);
+}
+
+static int aux_streams(aac_ctx* ctx) {
+  if (ctx->ev_fork) return AAC_OK;
+  for (int a = 0; a < aac_ctx::NAUX; ++a) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_join[a], cudaEventDisableTiming));
+  }
+  CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  return AAC_OK;
+}
+
+// All blocks of one wavefront pass: block 0 (the heaviest) on the library stream, the others
+// round-robin over the auxiliary streams. Profiled as ONE launch group (its events bracket the
+// fork and the join); every kernel counts in aac_launch_count.
+template <int H, int NT>
+static int waver_group(aac_ctx* ctx, const WSweep& S, int ncta, const WSlab& sl, const IterState* st,
+                       double bytes) {
+  AAC_TRY(aux_streams(ctx));
+  const bool gen = ctx->geo.dir || ctx->nranks > 1;
+  const int naux = std::min(aac_ctx::NAUX, S.nb - 1);
+  LaunchScope ls_(ctx, KID_SWEEP, bytes);
+  if (naux > 0) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+    for (int a = 0; a < naux; ++a) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux[a], ctx->ev_fork, 0));
+  }
+  for (int i = 0; i < S.nb; ++i) {
+    const WROne P{S.b[i], S.nstrip, S.ly[i]};
+    const cudaStream_t s = i == 0 ? ctx->stream : ctx->aux[(i - 1) % naux];
+    AAC_TRY(waver_launch_ns<H, NT, H>(ctx, P, ncta, sl, st, s, gen));
+  }
+  for (int a = 0; a < naux; ++a) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[a], 0));
+  }
+  ctx->launches += S.nb - 1;
+  return ls_.end();
+}
+
+// ------------------------------------------------------------------------------------------
 // Preconditioner: forward DFT (optionally fused with the Arnoldi update), Chebyshev sweeps,
 // last sweep fused with the inverse DFT. gmres_mode: input is the Arnoldi update (W, V, c),
 // output Z_j with j read on the device; otherwise r -> z.
@@ -702,6 +806,10 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   const long long N = g.N, L = (long long)ell * N;
   const double C = 8.0 * ctx->dim * N;
   const Dft D = make_dft(ctx);
+  // register-resident wavefront (wave_r.cuh) by default; AAC_WAVE_OLD=1: the shared-memory
+  // history kernel of wave.cuh
+  static const bool old = getenv("AAC_WAVE_OLD") != nullptr;
+  const size_t smem = WG::SMEM;
   AAC_TRY(smem_optin(ctx, k_wave<H, NT, false>, WG::SMEM));
   AAC_TRY(smem_optin(ctx, k_wave<H, NT, true>, WG::SMEM));
   const int nstrip = (g.nx + WG::TX - 1) / WG::TX;
@@ -771,6 +879,20 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       return ncta;
     };
     int ly0 = ly_env;
+    if (ly0 <= 0 && !old) {
+      // per-block register wavefront: latency-bound at 2-3 CTAs per SM, so more, shorter chunks
+      // pay for their warm-up rows -- about 64 rows, ny split evenly (measured at the headline:
+      // 8.41 ms per solve at 64 rows, 8.46-8.57 at 40-72, 8.63 at 80, 9.21 at 160)
+      const int nch = std::max(1, (g.ny + 63) / 64);
+      ly0 = (g.ny + nch - 1) / nch;
+      const long long slots = 2LL * ctx->num_sms;
+      const long long cols = (long long)g.ny * nstrip * nb;
+      if (cols / ly0 < slots) {                        // small grids: fill the resident slots
+        int ns_max = 1;
+        for (int i = 0; i < nb; ++i) ns_max = std::max(ns_max, S.b[i].ns);
+        ly0 = (int)std::max<long long>(2LL * ns_max, (cols + slots - 1) / slots);
+      }
+    }
     if (ly0 <= 0) {
       const long long slots = (long long)(NT > 128 ? 2 : 3) * ctx->num_sms;
       const long long want = std::max<long long>(1, 2 * slots / std::max(1, nstrip * nb));
@@ -803,10 +925,14 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
                  (int)ctx->lo, (int)ctx->n[1]};
     }
     ctx->next_flops = flops;
-    LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
-           ((g.dir || ctx->nranks > 1)
-                ? k_wave<H, NT, true><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)
-                : k_wave<H, NT, false><<<ncta, NT, WG::SMEM, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
+    if (old) {
+      LAUNCH(ctx, KID_SWEEP, 8.0 * N * passes + C,
+             ((g.dir || ctx->nranks > 1)
+                  ? k_wave<H, NT, true><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)
+                  : k_wave<H, NT, false><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
+    } else {
+      AAC_TRY(waver_group<H, NT>(ctx, S, ncta / nb, sl, st, 8.0 * N * passes + C));
+    }
   }
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
@@ -858,6 +984,8 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
+    const int rc = poll_after_forward(ctx);
+    if (rc != AAC_OK) return rc;
   } else {
     if (ell <= 10)
       LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));
@@ -1066,6 +1194,7 @@ static int arnoldi_impl(aac_ctx* ctx, int host_j) {
 // One Arnoldi step (device j): precondition V_j -> Z_j (forward fused with the update that
 // forms V_j), then w = calA Z_j with the CGS2 projections and Gram column.
 static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
+  int rc = AAC_OK;
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
     AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
@@ -1073,12 +1202,15 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
+    rc = poll_after_forward(ctx);
+    if (rc != AAC_OK) return rc;
     AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
   } else if (method == AAC_EXACT) {
-    AAC_TRY(exact_apply(ctx, nullptr, ctx->d_Z, true, host_j));
+    rc = exact_apply(ctx, nullptr, ctx->d_Z, true, host_j);
   } else {
-    AAC_TRY(nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j));
+    rc = nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j);
   }
+  if (rc != AAC_OK) return rc;                         // error, or the solve finished
   if (ctx->nranks > 1) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
   AAC_TRY(arnoldi_impl(ctx, host_j));
   if (ctx->nranks > 1) {
@@ -1169,14 +1301,19 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
         if (ctx->h_st->done) break;
       }
     } else {
-      AAC_TRY(arnoldi_step(ctx, method, k, it));
+      ctx->eager_poll = true;
+      const int rc = arnoldi_step(ctx, method, k, it);
+      ctx->eager_poll = false;
+      if (rc == AAC_STEP_DONE) break;
+      AAC_TRY(rc);
       AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
       CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       if (ctx->h_st->done) break;
     }
   }
-  // finalise the last column (no-op when already done) and form x = sum y_i Z_i
-  {
+  // finalise the last column and form x = sum y_i Z_i. The finalising forward step does work
+  // only when the loop stopped at maxit; after convergence (h_st->done, final) it is skipped.
+  if (!ctx->h_st->done) {
     // finalise the last Arnoldi column (same kernel; its transform output is unused)
     AAC_TRY(launch_fwd_upd(ctx, 0));
     if (ctx->nranks > 1) {

@@ -104,6 +104,10 @@ struct aac_ctx {
   double* d_bb = nullptr;              // [4][ell][N] b | b | x | x for aac_gmres_host_batch
   cudaStream_t cstream = nullptr;      // copy stream of aac_gmres_host_batch
   cudaEvent_t ev_cp[6] = {};           // in[2] | done[2] | out[2]
+  // fork/join streams of the per-block wavefront launches (wave_r.cuh)
+  static constexpr int NAUX = 4;
+  cudaStream_t aux[NAUX] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {};
   double* d_halo = nullptr;            // [2][ell][S]  lo | hi
   double* d_part = nullptr;            // per-CTA partial sums
   unsigned* d_grp = nullptr;           // two-level ticket counters (zeroed)
@@ -147,6 +151,7 @@ struct aac_ctx {
   long long launches = 0;
   long long sweeps = 0;
   bool prof = false;
+  bool eager_poll = false;             // eager GMRES: read the state back after each forward step
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[KID_COUNT] = {0};

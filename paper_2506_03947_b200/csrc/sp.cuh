@@ -1041,9 +1041,24 @@ static bool dense_inverse(const HostLevel& c, int dim, double s, std::vector<dou
 
 static void shift_of_block(const aac_ctx* ctx, int kb, double* lr, double* li);
 
+static int sp_prepare_impl(aac_ctx* ctx, int k);
+
+// Build the SP plan once per context. The plan is attached to ctx->sp while it is built (the
+// helpers read it from there); any failure frees the partial plan and leaves ctx->sp NULL, so a
+// later call retries from scratch instead of running on a half-built hierarchy.
 static int sp_prepare(aac_ctx* ctx, int k) {
-  (void)k;
   if (ctx->sp) return AAC_OK;
+  const int rc = sp_prepare_impl(ctx, k);
+  if (rc != AAC_OK) {
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaGetLastError();
+    sp_destroy(ctx);
+  }
+  return rc;
+}
+
+static int sp_prepare_impl(aac_ctx* ctx, int k) {
+  (void)k;
   if (ctx->geo.dir)   // the aggregation hierarchy carries no Dirichlet boundary terms
     return aac_fail(ctx, AAC_EINVAL, "AAC_SP needs the Neumann operator (no aac_set_boundary)");
   SpPlan* P = new SpPlan();
