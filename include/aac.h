@@ -221,6 +221,13 @@ int aac_profile_flops(aac_ctx* ctx, int id, double* model_flops);
 int aac_profile_reset(aac_ctx* ctx);
 long long aac_launch_count(const aac_ctx* ctx);
 
+/* Transport of the slab exchanges: 0 = none (one rank), 1 = NCCL (nranks > 1,
+ * or the one-rank communicator AAC_NCCL_SELF=1 creates so that a single GPU runs the whole
+ * multi-rank code path), 2 = the host-staged transport of aac_setup_host_transport.
+ * NCCL waits watch ncclCommGetAsyncError and give up after AAC_NCCL_TIMEOUT_S seconds
+ * (default 300): the communicator is then aborted and calls return AAC_ENCCL.           */
+int aac_comm_kind(const aac_ctx* ctx);
+
 const char* aac_last_error(const aac_ctx* ctx);   /* also valid for ctx == NULL */
 void aac_destroy(aac_ctx* ctx);
 

@@ -211,6 +211,7 @@ extern "C" int aac_setup_host_transport(const aac_grid* g, const double* kx, con
 static int setup_impl(const aac_grid* g, const double* kx, const double* ky, const double* kz,
                       double c, int ell, double alpha, int max_krylov, void* cuda_stream,
                       const void* nccl_id, const aac_host_transport* tr, aac_ctx** out) {
+  NvtxRange nv("aac_setup");
   if (!g || !out) return aac_fail(nullptr, AAC_EINVAL, "aac_setup: NULL grid or out");
   *out = nullptr;
   if (g->dim < 1 || g->dim > 3) return aac_fail(nullptr, AAC_EINVAL, "dim must be 1, 2 or 3");
@@ -299,7 +300,8 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   if (ctx->wave_h != 0 && ctx->wave_h != 4) ctx->wave_h = 8;
   ctx->wave_forced = getenv("AAC_WAVE_H") != nullptr;
   cudaDeviceGetAttribute(&ctx->l2_bytes, cudaDevAttrL2CacheSize, ctx->device);
-  if (ctx->nranks > 1) ctx->use_graphs = false;
+  // host-staged transport: host syncs inside a step, eager launches; NCCL: captured in the graph
+  if (ctx->host_tr) ctx->use_graphs = false;
 
   // device allocations
   auto alloc = [&](double** p, long long n) -> bool {
@@ -508,6 +510,7 @@ static int matvec_impl(aac_ctx* ctx, const double* x, double* y) {
 
 extern "C" int aac_matvec(aac_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y) return aac_fail(ctx, AAC_EINVAL, "aac_matvec: bad pointers");
+  NvtxRange nv("aac_matvec");
   StreamScope ss(ctx);
   return matvec_impl(ctx, x, y);
 }
@@ -651,7 +654,7 @@ static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
   ac.c = ctx->d_giv + 5 * ldh;
   ac.G = ctx->d_G;
   ac.red = ctx->d_red;
-  ac.local_only = ctx->nranks > 1;
+  ac.local_only = ctx->multi();
   return ac;
 }
 
@@ -665,7 +668,7 @@ static int publish(aac_ctx* ctx, const void* dsrc, void* hdst, size_t bytes);
 static int poll_after_forward(aac_ctx* ctx) {
   if (!ctx->eager_poll) return AAC_OK;
   AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  AAC_TRY(comm_sync(ctx));
   return ctx->h_st->done ? AAC_STEP_DONE : AAC_OK;
 }
 
@@ -980,7 +983,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   if (gmres_mode) {
     // algorithmic bytes: W + V_0..V_{j-1} in, V_j and hat w out (j = 0: V_0 in, hat w out)
     AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
-    if (ctx->nranks > 1) {
+    if (ctx->multi()) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
@@ -1110,6 +1113,7 @@ extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* 
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
   if (k < 1 && method != AAC_EXACT) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
   AAC_TRY(check_alpha(ctx));
+  NvtxRange nv("aac_precond_apply");
   StreamScope ss(ctx);
   if (method == AAC_NC1 || method == AAC_NC2) return nc_apply(ctx, method, k, r, z, false);
   if (method == AAC_EXACT) return exact_apply(ctx, r, z, false, 0);
@@ -1198,7 +1202,7 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
     AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
-    if (ctx->nranks > 1) {
+    if (ctx->multi()) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
@@ -1213,7 +1217,7 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   if (rc != AAC_OK) return rc;                         // error, or the solve finished
   if (ctx->nranks > 1) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
   AAC_TRY(arnoldi_impl(ctx, host_j));
-  if (ctx->nranks > 1) {
+  if (ctx->multi()) {
     AAC_TRY(comm_allreduce(ctx, ctx->d_red, 2 * (host_j + 1), ncclSum));
     LAUNCH(ctx, KID_SCALAR, 0, k_scalar_cgs2<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
   }
@@ -1256,6 +1260,7 @@ static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
 
 static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* x, double rtol,
                       int maxit, aac_gmres_info* info) {
+  NvtxRange nv("aac_gmres");
   if (maxit < 1 || maxit > ctx->max_krylov)
     return aac_fail(ctx, AAC_EINVAL, "maxit must be in [1, max_krylov=%d]", ctx->max_krylov);
   if (!(rtol >= 0.0)) return aac_fail(ctx, AAC_EINVAL, "rtol must be >= 0");
@@ -1297,7 +1302,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
       ctx->launches += ge->nodes;
       CUDA_TRY(ctx, cudaEventRecord(ctx->ev_it[it & 1], ctx->stream));
       if (it >= 1) {
-        CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_it[(it - 1) & 1]));
+        AAC_TRY(comm_wait_event(ctx, ctx->ev_it[(it - 1) & 1]));
         if (ctx->h_st->done) break;
       }
     } else {
@@ -1307,7 +1312,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
       if (rc == AAC_STEP_DONE) break;
       AAC_TRY(rc);
       AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
-      CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      AAC_TRY(comm_sync(ctx));
       if (ctx->h_st->done) break;
     }
   }
@@ -1316,7 +1321,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   if (!ctx->h_st->done) {
     // finalise the last Arnoldi column (same kernel; its transform output is unused)
     AAC_TRY(launch_fwd_upd(ctx, 0));
-    if (ctx->nranks > 1) {
+    if (ctx->multi()) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
     }
@@ -1325,7 +1330,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   LAUNCH(ctx, KID_SCALAR, 0,
          k_backsub<<<1, 1, 0, ctx->stream>>>(ctx->d_st, ldh, ctx->d_H, ctx->d_giv + 2 * ldh, ctx->d_giv + 4 * ldh, yy));
   AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  AAC_TRY(comm_sync(ctx));
   const IterState fin = *ctx->h_st;
   const int m = fin.m;
   if (m > 0)
@@ -1343,7 +1348,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
     LAUNCH(ctx, KID_REDUCE, 0, k_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_part, nb, ctx->d_stat));
     AAC_TRY(comm_allreduce(ctx, ctx->d_stat, 1, ncclSum));
     AAC_TRY(publish(ctx, ctx->d_stat, ctx->h_stat, sizeof(double)));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    AAC_TRY(comm_sync(ctx));
     rtrue = sqrt(ctx->h_stat[0]) / fin.beta;
   }
   if (info) {
@@ -1488,5 +1493,10 @@ extern "C" int aac_profile_reset(aac_ctx* ctx) {
   return AAC_OK;
 }
 extern "C" long long aac_launch_count(const aac_ctx* ctx) { return ctx ? ctx->launches : 0; }
+extern "C" int aac_comm_kind(const aac_ctx* ctx) {
+  if (!ctx) return 0;
+  if (ctx->host_tr) return 2;
+  return ctx->nccl_comm ? 1 : 0;
+}
 
 #include "paper_mode.cuh"   // aac_set_boundary / aac_set_bounds / aac_ci (N1)

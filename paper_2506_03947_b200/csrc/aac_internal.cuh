@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/aac.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a profiler is attached
 
 #define AAC_MAX_ELL 16
 #define AAC_MAX_BLK (AAC_MAX_ELL / 2 + 1)
@@ -143,6 +144,8 @@ struct aac_ctx {
   int exact_n = 0;                     // > 0 once prepared
   // NCCL (dlopen'ed), or the host-staged transport
   void* nccl_comm = nullptr;
+  bool nccl_self = false;              // AAC_NCCL_SELF=1: a one-rank NCCL communicator (test switch)
+  cudaEvent_t ev_sync = nullptr;       // NCCL waits: polled with the async-error check + timeout
   bool host_tr = false;
   aac_host_transport htr{};
   double* h_stage = nullptr;           // pinned staging for host-transport exchanges
@@ -160,6 +163,8 @@ struct aac_ctx {
   double prof_flops[KID_COUNT] = {0};  // model fp64 flops (set for ALU-bound kernels)
   double next_flops = 0.0;             // attached to the next launch
   std::string err;
+  // the multi-rank code path runs (local partial sums + all-reduce + scalar kernels)
+  bool multi() const { return nranks > 1 || nccl_self; }
 };
 
 // ------------------------------------------------------------------------------------------
@@ -178,6 +183,13 @@ int aac_fail(aac_ctx* ctx, int code, const char* fmt, ...);
     int r_ = (__VA_ARGS__);  \
     if (r_ < 0) return r_;   \
   } while (0)
+
+// NVTX range over a C-ABI call (setup, matvec, precond_apply, gmres, ci): the phases show up
+// in nsys / ncu --nvtx timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Bracket one launch with profiling events when enabled; count it; check launch errors.
 struct LaunchScope {

@@ -9,6 +9,8 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <time.h>
+#include <unistd.h>
 
 #include "aac_internal.cuh"
 
@@ -23,6 +25,9 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 static NcclApi g_nccl;
@@ -42,6 +47,9 @@ static int nccl_load(aac_ctx* ctx) {
   SYM("ncclGroupStart", GroupStart)
   SYM("ncclGroupEnd", GroupEnd)
   SYM("ncclGetErrorString", GetErrorString)
+  SYM("ncclGetUniqueId", GetUniqueId)
+  SYM("ncclCommGetAsyncError", CommGetAsyncError)
+  SYM("ncclCommAbort", CommAbort)
 #undef SYM
   g_nccl.h = h;
   return AAC_OK;
@@ -55,12 +63,24 @@ static int nccl_load(aac_ctx* ctx) {
                       g_nccl.GetErrorString(r_));                                           \
   } while (0)
 
+// nranks > 1: the caller's unique id (rank 0 created it). nranks == 1 with AAC_NCCL_SELF=1: a
+// one-rank communicator of this process, so a single GPU runs the whole multi-rank code path --
+// local partial sums, NCCL all-reduces captured in the step graph, the scalar kernels -- which
+// is how that path is exercised where only one GPU exists (tests/test_gpu_nccl.py).
 static int comm_init(aac_ctx* ctx, const void* nccl_id) {
-  if (ctx->nranks == 1 || ctx->host_tr) return AAC_OK;
-  if (!nccl_id) return aac_fail(ctx, AAC_EINVAL, "nccl_id required when nranks > 1");
-  AAC_TRY(nccl_load(ctx));
+  if (ctx->host_tr) return AAC_OK;
   ncclUniqueId id;
-  memcpy(&id, nccl_id, sizeof(id));
+  if (ctx->nranks == 1) {
+    const char* e = getenv("AAC_NCCL_SELF");
+    if (!e || atoi(e) != 1) return AAC_OK;
+    AAC_TRY(nccl_load(ctx));
+    NCCL_TRY(ctx, g_nccl.GetUniqueId(&id));
+    ctx->nccl_self = true;
+  } else {
+    if (!nccl_id) return aac_fail(ctx, AAC_EINVAL, "nccl_id required when nranks > 1");
+    AAC_TRY(nccl_load(ctx));
+    memcpy(&id, nccl_id, sizeof(id));
+  }
   ncclComm_t comm;
   NCCL_TRY(ctx, g_nccl.CommInitRank(&comm, ctx->nranks, id, ctx->rank));
   ctx->nccl_comm = (void*)comm;
@@ -70,6 +90,8 @@ static int comm_init(aac_ctx* ctx, const void* nccl_id) {
 static void comm_destroy(aac_ctx* ctx) {
   if (ctx->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)ctx->nccl_comm);
   ctx->nccl_comm = nullptr;
+  if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
+  ctx->ev_sync = nullptr;
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   ctx->h_stage = nullptr;
 }
@@ -97,9 +119,55 @@ static int host_allreduce(aac_ctx* ctx, double* d, int n, int op) {
   return AAC_OK;
 }
 
+// Wait for `ev` while watching the communicator: a peer that died or an NCCL failure
+// (ncclCommGetAsyncError) or no progress within AAC_NCCL_TIMEOUT_S seconds (default 300)
+// aborts the communicator and returns AAC_ENCCL instead of hanging the solve.
+static double comm_now() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+static int comm_wait_event(aac_ctx* ctx, cudaEvent_t ev) {
+  if (!ctx->nccl_comm) {
+    CUDA_TRY(ctx, cudaEventSynchronize(ev));
+    return AAC_OK;
+  }
+  static const double limit = getenv("AAC_NCCL_TIMEOUT_S") ? atof(getenv("AAC_NCCL_TIMEOUT_S")) : 300.0;
+  const double t0 = comm_now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e == cudaSuccess) return AAC_OK;
+    if (e != cudaErrorNotReady) return aac_fail(ctx, AAC_ECUDA, "wait: %s", cudaGetErrorString(e));
+    ncclResult_t ar = ncclSuccess;
+    g_nccl.CommGetAsyncError((ncclComm_t)ctx->nccl_comm, &ar);
+    const bool late = comm_now() - t0 > limit;
+    if ((ar != ncclSuccess && ar != ncclInProgress) || late) {
+      g_nccl.CommAbort((ncclComm_t)ctx->nccl_comm);
+      ctx->nccl_comm = nullptr;
+      return aac_fail(ctx, AAC_ENCCL, late ? "NCCL: no progress within %.0f s (communicator aborted)"
+                                           : "NCCL asynchronous error: %s (communicator aborted)",
+                      late ? limit : 0.0, late ? "" : g_nccl.GetErrorString(ar));
+    }
+    if (spin > 64) usleep(20);
+  }
+}
+
+// cudaStreamSynchronize of the library stream with the same watch (NCCL contexts).
+static int comm_sync(aac_ctx* ctx) {
+  if (!ctx->nccl_comm) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return AAC_OK;
+  }
+  if (!ctx->ev_sync) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_sync, cudaEventDisableTiming));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_sync, ctx->stream));
+  return comm_wait_event(ctx, ctx->ev_sync);
+}
+
 // In-place all-reduce of n doubles on the context stream (no-op on one rank).
 static int comm_allreduce(aac_ctx* ctx, double* d, int n, ncclRedOp_t op) {
-  if (ctx->nranks == 1 || n <= 0) return AAC_OK;
+  if (!ctx->multi() || n <= 0) return AAC_OK;
+  if (!ctx->host_tr && !ctx->nccl_comm) return aac_fail(ctx, AAC_ENCCL, "NCCL communicator aborted");
   if (ctx->host_tr) return host_allreduce(ctx, d, n, op == ncclMax ? 1 : 0);
   NCCL_TRY(ctx, g_nccl.AllReduce(d, d, (size_t)n, ncclFloat64, op, (ncclComm_t)ctx->nccl_comm,
                                  ctx->stream));
@@ -142,21 +210,30 @@ static int comm_halo_ex(aac_ctx* ctx, const Geo& g, const double* const* planes,
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return AAC_OK;
   }
+  if (!ctx->nccl_comm) return aac_fail(ctx, AAC_ENCCL, "NCCL communicator aborted");
   ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
   NCCL_TRY(ctx, g_nccl.GroupStart());
-  for (int i = 0; i < count; ++i) {
+  // the group is always closed: the first failing call is recorded, the rest skipped
+  ncclResult_t bad = ncclSuccess;
+  const char* what = "";
+  auto rec = [&](ncclResult_t r, const char* w) {
+    if (r != ncclSuccess && bad == ncclSuccess) { bad = r; what = w; }
+  };
+  for (int i = 0; i < count && bad == ncclSuccess; ++i) {
     const double* u = planes[i];
     const int q = qs[i];
     if (g.has_lo) {
-      NCCL_TRY(ctx, g_nccl.Send(u, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream));
-      NCCL_TRY(ctx, g_nccl.Recv(hlo + q * S, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream));
+      rec(g_nccl.Send(u, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream), "ncclSend (lower)");
+      rec(g_nccl.Recv(hlo + q * S, S, ncclFloat64, ctx->rank - 1, comm, ctx->stream), "ncclRecv (lower)");
     }
     if (g.has_hi) {
-      NCCL_TRY(ctx, g_nccl.Send(u + g.N - S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream));
-      NCCL_TRY(ctx, g_nccl.Recv(hhi + q * S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream));
+      rec(g_nccl.Send(u + g.N - S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream), "ncclSend (upper)");
+      rec(g_nccl.Recv(hhi + q * S, S, ncclFloat64, ctx->rank + 1, comm, ctx->stream), "ncclRecv (upper)");
     }
   }
-  NCCL_TRY(ctx, g_nccl.GroupEnd());
+  const ncclResult_t ge = g_nccl.GroupEnd();
+  if (bad != ncclSuccess) return aac_fail(ctx, AAC_ENCCL, "halo exchange: %s: %s", what, g_nccl.GetErrorString(bad));
+  if (ge != ncclSuccess) return aac_fail(ctx, AAC_ENCCL, "halo exchange: ncclGroupEnd: %s", g_nccl.GetErrorString(ge));
   return AAC_OK;
 }
 

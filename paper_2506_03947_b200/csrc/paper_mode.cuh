@@ -80,6 +80,7 @@ extern "C" int aac_set_bounds(aac_ctx* ctx, double mu_min, double mu_max) {
 extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* x, double lmin,
                       double lmax, double tol, int maxit, aac_gmres_info* info) {
   if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_ci: bad pointers");
+  NvtxRange nv("aac_ci");
   if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP && method != AAC_EXACT)
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
   if ((method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) && k < 1)

@@ -1413,7 +1413,7 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     }
     return io;
   };
-  const bool multi = ctx->nranks > 1;
+  const bool multi = ctx->multi();
   SpStepCtx S{P->blk, P->part, P->tick, P->K, 0, st, multi ? P->red : nullptr, ctx->d_halo,
               ctx->d_halo + (long long)ell * ctx->geo.S};
   // multi-rank: all-reduce the local sums of the last kernel, then the scalar step

@@ -159,7 +159,10 @@ class Solver:
         b = np.ascontiguousarray(b, dtype=np.float64)
         if b.size != self.ell * self.n_local:
             raise ValueError("b has the wrong size")
-        x = np.empty_like(b) if x is None else x
+        if x is None:
+            x = np.empty_like(b)
+        elif x.dtype != np.float64 or not x.flags.c_contiguous or x.size != self.ell * self.n_local:
+            raise ValueError("x must be a C-contiguous float64 array of ell * n_local values")
         info = aac_gmres_info()
         rc = lib.aac_gmres_host(self.ctx, _method(method), int(k), _dptr(b), _dptr(x), float(rtol),
                                 int(maxit or self.max_krylov), ctypes.byref(info))
@@ -237,6 +240,10 @@ class Solver:
 
     def launch_count(self):
         return lib.aac_launch_count(self.ctx)
+
+    def comm_kind(self):
+        """0: one rank, no communicator; 1: NCCL; 2: host-staged transport (aac_comm_kind)."""
+        return {0: "none", 1: "nccl", 2: "host"}[lib.aac_comm_kind(self.ctx)]
 
     def close(self):
         if getattr(self, "ctx", None):

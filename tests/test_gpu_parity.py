@@ -104,11 +104,17 @@ def test_precond_c_zero_equals_exact_P_alpha():
 
 GM = [
     ("1d", {}, None, None),
+    # BASELINE.json configs[1]: 256^2, alpha in {1e-2, 1e-4} x k in {5, 20} -- all four pairs
     ("2d256", dict(n=256), "nc1", 5),
+    ("2d256", dict(n=256), "nc1", 20),
+    ("2d256", dict(n=256, alpha=1e-4), "nc1", 5),
     ("2d256", dict(n=256, alpha=1e-4), "nc1", 20),
     ("headline", dict(n=256), "nc2", 8),
     ("headline", dict(shape=(1, 100, 73)), "nc1", 8),
     ("3d", dict(shape=(16, 16, 16)), "nc1", 10),
+    # 64^3, ell = 12: large enough that k_arnoldi streams every basis vector of a tile in one
+    # CTA (ng = 1), as at the full 256^3 size of configs[4] (~25 s of oracle)
+    ("3d", dict(n=64), "nc1", 10),
 ]
 
 
@@ -260,6 +266,23 @@ def test_headline_full_size_gmres_vs_stored_oracle():
     ref = np.array(g["sample_x"])
     assert np.linalg.norm(xs[idx] - ref) <= 1e-9 * np.linalg.norm(ref)
     assert np.linalg.norm(xs) == pytest.approx(g["x_norm"], rel=1e-9)
+    s.close()
+
+
+def test_headline_full_size_gmres_full_vector_vs_oracle():
+    """The full headline solve (N = 1024^2, ell = 10, NC2 k = 8) element by element against an
+    oracle FGMRES run in this test (~95 s of CPU): counts +-1, the whole x to 1e-9, and the
+    forced-equal-m iterate (rtol = 0, maxit = the oracle's count) far below that."""
+    p = synth.make_problem("headline")
+    ro = _oracle_gmres(p, "nc2", p.k, 40)
+    s = _solver(p, max_krylov=40)
+    x, info = s.gmres("nc2", p.k, _dev(p.b, p.ell), rtol=p.rtol, maxit=40)
+    assert ro.converged and info["converged"] == 1
+    assert abs(info["iters"] - ro.iters) <= 1
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    xm, im = s.gmres("nc2", p.k, _dev(p.b, p.ell), rtol=0.0, maxit=ro.iters)
+    assert im["iters"] == ro.iters
+    assert _rel(xm.cpu().numpy(), ro.x) <= 1e-11
     s.close()
 
 

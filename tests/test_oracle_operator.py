@@ -60,6 +60,36 @@ def test_neumann_constant_mode_and_spd(shape):
     assert ev.max() <= op.gershgorin_max(w) * (1 + 1e-14)
 
 
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gershgorin_equals_dense_row_sums(shape):
+    """gershgorin_max is THE Gershgorin bound max_i (a_ii + sum_{j != i} |a_ij|) of the
+    brute-force per-cell assembly above (reading R5), not merely some upper bound."""
+    w = _w(shape)
+    nz, ny, nx = shape
+    idx = np.arange(w.N).reshape(shape)
+    Ab = np.eye(w.N)
+    for (k, j, i), P in np.ndenumerate(idx):
+        for (dk, dj, di, wf) in ((0, 0, 1, w.wx[k, j, i] if i < nx - 1 else 0),
+                                 (0, 0, -1, w.wx[k, j, i - 1] if i > 0 else 0),
+                                 (0, 1, 0, w.wy[k, j, i] if j < ny - 1 else 0),
+                                 (0, -1, 0, w.wy[k, j - 1, i] if j > 0 else 0),
+                                 (1, 0, 0, w.wz[k, j, i] if k < nz - 1 else 0),
+                                 (-1, 0, 0, w.wz[k - 1, j, i] if k > 0 else 0)):
+            if wf:
+                Ab[P, P] += wf
+                Ab[P, idx[k + dk, j + dj, i + di]] -= wf
+    dense = max(Ab[i, i] + np.sum(np.abs(Ab[i])) - abs(Ab[i, i]) for i in range(w.N))
+    assert op.gershgorin_max(w) == pytest.approx(dense, rel=1e-15)
+
+
+@pytest.mark.parametrize("name,printed", [("1d", 36.61), ("2d256", 50.81), ("headline", 32.14)])
+def test_gershgorin_survey_values(name, printed):
+    """mu_max of the seeded BASELINE configs as printed by the survey's independent numpy
+    prototype ("Est. mu_max", seed 0), to the printed 4 digits."""
+    w = op.weights(synth.make_problem(name))
+    assert round(op.gershgorin_max(w), 2) == printed
+
+
 @pytest.mark.parametrize("shape", [(1, 1, 16), (1, 8, 12), (4, 6, 5)])
 def test_kappa_one_closed_form_dct(shape):
     """kappa = 1: A cos-modes prod_a cos(pi m_a (i_a + 1/2)/n_a) have eigenvalue
