@@ -771,7 +771,7 @@ static int aux_streams(aac_ctx* ctx) {
 // round-robin over the auxiliary streams. Profiled as ONE launch group (its events bracket the
 // fork and the join); every kernel counts in aac_launch_count.
 template <int H, int NT>
-static int waver_group(aac_ctx* ctx, const WSweep& S, int ncta, const WSlab& sl, const IterState* st,
+static int waver_group(aac_ctx* ctx, const WSweep& S, int nchunk, const WSlab& sl, const IterState* st,
                        double bytes) {
   AAC_TRY(aux_streams(ctx));
   const bool gen = ctx->geo.dir || ctx->nranks > 1;
@@ -782,9 +782,13 @@ static int waver_group(aac_ctx* ctx, const WSweep& S, int ncta, const WSlab& sl,
     for (int a = 0; a < naux; ++a) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux[a], ctx->ev_fork, 0));
   }
   for (int i = 0; i < S.nb; ++i) {
-    const WROne P{S.b[i], S.nstrip, S.ly[i]};
+    // strips of NT - 2 ns columns: the x-halo of a block is its step count (one-role kernel)
+    static const bool two_roles = getenv("AAC_WAVE_ROLES") && atoi(getenv("AAC_WAVE_ROLES")) == 2;
+    const int halo = (two_roles && S.b[i].ns >= 5) ? H : S.b[i].ns;
+    const int nstrip = (ctx->geo.nx + (NT - 2 * halo) - 1) / (NT - 2 * halo);
     const cudaStream_t s = i == 0 ? ctx->stream : ctx->aux[(i - 1) % naux];
-    AAC_TRY(waver_launch_ns<H, NT, H>(ctx, P, ncta, sl, st, s, gen));
+    const WROne P{S.b[i], two_roles && S.b[i].ns >= 5 ? S.nstrip : nstrip, S.ly[i]};
+    AAC_TRY(waver_launch_ns<H, NT, H>(ctx, P, P.nstrip * nchunk, sl, st, s, gen));
   }
   for (int a = 0; a < naux; ++a) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
@@ -934,7 +938,7 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
                   ? k_wave<H, NT, true><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)
                   : k_wave<H, NT, false><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
     } else {
-      AAC_TRY(waver_group<H, NT>(ctx, S, ncta / nb, sl, st, 8.0 * N * passes + C));
+      AAC_TRY(waver_group<H, NT>(ctx, S, (g.ny + S.ly[0] - 1) / S.ly[0], sl, st, 8.0 * N * passes + C));
     }
   }
   NcFinal F{};

@@ -132,7 +132,9 @@ __device__ __forceinline__ void wr_level(double c0, double c1, double up0, doubl
 //                  ring never moves (the step loop is unrolled by 3: slot indices are static)
 //   R*[i]:         operands of the row level i works on (row tau - i); index 0 = the row that
 //                  entered at this step. These rows move one level down per step (register
-//                  moves).
+//                  moves). A 9-slot row ring with the step loop unrolled by 9 needs no moves but
+//                  measured slower (8.58 vs 8.36 ms per headline solve: a 58 KB loop body and
+//                  uniform-register spills).
 template <int NS, int NP>
 struct WRState {
   double L[NS + 1][3][NP];
@@ -284,12 +286,14 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   extern __shared__ __align__(16) double wsm[];
   const WBlk& B = P.b;
   const int t = threadIdx.x;
-  constexpr int TX = NT - 2 * H;
+  // x-halo of NS columns per side: a wrong edge value reaches one column further per level
+  constexpr int HX = NS;
+  constexpr int TX = NT - 2 * HX;
   const int cta = (int)blockIdx.x;
   const int strip = cta % P.nstrip, chunk = cta / P.nstrip;
-  const int x = strip * TX - H + t;
+  const int x = strip * TX - HX + t;
   const bool colin = x >= 0 && x < g.nx;
-  const bool colout = t >= H && t < NT - H && x < g.nx;
+  const bool colout = t >= HX && t < NT - HX && x < g.nx;
   const int y0 = chunk * P.ly;
   const int y1 = min(y0 + P.ly, g.ny);
   // zero pads of the exchange rows (never written)
