@@ -516,9 +516,9 @@ def run_paper(args):
     rl = None
     if dom[1].get("model_flops", 0) > 0:
         ach = dom[1]["model_flops"] / (dom[1]["ms"] / 1e3) / 1e12
-        # exact P_alpha (N3): the shifted-solve class is the DST as batched cuBLAS DGEMMs (library
-        # code, fp64 tensor cores) + k_exact_scale; NC: the wavefront k_wave
-        kname = ("shifted_solves: DST by cuBLAS DGEMM + k_exact_scale" if meth == "exact" and dom[0] == "cheb_sweep"
+        # exact P_alpha (N3): the shifted-solve class is the DST as batched fp64 tensor-core GEMMs
+        # (k_dst_gemm, DMMA) + k_exact_scale; NC: the wavefront k_waver
+        kname = ("shifted_solves: DST by k_dst_gemm (DMMA) + k_exact_scale" if meth == "exact" and dom[0] == "cheb_sweep"
                  else dom[0])
         rl = {"bound": "alu", "kernel": kname, "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
               "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,

@@ -1295,7 +1295,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
     for (int j = 0; j < ctx->ell; ++j) alloc_sum += al[j];
   }
   GraphEntry* ge = nullptr;
-  const bool graphs = ctx->use_graphs && !ctx->prof && method != AAC_EXACT;   // (cuBLAS: eager)
+  const bool graphs = ctx->use_graphs && !ctx->prof;
   if (graphs) AAC_TRY(get_graph(ctx, method, k, &ge));
   // Arnoldi steps. Graph path: replay one captured step per iteration and poll the state of
   // the PREVIOUS step (speculative: a step launched after convergence returns at once).

@@ -1,29 +1,10 @@
-// exact_host.cuh -- host side of AAC_EXACT: cuBLAS (dlopen'ed), the
-// DST-I factorisation of the paper's operator, and the exact P_alpha^{-1} apply. Textually
+// exact_host.cuh -- host side of AAC_EXACT: the DST-I factorisation of the
+// paper's operator and the exact P_alpha^{-1} apply (fp64 tensor-core GEMMs of exact.cuh). Textually
 // included by aac.cu (one translation unit), after the NC helpers it uses.
 #pragma once
 
 // ------------------------------------------------------------------------------------------
 // Exact P_alpha for the paper's operator (exact.cuh).
-static CublasApi g_cublas;
-
-static int cublas_load(aac_ctx* ctx) {
-  if (g_cublas.h) return AAC_OK;
-  void* h = nullptr;
-  for (const char* nm : {"libcublas.so.12", "libcublas.so"})
-    if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
-  if (!h) return aac_fail(ctx, AAC_ECUDA, "dlopen libcublas failed: %s", dlerror());
-  *(void**)(&g_cublas.Create) = dlsym(h, "cublasCreate_v2");
-  *(void**)(&g_cublas.Destroy) = dlsym(h, "cublasDestroy_v2");
-  *(void**)(&g_cublas.SetStream) = dlsym(h, "cublasSetStream_v2");
-  *(void**)(&g_cublas.DgemmStridedBatched) = dlsym(h, "cublasDgemmStridedBatched");
-  if (!g_cublas.Create || !g_cublas.SetStream || !g_cublas.DgemmStridedBatched)
-    return aac_fail(ctx, AAC_ECUDA, "cuBLAS symbols missing");
-  if (g_cublas.Create(&g_cublas.handle) != 0) return aac_fail(ctx, AAC_ECUDA, "cublasCreate failed");
-  g_cublas.h = h;
-  return AAC_OK;
-}
-
 static int exact_prepare(aac_ctx* ctx) {
   if (ctx->exact_n > 0) return AAC_OK;
   const Geo& g = ctx->geo;
@@ -45,7 +26,6 @@ static int exact_prepare(aac_ctx* ctx) {
   if (!ok)
     return aac_fail(ctx, AAC_EINVAL,
                     "AAC_EXACT needs a constant face weight w on every interior and Dirichlet boundary face");
-  AAC_TRY(cublas_load(ctx));
   std::vector<double> S((size_t)n * n), lam(n);
   const double sc = sqrt(2.0 / (n + 1));
   for (int i = 0; i < n; ++i) {
@@ -67,17 +47,24 @@ static int exact_prepare(aac_ctx* ctx) {
   return AAC_OK;
 }
 
-// C_q = op(A) op(B) for the ell planes (column-major views of the row-major planes; S = S^T)
-static int gemm_planes(aac_ctx* ctx, const double* A, long long sa, const double* B, long long sb, double* C) {
+// C_q = A_q B_q for the ell planes (row-major n x n; S = S^T, stride 0 = the shared S)
+static int gemm_planes(aac_ctx* ctx, const double* A, long long sa, const double* B, long long sb, double* C,
+                       const IterState* st) {
   const int n = ctx->exact_n;
-  const double one = 1.0, zero = 0.0;
-  g_cublas.SetStream(g_cublas.handle, ctx->stream);
-  LaunchScope ls(ctx, KID_SWEEP, 8.0 * ctx->ell * 3.0 * n * n);
-  ctx->prof_flops[KID_SWEEP] += 2.0 * ctx->ell * (double)n * n * n;
-  if (g_cublas.DgemmStridedBatched(g_cublas.handle, 0, 0, n, n, n, &one, A, n, sa, B, n, sb, &zero, C, n,
-                                   (long long)n * n, ctx->ell) != 0)
-    return aac_fail(ctx, AAC_ECUDA, "cublasDgemmStridedBatched failed");
-  return ls.end();
+  const unsigned mt = (unsigned)((n + DG_T - 1) / DG_T);
+  ctx->next_flops = 2.0 * ctx->ell * (double)n * n * n;
+  // CTA tile 64 x 32 by default: more, smaller tiles fill the SMs more evenly than 64 x 64
+  // (n = 500, ell = 10: 1280 CTAs over 3-4 resident per SM instead of 640)
+  static const int tn = getenv("AAC_DST_TN") ? atoi(getenv("AAC_DST_TN")) : 32;
+  if (tn == 64)
+    LAUNCH(ctx, KID_SWEEP, 8.0 * ctx->ell * 3.0 * n * n,
+           k_dst_gemm<64><<<dim3((n + 63) / 64, mt, ctx->ell), 128, 0, ctx->stream>>>(n, A, sa, B, sb, C,
+                                                                                       (long long)n * n, st));
+  else
+    LAUNCH(ctx, KID_SWEEP, 8.0 * ctx->ell * 3.0 * n * n,
+           k_dst_gemm<32><<<dim3((n + 31) / 32, mt, ctx->ell), 128, 0, ctx->stream>>>(n, A, sa, B, sb, C,
+                                                                                       (long long)n * n, st));
+  return AAC_OK;
 }
 
 static int exact_apply(aac_ctx* ctx, const double* r, double* zbase, bool gmres_mode, int host_j) {
@@ -98,13 +85,13 @@ static int exact_apply(aac_ctx* ctx, const double* r, double* zbase, bool gmres_
   }
   double* X = ctx->d_X;
   // DST both sides: T = S W, X = T S; divide by mu - Lambda_k; back: T = S X, X = T S
-  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, ctx->d_what, NN, ctx->d_T));
-  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
+  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, ctx->d_what, NN, ctx->d_T, st));
+  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X, st));
   ExactShifts Sh{};
   for (int kb = 0; kb <= h; ++kb) shift_of_block(ctx, kb, &Sh.lr[kb], &Sh.li[kb]);
-  LAUNCH(ctx, KID_SWEEP, 2 * V, k_exact_scale<<<grid1d(NN, 256), 256, 0, ctx->stream>>>(n, ell, ctx->d_lam1, X, Sh));
-  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, X, NN, ctx->d_T));
-  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X));
+  LAUNCH(ctx, KID_SWEEP, 2 * V, k_exact_scale<<<grid1d(NN, 256), 256, 0, ctx->stream>>>(n, ell, ctx->d_lam1, X, Sh, st));
+  AAC_TRY(gemm_planes(ctx, ctx->d_S, 0, X, NN, ctx->d_T, st));
+  AAC_TRY(gemm_planes(ctx, ctx->d_T, NN, ctx->d_S, 0, X, st));
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
     F.src[kb] = X + (long long)plane_of_block(ell, kb) * N;

@@ -124,6 +124,55 @@ def test_exact_precond_parity(nx, ell, alpha):
     s.close()
 
 
+def _exact_apply_longdouble(nx, ell, alpha, w, r):
+    """P_alpha^{-1} r for the paper's operator in np.longdouble (x87 80-bit): Gamma-scaled DFT
+    across the blocks (pairing of reading R6), each block solved exactly by the
+    DST-I diagonalisation A = S diag(mu) S (Appendix A), inverse DFT. The
+    reading-R18 diagnostic: an independent evaluation with ~3 more decimal digits."""
+    ld = np.longdouble
+    n = nx
+    i = np.arange(1, n + 1, dtype=ld)
+    S = np.sqrt(ld(2) / ld(n + 1)) * np.sin(np.pi * np.outer(i, i) / ld(n + 1))
+    lam = ld(4) * np.sin(np.pi * i / (ld(2) * ld(n + 1))) ** 2
+    mu = ld(1) + ld(w) * (lam[:, None] + lam[None, :])
+    gam = np.array([ld(alpha) ** (ld(j) / ld(ell)) for j in range(ell)])
+    root = ld(alpha) ** (ld(1) / ld(ell))
+    rr = r.reshape(ell, n, n).astype(ld)
+    jj = np.arange(ell)
+    F = np.exp(np.clongdouble(-2j) * np.pi * np.outer(jj, jj).astype(ld) / ld(ell)) / np.sqrt(ld(ell))
+    what = np.einsum("kj,jyx->kyx", F, gam[:, None, None] * rr)
+    y = np.empty_like(what)
+    for k in range(ell):
+        Lk = root * np.exp(np.clongdouble(-2j) * np.pi * ld(k) / ld(ell))
+        y[k] = S @ ((S @ what[k] @ S) / (mu - Lk)) @ S
+    z = np.einsum("jk,kyx->jyx", np.conj(F).T, y) / gam[:, None, None]
+    return z.real.astype(ld)
+
+
+@pytest.mark.parametrize("nx,ell,alpha", [(37, 6, 1e-4), (50, 10, 0.01)])
+def test_exact_precond_long_double_diagnostic(nx, ell, alpha):
+    """Reading R18: the exact apply's error is rounding amplified by kappa(Gamma_alpha); against a
+    long-double evaluation both the GPU (fp64 tensor-core DST GEMMs) and the oracle (sparse LU)
+    sit at that rounding level, the GPU no farther from it than the oracle (up to 4x)."""
+    from oracle import circulant as circ
+    p = synth.make_paper_problem(nx, ell, alpha)
+    s = _solver(p)
+    w = paper.weights(nx, ell)
+    r = np.random.default_rng(4).standard_normal((ell, 1, nx, nx))
+    z = s.precond_apply("exact", 1, _dev(r, ell)).cpu().numpy().astype(np.longdouble)
+    zo = circ.exact_apply(w, r, ell, alpha).astype(np.longdouble)
+    zl = _exact_apply_longdouble(nx, ell, alpha, float(w.wx[0, 0, 0]), r)
+    nrm = np.sqrt(np.sum(zl * zl))
+    e_gpu = float(np.sqrt(np.sum((z.reshape(zl.shape) - zl) ** 2)) / nrm)
+    e_orc = float(np.sqrt(np.sum((zo.reshape(zl.shape) - zl) ** 2)) / nrm)
+    kg = circ.gamma_condition(ell, alpha)
+    print(f"kappa(Gamma) {kg:.3g}: GPU {e_gpu:.3e}, oracle {e_orc:.3e} from the long-double apply")
+    assert e_orc <= 1e-13 * max(1.0, kg)
+    assert e_gpu <= 1e-13 * max(1.0, kg)
+    assert e_gpu <= 4.0 * max(e_orc, 1e-15)
+    s.close()
+
+
 def test_exact_rejects_other_operators():
     from paper_2506_03947_b200 import AacError
     p = synth.make_problem("headline", shape=(1, 16, 16))          # Neumann, variable kappa
