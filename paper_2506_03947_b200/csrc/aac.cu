@@ -302,6 +302,9 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   cudaDeviceGetAttribute(&ctx->l2_bytes, cudaDevAttrL2CacheSize, ctx->device);
   // host-staged transport: host syncs inside a step, eager launches; NCCL: captured in the graph
   if (ctx->host_tr) ctx->use_graphs = false;
+  // one reduction per Arnoldi step on several ranks (it saves an all-reduce; on one GPU the
+  // fused norm costs nothing and the lagged test would cost an extra apply); AAC_GMRES_1R=0/1
+  ctx->one_reduce = getenv("AAC_GMRES_1R") ? atoi(getenv("AAC_GMRES_1R")) != 0 : ctx->multi();
 
   // device allocations
   auto alloc = [&](double** p, long long n) -> bool {
@@ -655,6 +658,7 @@ static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
   ac.G = ctx->d_G;
   ac.red = ctx->d_red;
   ac.local_only = ctx->multi();
+  ac.one_reduce = ctx->one_reduce ? 1 : 0;
   return ac;
 }
 
@@ -691,9 +695,9 @@ static int smem_optin(aac_ctx* ctx, K kernel, size_t bytes) {
 }
 
 template <int ELLC, bool TMA>
-static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
+static int launch_fwd_upd_t(aac_ctx* ctx, double bytes, bool norm) {
   const long long N = ctx->geo.N, L = (long long)ctx->ell * N;
-  FwdUpd U{ctx->d_W, ctx->d_V, L, ctx->d_part, arnoldi_ctx(ctx), ctx->d_grp};
+  FwdUpd U{ctx->d_W, ctx->d_V, L, ctx->d_part, arnoldi_ctx(ctx), ctx->d_grp, norm ? 1 : 0};
   const Dft D = make_dft(ctx);
   const size_t smem = TMA ? (size_t)FS * ELLC * FT * sizeof(double) : 0;
   AAC_TRY(smem_optin(ctx, k_fwd_upd<ELLC, TMA>, smem));
@@ -702,12 +706,26 @@ static int launch_fwd_upd_t(aac_ctx* ctx, double bytes) {
   return AAC_OK;
 }
 
-static int launch_fwd_upd(aac_ctx* ctx, double bytes) {
+// Forward step of an Arnoldi step: the update forming V_j + its transform; `norm`: also reduce
+// ||V_j||^2 and run the norm step (always, except in one-reduce mode inside the loop).
+static int launch_fwd_upd(aac_ctx* ctx, double bytes, bool norm) {
   const bool tma = (ctx->geo.N % 2) == 0;         // 16-byte aligned plane tiles
   // plane capacity = ell rounded up to 10 / 12 / 16: the shared-memory ring scales with it
-  if (ctx->ell <= 10) return tma ? launch_fwd_upd_t<10, true>(ctx, bytes) : launch_fwd_upd_t<10, false>(ctx, bytes);
-  if (ctx->ell <= 12) return tma ? launch_fwd_upd_t<12, true>(ctx, bytes) : launch_fwd_upd_t<12, false>(ctx, bytes);
-  return tma ? launch_fwd_upd_t<16, true>(ctx, bytes) : launch_fwd_upd_t<16, false>(ctx, bytes);
+  if (ctx->ell <= 10) return tma ? launch_fwd_upd_t<10, true>(ctx, bytes, norm) : launch_fwd_upd_t<10, false>(ctx, bytes, norm);
+  if (ctx->ell <= 12) return tma ? launch_fwd_upd_t<12, true>(ctx, bytes, norm) : launch_fwd_upd_t<12, false>(ctx, bytes, norm);
+  return tma ? launch_fwd_upd_t<16, true>(ctx, bytes, norm) : launch_fwd_upd_t<16, false>(ctx, bytes, norm);
+}
+
+// The forward step inside the Arnoldi loop: with the norm step (+ its all-reduce on several
+// ranks and the eager poll), or without it in one-reduce mode.
+static int forward_step(aac_ctx* ctx, double bytes) {
+  AAC_TRY(launch_fwd_upd(ctx, bytes, !ctx->one_reduce));
+  if (ctx->one_reduce) return AAC_OK;
+  if (ctx->multi()) {
+    AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
+    LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+  }
+  return poll_after_forward(ctx);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -986,12 +1004,7 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   const IterState* st = gmres_mode ? ctx->d_st : nullptr;
   if (gmres_mode) {
     // algorithmic bytes: W + V_0..V_{j-1} in, V_j and hat w out (j = 0: V_0 in, hat w out)
-    AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
-    if (ctx->multi()) {
-      AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
-      LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
-    }
-    const int rc = poll_after_forward(ctx);
+    const int rc = forward_step(ctx, (host_j == 0 ? 2 : host_j + 3) * V);
     if (rc != AAC_OK) return rc;
   } else {
     if (ell <= 10)
@@ -1205,12 +1218,7 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   int rc = AAC_OK;
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
-    AAC_TRY(launch_fwd_upd(ctx, (host_j + 3) * V));
-    if (ctx->multi()) {
-      AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
-      LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
-    }
-    rc = poll_after_forward(ctx);
+    rc = forward_step(ctx, (host_j + 3) * V);
     if (rc != AAC_OK) return rc;
     AAC_TRY(sp_solve(ctx, k, ctx->d_Z, (long long)ctx->ell * ctx->geo.N, ctx->d_st));
   } else if (method == AAC_EXACT) {
@@ -1324,7 +1332,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   // only when the loop stopped at maxit; after convergence (h_st->done, final) it is skipped.
   if (!ctx->h_st->done) {
     // finalise the last Arnoldi column (same kernel; its transform output is unused)
-    AAC_TRY(launch_fwd_upd(ctx, 0));
+    AAC_TRY(launch_fwd_upd(ctx, 0, true));
     if (ctx->multi()) {
       AAC_TRY(comm_allreduce(ctx, ctx->d_red, 1, ncclSum));
       LAUNCH(ctx, KID_SCALAR, 0, k_scalar_norm<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));

@@ -155,6 +155,7 @@ struct aac_ctx {
   long long sweeps = 0;
   bool prof = false;
   bool eager_poll = false;             // eager GMRES: read the state back after each forward step
+  bool one_reduce = false;             // lagged normalisation: one reduction per Arnoldi step
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[KID_COUNT] = {0};

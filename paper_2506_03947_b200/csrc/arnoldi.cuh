@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
     st->tick = 0;
     if (P.ac.local_only) {
       for (int k = 0; k < nv2; ++k) P.ac.red[k] = tot[k];
+    } else if (P.ac.one_reduce) {
+      arnoldi_lagged_step(P.ac, j, tot, tot + nv);
     } else {
       arnoldi_cgs2_step(P.ac, j, tot, tot + nv);
     }

@@ -75,8 +75,7 @@ static int exact_apply(aac_ctx* ctx, const double* r, double* zbase, bool gmres_
   const Dft D = make_dft(ctx);
   const IterState* st = gmres_mode ? ctx->d_st : nullptr;
   if (gmres_mode) {
-    AAC_TRY(launch_fwd_upd(ctx, (host_j == 0 ? 2 : host_j + 3) * V));
-    const int rc = poll_after_forward(ctx);
+    const int rc = forward_step(ctx, (host_j == 0 ? 2 : host_j + 3) * V);
     if (rc != AAC_OK) return rc;
   } else if (ell <= 10) {
     LAUNCH(ctx, KID_FWD, 2 * V, (k_forward<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, r, ctx->d_what)));

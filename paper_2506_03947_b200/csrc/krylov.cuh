@@ -57,6 +57,8 @@ struct ArnoldiCtx {
   double* G;        // Gram matrix (ldh x ldh)
   double* red;      // multi-rank: locally reduced raw sums before the all-reduce
   int local_only;   // 1 when nranks > 1
+  int one_reduce;   // 1: lagged normalisation -- ||V_j||^2 is taken from the Gram column of the
+                    // projection pass (one reduction / all-reduce per Arnoldi step), see below
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -139,6 +141,19 @@ __device__ void arnoldi_cgs2_step(const ArnoldiCtx& ac, int j, const double* s, 
   ac.st->j = j + 1;
 }
 
+// One-reduce Arnoldi step (not in the paper, GMRES is the north star's). The
+// projection pass already measures the Gram column <V_i, V_j>, i <= j, whose last entry is
+// ||V_j||^2 -- so the norm of the vector formed by the previous update need not be reduced on
+// its own: its normalisation (beta or H[j, j-1], the Givens rotation of column j-1 and the
+// convergence test) is lagged into the same reduction as column j's CGS2 coefficients. One
+// all-reduce per step instead of two on several ranks; the price is that convergence of column
+// j-1 is seen one preconditioner apply and calA apply later. In exact arithmetic identical to
+// the two-reduction form (and to the oracle's literal CGS2).
+__device__ void arnoldi_lagged_step(const ArnoldiCtx& ac, int j, const double* s, const double* gg) {
+  arnoldi_norm_step(ac, j, gg[j]);
+  arnoldi_cgs2_step(ac, j, s, gg);
+}
+
 // Multi-rank scalar kernels (after the NCCL all-reduce of the local sums).
 __global__ void k_scalar_norm(ArnoldiCtx ac) {
   if (ac.st->done) return;
@@ -147,7 +162,8 @@ __global__ void k_scalar_norm(ArnoldiCtx ac) {
 __global__ void k_scalar_cgs2(ArnoldiCtx ac) {
   if (ac.st->done) return;
   const int j = ac.st->j;
-  arnoldi_cgs2_step(ac, j, ac.red, ac.red + (j + 1));
+  if (ac.one_reduce) arnoldi_lagged_step(ac, j, ac.red, ac.red + (j + 1));
+  else arnoldi_cgs2_step(ac, j, ac.red, ac.red + (j + 1));
 }
 
 // y = R^{-1} g for the m x m upper-triangular rotated Hessenberg; y_i *= sigma_i so that

@@ -49,6 +49,8 @@ struct FwdUpd {
   double* part;              // per-CTA partials of ||u||^2
   ArnoldiCtx ac;             // st, sigma, c (CGS2 coefficients of column j-1), Givens state
   unsigned* grp;             // per-32-CTA ticket counters (zero between launches)
+  int norm;                  // 1: reduce ||u||^2 and run the norm step here; 0: one-reduce mode
+                             // (the projection pass measures it, krylov.cuh arnoldi_lagged_step)
 };
 
 // gamma-scale + real -> packed half-complex DFT of the ell values w[] of one point.
@@ -204,6 +206,7 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   }
   // ||u||^2: CTA partial, then the last CTA reduces in a fixed order and finalises Arnoldi
   // column j-1 (or beta when j == 0).
+  if (!U.norm) return;
   __syncthreads();
   if (t == 0) {
     double tot = 0.0;

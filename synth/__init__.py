@@ -9,4 +9,4 @@ in face-weight form, with the spectral bounds the paper's experiments take as gi
 (Appendix A closed form) -- problem data, like kappa; the oracle pins its own
 copy of that formula against dense eigenvalues.
 """
-from .inputs import CONFIGS, Problem, make_problem, make_paper_problem, config  # noqa: F401
+from .inputs import CONFIGS, Problem, VaryingProblem, make_problem, make_paper_problem, make_varying_problem, config  # noqa: F401

@@ -174,3 +174,52 @@ def make_paper_problem(nx: int, ell: int = 10, alpha: float = 0.01, *, D: float 
                    kz=np.zeros((0, nx, nx)), b=b, method=method, k=max(1, round(nx * eta)),
                    rtol=1e-6, name=f"paper{nx}", seed=seed, bd=(f, f, 0.0),
                    mu_bounds=(mu_min, mu_max))
+
+
+@dataclasses.dataclass
+class VaryingProblem(Problem):
+    """Problem with varying diagonal blocks: block j has its own
+    diffusivity kx_blocks[j] (same layouts as kx); kx/ky/kz hold block 0's."""
+    kx_blocks: list = None
+    ky_blocks: list = None
+    kz_blocks: list = None
+
+
+def make_varying_problem(name: str = "headline", *, drift: float = 0.5, seed: int = 0, **kw) -> VaryingProblem:
+    """Time-varying diffusivity for the varying-block extension (DESIGN.md input recipe): the
+    seeded field of `name` (make_problem, same draws) modulated per block j by a second seeded
+    random Fourier field g2 of the same recipe (numpy default_rng(seed + 1)):
+        kappa_j = kappa * exp(0.5 * drift * (t_j - 1/2) * g2),  t_j = j / (ell - 1),
+    so the blocks drift smoothly across the window (drift = 0: every block equals block 0).
+    No method arithmetic: face values of seeded fields only."""
+    base = make_problem(name, seed=seed, **kw)
+    spec = CONFIGS[name]
+    dim = base.dim
+    nz, ny, nx = base.shape
+    ell = base.ell
+    rng = np.random.default_rng(seed + 1)
+    M = spec.modes
+    a = rng.standard_normal(M) / M
+    p = rng.integers(1, 5, M)
+    q = rng.integers(1, 5, M) if dim >= 2 else np.zeros(M, dtype=np.int64)
+    r = rng.integers(1, 5, M) if dim >= 3 else np.zeros(M, dtype=np.int64)
+    phi = rng.uniform(0.0, 2.0 * math.pi, M)
+    hx, hy, hz = 1.0 / nx, 1.0 / ny, 1.0 / nz
+    ic = (np.arange(nx) + 0.5) * hx
+    jc = (np.arange(ny) + 0.5) * hy
+    kc = (np.arange(nz) + 0.5) * hz
+    Zc, Yc, Xf = np.meshgrid(kc, jc, np.arange(1, nx) * hx, indexing="ij")
+    ex = _field(dim, a, p, q, r, phi, Xf, Yc, Zc)          # exp(g2 / 2) on x-faces
+    Zc, Yf, Xc = np.meshgrid(kc, np.arange(1, ny) * hy, ic, indexing="ij")
+    ey = _field(dim, a, p, q, r, phi, Xc, Yf, Zc)
+    Zf, Yc, Xc = np.meshgrid(np.arange(1, nz) * hz, jc, ic, indexing="ij")
+    ez = _field(dim, a, p, q, r, phi, Xc, Yc, Zf)
+    kxb, kyb, kzb = [], [], []
+    for j in range(ell):
+        s = drift * ((j / (ell - 1) if ell > 1 else 0.0) - 0.5)
+        kxb.append(np.ascontiguousarray(base.kx * ex ** s))
+        kyb.append(np.ascontiguousarray(base.ky * ey ** s))
+        kzb.append(np.ascontiguousarray(base.kz * ez ** s))
+    fields = {f.name: getattr(base, f.name) for f in dataclasses.fields(Problem)}
+    fields.update(kx=kxb[0], ky=kyb[0], kz=kzb[0], name=base.name + "-varying")
+    return VaryingProblem(**fields, kx_blocks=kxb, ky_blocks=kyb, kz_blocks=kzb)

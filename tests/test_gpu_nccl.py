@@ -66,7 +66,9 @@ CASES = [
 @pytest.mark.parametrize("name,kw,method,k,extra", CASES)
 def test_nccl_one_rank_bit_identical(name, kw, method, k, extra):
     p = synth.make_problem(name, **kw)
-    x0, i0, z0, kind0 = _solve(p, method, k, **extra)
+    # the NCCL path runs one-reduce Arnoldi by default (krylov.cuh arnoldi_lagged_step): the
+    # one-rank reference runs it too
+    x0, i0, z0, kind0 = _solve(p, method, k, AAC_GMRES_1R="1", **extra)
     x1, i1, z1, kind1 = _solve(p, method, k, AAC_NCCL_SELF="1", **extra)
     assert kind0 == "none" and kind1 == "nccl"
     assert i1["iters"] == i0["iters"] and i1["converged"] == 1

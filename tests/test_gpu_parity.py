@@ -144,6 +144,40 @@ def test_gmres_parity(name, kw, method, k):
     s.close()
 
 
+@pytest.mark.parametrize("name,kw,method,k", [("headline", dict(shape=(1, 130, 67)), "nc2", 8),
+                                              ("2d256", dict(n=256), "nc1", 5),
+                                              ("3d", dict(shape=(16, 16, 16)), "nc1", 10),
+                                              ("saddle", dict(shape=(1, 48, 40)), "sp", 8)])
+def test_gmres_one_reduce_parity(monkeypatch, name, kw, method, k):
+    """One-reduce Arnoldi (AAC_GMRES_1R=1, the default on several ranks): the
+    norm of each new basis vector comes from the Gram column of the projection pass, so every
+    step does one reduction. Same counts (+-1) and solutions (1e-9) as the oracle's literal CGS2,
+    and iterate-for-iterate the same as the two-reduction path at a forced equal m."""
+    from oracle import saddle
+    monkeypatch.setenv("AAC_GMRES_1R", "1")
+    p = synth.make_problem(name, **kw)
+    s = _solver(p, max_krylov=60)
+    x, info = s.gmres(method, k, _dev(p.b, p.ell), rtol=p.rtol, maxit=60)
+    if method == "sp":
+        w = op.weights(p)
+        lev = saddle.hierarchy(w)
+        ro = og.fgmres(lambda v: op.apply_allatonce(w, v),
+                       lambda r: saddle.sp_apply(w, r, p.ell, p.alpha, k, lev), p.b, p.rtol, 60)
+    else:
+        ro = _oracle_gmres(p, method, k, 60)
+    assert info["converged"] == 1 and abs(info["iters"] - ro.iters) <= 1
+    assert _rel(x.cpu().numpy(), ro.x) <= 1e-9
+    assert info["relres_true"] <= 1.5 * p.rtol
+    xm, im = s.gmres(method, k, _dev(p.b, p.ell), rtol=0.0, maxit=6)
+    s.close()
+    monkeypatch.setenv("AAC_GMRES_1R", "0")
+    s2 = _solver(p, max_krylov=60)
+    x2, i2 = s2.gmres(method, k, _dev(p.b, p.ell), rtol=0.0, maxit=6)
+    assert im["iters"] == i2["iters"] == 6
+    assert _rel(xm.cpu().numpy(), x2.cpu().numpy()) <= 1e-12
+    s2.close()
+
+
 def test_gmres_equal_iteration_count_agreement():
     """Forced equal m (rtol = 0, maxit = m): GPU and oracle iterates agree far below 1e-9."""
     p = synth.make_problem("2d256", shape=(1, 40, 45))

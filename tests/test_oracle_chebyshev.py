@@ -186,3 +186,18 @@ def test_c_zero_nc_is_exact():
     z = ch.nc_apply(w, r, ell, alpha, 1.0, op.gershgorin_max(w), [1] * ell)
     zd = np.linalg.solve(circ.dense_P_alpha(op.dense_A(w), ell, alpha), r.ravel())
     assert np.linalg.norm(z.ravel() - zd) <= 1e-12 * np.linalg.norm(zd) * circ.gamma_condition(ell, alpha)
+
+
+def test_paper_nc1_golden_is_self_consistent():
+    """The typed NC1 cells of Tables 3/4 (tests/golden/paper_nc1_tables.json): P_NC1 spends
+    ell (calA) + ell * n_x * eta (inner) matvecs per outer iteration (Table 1),
+    so every printed total equals its iteration count times that -- a check on every cell."""
+    d = json.load(open(os.path.join(HERE, "golden", "paper_nc1_tables.json")))
+    for tab in ("table3", "table4"):
+        T = d[tab]
+        for a in ("alpha_1", "alpha_0.01"):
+            for key, cells in T[a].items():
+                ell = T["ell"] if tab == "table3" else int(key)
+                nx = int(key) if tab == "table3" else T["nx"]
+                for eta, (its, mv) in zip(T["eta"], cells):
+                    assert its * (ell + ell * round(nx * eta)) == mv, (tab, a, key, eta)
