@@ -221,6 +221,17 @@ int aac_profile_flops(aac_ctx* ctx, int id, double* model_flops);
 int aac_profile_reset(aac_ctx* ctx);
 long long aac_launch_count(const aac_ctx* ctx);
 
+/* Varying diagonal blocks: from now on calA has block j's own
+ * operator A_j = I + c(-div kappa_j grad)_h (y_0 = A_0 x_0, y_j = A_j x_j - x_{j-1}), and every
+ * preconditioner is built on the average A_hat = (1/ell) sum_j A_j (= the operator of the mean
+ * face weights; mu_max its Gershgorin bound, mu_min = 1). kx, ky, kz: HOST, the ell blocks'
+ * GLOBAL face diffusivities stacked block after block, each in aac_setup's layout; copied.
+ * One rank, Neumann only; aac_ci is refused afterwards (the eigenvalue bounds behind the
+ * outer CI no longer hold) -- use aac_gmres. Drops cached plans and graphs.
+ * Errors: AAC_EINVAL (several ranks, Dirichlet faces, missing or non-positive kappa),
+ * AAC_ENOMEM, AAC_ECUDA.                                                                  */
+int aac_set_blocks(aac_ctx* ctx, const double* kx, const double* ky, const double* kz);
+
 /* Transport of the slab exchanges: 0 = none (one rank), 1 = NCCL (nranks > 1,
  * or the one-rank communicator AAC_NCCL_SELF=1 creates so that a single GPU runs the whole
  * multi-rank code path), 2 = the host-staged transport of aac_setup_host_transport.

@@ -21,7 +21,7 @@ METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP, "exac
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",
            "aac_gmres_host", "aac_gmres_host_batch", "aac_query", "aac_profile_enable", "aac_profile_count",
            "aac_profile_read", "aac_profile_flops", "aac_profile_reset", "aac_set_boundary",
-           "aac_set_bounds", "aac_ci", "aac_launch_count", "aac_comm_kind", "aac_last_error",
+           "aac_set_bounds", "aac_set_blocks", "aac_ci", "aac_launch_count", "aac_comm_kind", "aac_last_error",
            "aac_destroy"]
 
 
@@ -87,6 +87,7 @@ def _load():
         "aac_profile_reset": (I, [P]),
         "aac_set_boundary": (I, [P, D, D, D]),
         "aac_set_bounds": (I, [P, D, D]),
+        "aac_set_blocks": (I, [P, dp, dp, dp]),
         "aac_ci": (I, [P, I, I, P, P, D, D, D, I, ctypes.POINTER(aac_gmres_info)]),
         "aac_launch_count": (L, [P]),
         "aac_comm_kind": (I, [P]),

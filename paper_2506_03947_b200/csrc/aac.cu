@@ -408,6 +408,7 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   if (ctx->d_st) cudaFree(ctx->d_st);
   if (ctx->d_grp) cudaFree(ctx->d_grp);
   if (ctx->d_wext) cudaFree(ctx->d_wext);
+  if (ctx->d_wblk) cudaFree(ctx->d_wblk);
   if (ctx->d_S) cudaFree(ctx->d_S);
   if (ctx->d_lam1) cudaFree(ctx->d_lam1);
   if (ctx->d_T) cudaFree(ctx->d_T);
@@ -473,6 +474,8 @@ static inline bool vec2(const aac_ctx* ctx) {
   return (ctx->geo.nx % 2) == 0 && !(ctx->dim == 3 && v3_one);
 }
 
+#include "varying.cuh"      // varying diagonal blocks (N4)
+
 // ------------------------------------------------------------------------------------------
 // calA apply
 template <int DIM, int VEC>
@@ -498,6 +501,11 @@ static int halo_planes(aac_ctx* ctx, const double* x) {
 }
 
 static int matvec_impl(aac_ctx* ctx, const double* x, double* y) {
+  if (ctx->varying) {
+    AAC_TRY(matvec_var(ctx, x, 0, nullptr, y));
+    ctx->sweeps += ctx->ell;
+    return AAC_OK;
+  }
   AAC_TRY(halo_planes(ctx, x));
   const double V = 8.0 * ctx->ell * ctx->geo.N, C = 8.0 * ctx->dim * ctx->geo.N;
   const double bytes = 2 * V + C;
@@ -1158,7 +1166,10 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
   const double V = 8.0 * ctx->ell * g.N, C = 8.0 * ctx->dim * g.N;
   KAParams P{ctx->d_Z, ctx->d_V, ctx->d_W, L, ctx->d_part,
              ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, arnoldi_ctx(ctx)};
-  if (!FUSED) {                      // w = calA Z_j by the stencil kernel (j read on the device)
+  if (!FUSED && ctx->varying) {      // varying blocks: each plane its own operator
+    AAC_TRY(matvec_var(ctx, ctx->d_Z, L, reinterpret_cast<const int*>(ctx->d_st), ctx->d_W));
+    ctx->sweeps += ctx->ell;
+  } else if (!FUSED) {               // w = calA Z_j by the stencil kernel (j read on the device)
     const bool v2 = vec2(ctx);
     const dim3 gm(grid1d(g.nx / (v2 ? 2 : 1), 256), g.ny, g.nz);
     const int* jd = reinterpret_cast<const int*>(ctx->d_st);
@@ -1191,7 +1202,8 @@ template <int DIM>
 static int arnoldi_dim(aac_ctx* ctx, int host_j) {
   const bool tma = (ctx->geo.nx % 2) == 0;          // row-aligned tiles start at row * nx
   // split (k_matvec + dot kernel) by default; AAC_FUSED_ARNOLDI=1 keeps the stencil in-kernel
-  static const bool fused = getenv("AAC_FUSED_ARNOLDI") != nullptr;
+  static const bool fused_env = getenv("AAC_FUSED_ARNOLDI") != nullptr;
+  const bool fused = fused_env && !ctx->varying;   // (the fused stencil knows one operator)
   if (ctx->ell <= 10) {
     if (fused) return tma ? launch_arnoldi<DIM, 10, true, true>(ctx, host_j) : launch_arnoldi<DIM, 10, false, true>(ctx, host_j);
     return tma ? launch_arnoldi<DIM, 10, true, false>(ctx, host_j) : launch_arnoldi<DIM, 10, false, false>(ctx, host_j);

@@ -142,6 +142,10 @@ struct aac_ctx {
   double* d_lam1 = nullptr;            // [n] w * 4 sin^2(pi (i+1) / (2 (n+1)))
   double* d_T = nullptr;               // [ell][n][n] GEMM intermediate
   int exact_n = 0;                     // > 0 once prepared
+  // varying diagonal blocks (aac_set_blocks): per-block face weights; d_w then holds
+  // the mean-block A_hat the preconditioner uses
+  double* d_wblk = nullptr;            // [ell][wlen[0] + wlen[1] + wlen[2]]
+  bool varying = false;
   // NCCL (dlopen'ed), or the host-staged transport
   void* nccl_comm = nullptr;
   bool nccl_self = false;              // AAC_NCCL_SELF=1: a one-rank NCCL communicator (test switch)

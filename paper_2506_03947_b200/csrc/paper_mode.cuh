@@ -19,8 +19,66 @@ static void invalidate_plans(aac_ctx* ctx) {
   sp_destroy(ctx);
 }
 
+// ------------------------------------------------------------------------------------------
+// Varying diagonal blocks (varying.cuh).
+extern "C" int aac_set_blocks(aac_ctx* ctx, const double* kx, const double* ky, const double* kz) {
+  if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_blocks: NULL ctx");
+  if (ctx->nranks != 1 || ctx->host_tr || ctx->nccl_self)
+    return aac_fail(ctx, AAC_EINVAL, "aac_set_blocks: one rank only");
+  if (ctx->geo.dir) return aac_fail(ctx, AAC_EINVAL, "aac_set_blocks: the Neumann operator only");
+  if (!kx || (ctx->dim >= 2 && !ky) || (ctx->dim >= 3 && !kz))
+    return aac_fail(ctx, AAC_EINVAL, "aac_set_blocks: kappa arrays missing for a used axis");
+  const long long nx = ctx->n[0], ny = ctx->n[1], nz = ctx->n[2];
+  const long long sx = nz * ny * (nx - 1), sy = nz * (ny - 1) * nx, sz = (nz - 1) * ny * nx;
+  aac_grid g{};
+  g.dim = ctx->dim;
+  g.n[0] = nx;
+  g.n[1] = ny;
+  g.n[2] = nz;
+  g.rank = 0;
+  g.nranks = 1;
+  const long long wtot = ctx->wlen[0] + ctx->wlen[1] + ctx->wlen[2];
+  std::vector<double> all((size_t)ctx->ell * wtot), mean((size_t)wtot, 0.0), hw;
+  long long lens[3];
+  for (int j = 0; j < ctx->ell; ++j) {
+    double gm;
+    if (!slab_weights(&g, kx + j * sx, ctx->dim >= 2 ? ky + j * sy : nullptr, ctx->dim >= 3 ? kz + j * sz : nullptr,
+                      ctx->c, 0, ctx->dim == 1 ? 1 : ctx->n[ctx->dim - 1], hw, lens, &gm))
+      return aac_fail(ctx, AAC_EINVAL, "aac_set_blocks: kappa of block %d must be finite and > 0", j);
+    std::copy(hw.begin(), hw.end(), all.begin() + (size_t)j * wtot);
+    for (long long i = 0; i < wtot; ++i) mean[i] += hw[i];
+  }
+  for (auto& v : mean) v /= ctx->ell;            // A_hat = mean_j A_j (affine in the weights)
+  // Gershgorin bound of A_hat (reading R5); mu_min = 1 exactly (A_hat 1 = 1 under Neumann)
+  const double* wx = mean.data();
+  const double* wy = wx + ctx->wlen[0];
+  const double* wz = wy + ctx->wlen[1];
+  const Geo& G = ctx->geo;
+  double gmax = 1.0;
+  for (long long p = 0; p < G.N; ++p) {
+    double sum = wx[p] + wx[p + 1];
+    if (ctx->dim >= 2) sum += wy[p] + wy[p + G.nx];
+    if (ctx->dim >= 3) sum += wz[p] + wz[p + G.S];
+    gmax = fmax(gmax, 1.0 + 2.0 * sum);
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (!ctx->d_wblk && cudaMalloc((void**)&ctx->d_wblk, all.size() * sizeof(double)) != cudaSuccess) {
+    ctx->d_wblk = nullptr;
+    cudaGetLastError();
+    return aac_fail(ctx, AAC_ENOMEM, "aac_set_blocks: allocation failed");
+  }
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_wblk, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_w, mean.data(), mean.size() * sizeof(double), cudaMemcpyHostToDevice));
+  invalidate_plans(ctx);
+  ctx->mu_min = 1.0;
+  ctx->mu_max = gmax;
+  ctx->varying = true;
+  return AAC_OK;
+}
+
 extern "C" int aac_set_boundary(aac_ctx* ctx, double bx, double by, double bz) {
   if (!ctx) return aac_fail(nullptr, AAC_EINVAL, "aac_set_boundary: NULL ctx");
+  if (ctx->varying) return aac_fail(ctx, AAC_EINVAL, "aac_set_boundary: not with varying blocks");
   if (!(bx >= 0.0 && by >= 0.0 && bz >= 0.0) || !std::isfinite(bx + by + bz))
     return aac_fail(ctx, AAC_EINVAL, "boundary face weights must be finite and >= 0");
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -81,6 +139,8 @@ extern "C" int aac_ci(aac_ctx* ctx, int method, int k, const double* b, double* 
                       double lmax, double tol, int maxit, aac_gmres_info* info) {
   if (!ctx || !b || !x || b == x) return aac_fail(ctx, AAC_EINVAL, "aac_ci: bad pointers");
   NvtxRange nv("aac_ci");
+  if (ctx->varying)   // the eigenvalue bounds behind the outer CI no longer hold
+    return aac_fail(ctx, AAC_EINVAL, "aac_ci: varying blocks (aac_set_blocks) need GMRES, not CI (PAPER.md:991)");
   if (method != AAC_NONE && method != AAC_NC1 && method != AAC_NC2 && method != AAC_SP && method != AAC_EXACT)
     return aac_fail(ctx, AAC_EINVAL, "unknown method %d", method);
   if ((method == AAC_NC1 || method == AAC_NC2 || method == AAC_SP) && k < 1)

@@ -204,6 +204,23 @@ class Solver:
         check(lib.aac_query(self.ctx, 1, 1, ctypes.byref(mu0), ctypes.byref(mu1), None, None), self.ctx)
         self.mu_min, self.mu_max = mu0.value, mu1.value
 
+    def set_blocks(self, kx_blocks, ky_blocks=None, kz_blocks=None):
+        """aac_set_blocks: varying diagonal blocks A_j (one face-diffusivity set per block, each
+        in the setup layout); the preconditioners then use the mean block A_hat."""
+        def stack(bl):
+            if bl is None:
+                return None
+            a = np.ascontiguousarray(np.stack([np.asarray(b, dtype=np.float64) for b in bl]))
+            if len(bl) != self.ell:
+                raise ValueError(f"need {self.ell} blocks")
+            return a
+        kx, ky, kz = stack(kx_blocks), stack(ky_blocks), stack(kz_blocks)
+        check(lib.aac_set_blocks(self.ctx, _dptr(kx), _dptr(ky) if ky is not None else None,
+                                 _dptr(kz) if kz is not None else None), self.ctx)
+        mu0, mu1 = ctypes.c_double(), ctypes.c_double()
+        check(lib.aac_query(self.ctx, 1, 1, ctypes.byref(mu0), ctypes.byref(mu1), None, None), self.ctx)
+        self.mu_min, self.mu_max = mu0.value, mu1.value
+
     def set_bounds(self, mu_min, mu_max):
         check(lib.aac_set_bounds(self.ctx, float(mu_min), float(mu_max)), self.ctx)
         self.mu_min, self.mu_max = float(mu_min), float(mu_max)
@@ -270,4 +287,7 @@ def from_problem(prob, *, rank=0, nranks=1, nccl_id=None, max_krylov=64, **kw) -
     mb = getattr(prob, "mu_bounds", None)
     if mb is not None:
         s.set_bounds(*mb)
+    kb = getattr(prob, "kx_blocks", None)
+    if kb is not None:                           # varying diagonal blocks (N4)
+        s.set_blocks(kb, prob.ky_blocks if prob.dim >= 2 else None, prob.kz_blocks if prob.dim >= 3 else None)
     return s
