@@ -53,6 +53,12 @@ enum {
 };
 
 enum { AAC_NONE = 0, AAC_NC1 = 1, AAC_NC2 = 2, AAC_SP = 3, AAC_EXACT = 4 };
+/* Flag OR'ed into AAC_NC1 / AAC_NC2 (aac_precond_apply, aac_gmres*): mixed precision
+ * -- the Chebyshev recurrence of the shifted solves runs in fp32 (operands
+ * and iterates stay fp64 in memory), the transforms, calA and GMRES in fp64. The
+ * preconditioner is then no longer the fp64 one (FGMRES absorbs the difference). 2D only
+ * (the wavefront path); other geometries return AAC_EINVAL.                              */
+enum { AAC_F32 = 16 };
 
 typedef struct {
   int dim;          /* 1, 2 or 3                                                     */

@@ -127,3 +127,37 @@ def nc_apply(w: op.Weights, r, ell: int, alpha: float, mu_min: float, mu_max: fl
         yhat[k] = ci_solve(lambda v, lk=lk: op.apply_A(w, v) - lk * v, what[k],
                            theta, delta, int(alloc[k]))
     return circ.inverse(yhat, ell, alpha)
+
+
+def nc_apply_f32(w: op.Weights, r, ell: int, alpha: float, mu_min: float, mu_max: float, alloc):
+    """Mixed-precision P_NC^{-1} r (fp32 inner sweeps, fp64 outer): nc_apply with
+    every block's CI recurrence evaluated in single precision -- the transformed right-hand side,
+    the face weights and the iterates in complex64 / float32, the scalars theta, delta, rho_s
+    computed in fp64 and rounded to fp32 -- and the transforms in fp64. Parity unpinned by the
+    paper (it names the setting only); pinned against nc_apply to fp32 accuracy."""
+    r = np.asarray(r).reshape((ell,) + w.shape)
+    what = circ.forward(r, ell, alpha)
+    lam = circ.shifts(ell, alpha)
+    delta = 0.5 * (mu_max - mu_min)
+    w32 = op.Weights.__new__(op.Weights)
+    w32.shape = w.shape
+    w32.wx, w32.wy, w32.wz = (np.asarray(a, dtype=np.float32) for a in (w.wx, w.wy, w.wz))
+    w32.bd = tuple(np.float32(v) for v in getattr(w, "bd", (0.0, 0.0, 0.0)))
+    yhat = np.empty_like(what)
+    for k in range(ell):
+        theta = 0.5 * (mu_max + mu_min) - lam[k]
+        lk = np.complex64(lam[k])
+        b = what[k].astype(np.complex64)
+        p = int(alloc[k])
+        x_prev = np.zeros_like(b)
+        x = (b * np.complex64(1.0 / theta)).astype(np.complex64)
+        if delta > 0.0:
+            rho_prev = delta / theta
+            for _s in range(1, p):
+                rho = 1.0 / (2.0 * theta / delta - rho_prev)
+                a_s, b_s = np.complex64(rho * rho_prev), np.complex64(2.0 * rho / delta)
+                res = b - (op.apply_A(w32, x).astype(np.complex64) - lk * x)
+                x_next = x + a_s * (x - x_prev) + b_s * res
+                x_prev, x, rho_prev = x, x_next.astype(np.complex64), rho
+        yhat[k] = x.astype(np.complex128)
+    return circ.inverse(yhat, ell, alpha)

@@ -15,7 +15,9 @@ LIB_PATH = os.path.join(HERE, "libaac.so")
 
 AAC_OK, AAC_ENOCONV, AAC_EINVAL, AAC_ECUDA, AAC_ENCCL, AAC_ENOMEM = 0, 1, -1, -2, -3, -4
 AAC_NONE, AAC_NC1, AAC_NC2, AAC_SP, AAC_EXACT = 0, 1, 2, 3, 4
-METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP, "exact": AAC_EXACT}
+AAC_F32 = 16                     # OR'ed into nc1 / nc2: fp32 inner Chebyshev recurrence
+METHODS = {"none": AAC_NONE, "nc1": AAC_NC1, "nc2": AAC_NC2, "sp": AAC_SP, "exact": AAC_EXACT,
+           "nc1-f32": AAC_NC1 | AAC_F32, "nc2-f32": AAC_NC2 | AAC_F32}
 
 # Every symbol include/aac.h declares (tests check the .so exports all of them).
 SYMBOLS = ["aac_slab_range", "aac_slab_weights", "aac_setup", "aac_setup_host_transport", "aac_matvec", "aac_precond_apply", "aac_gmres",

@@ -740,45 +740,32 @@ static int forward_step(aac_ctx* ctx, double bytes) {
 // Per-block wavefront launches (wave_r.cuh): one kernel instantiation per (steps, real/complex,
 // general, first pass), the active blocks of a pass forked over the auxiliary streams and joined
 // back into the library stream (a fork/join subgraph under graph capture).
-template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT>
+template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
 static int waver_launch_t(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
                           cudaStream_t s) {
-  // one warp role per CTA (k_waver) by default; AAC_WAVE_ROLES=2: two roles for 5+ steps
-  // (k_waver2: measured slower at the headline, 9.51 vs 8.63 ms per solve -- barrier stalls and
-  // spills at the 128-register cap)
-  static const bool two_roles = getenv("AAC_WAVE_ROLES") && atoi(getenv("AAC_WAVE_ROLES")) == 2;
-  if constexpr (NS >= 5) {
-    if (two_roles) {
-      auto kern = k_waver2<H, NT, NS, CPLX, GEN, VIRT>;
-      const size_t smem = waver2_smem<NT>(NS, CPLX ? 2 : 1);
-      AAC_TRY(smem_optin(ctx, kern, smem));
-      kern<<<ncta, 2 * NT, smem, s>>>(ctx->geo, P, ctx->d_what, st, sl);
-      return AAC_OK;
-    }
-  }
-  auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT>;
-  const size_t smem = waver_smem<NT>(NS, CPLX ? 2 : 1);
+  auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT, T>;
+  const size_t smem = waver_smem<NT, T>(NS, CPLX ? 2 : 1);
   AAC_TRY(smem_optin(ctx, kern, smem));
   kern<<<ncta, NT, smem, s>>>(ctx->geo, P, ctx->d_what, st, sl);
   return AAC_OK;
 }
 
-template <int H, int NT, int NS>
+template <int H, int NT, int NS, typename T>
 static int waver_launch_ns(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
                            cudaStream_t s, bool gen) {
   if constexpr (NS >= 1) {
-    if (P.b.ns != NS) return waver_launch_ns<H, NT, NS - 1>(ctx, P, ncta, sl, st, s, gen);
+    if (P.b.ns != NS) return waver_launch_ns<H, NT, NS - 1, T>(ctx, P, ncta, sl, st, s, gen);
     const bool c = P.b.np == 2, v = P.b.virt != 0;
     if (gen) {
-      if (c) return v ? waver_launch_t<H, NT, NS, true, true, true>(ctx, P, ncta, sl, st, s)
-                      : waver_launch_t<H, NT, NS, true, true, false>(ctx, P, ncta, sl, st, s);
-      return v ? waver_launch_t<H, NT, NS, false, true, true>(ctx, P, ncta, sl, st, s)
-               : waver_launch_t<H, NT, NS, false, true, false>(ctx, P, ncta, sl, st, s);
+      if (c) return v ? waver_launch_t<H, NT, NS, true, true, true, T>(ctx, P, ncta, sl, st, s)
+                      : waver_launch_t<H, NT, NS, true, true, false, T>(ctx, P, ncta, sl, st, s);
+      return v ? waver_launch_t<H, NT, NS, false, true, true, T>(ctx, P, ncta, sl, st, s)
+               : waver_launch_t<H, NT, NS, false, true, false, T>(ctx, P, ncta, sl, st, s);
     }
-    if (c) return v ? waver_launch_t<H, NT, NS, true, false, true>(ctx, P, ncta, sl, st, s)
-                    : waver_launch_t<H, NT, NS, true, false, false>(ctx, P, ncta, sl, st, s);
-    return v ? waver_launch_t<H, NT, NS, false, false, true>(ctx, P, ncta, sl, st, s)
-             : waver_launch_t<H, NT, NS, false, false, false>(ctx, P, ncta, sl, st, s);
+    if (c) return v ? waver_launch_t<H, NT, NS, true, false, true, T>(ctx, P, ncta, sl, st, s)
+                    : waver_launch_t<H, NT, NS, true, false, false, T>(ctx, P, ncta, sl, st, s);
+    return v ? waver_launch_t<H, NT, NS, false, false, true, T>(ctx, P, ncta, sl, st, s)
+             : waver_launch_t<H, NT, NS, false, false, false, T>(ctx, P, ncta, sl, st, s);
   }
   return aac_fail(ctx, AAC_EINVAL, "wavefront: bad step count %d", P.b.ns);
 }
@@ -808,13 +795,15 @@ static int waver_group(aac_ctx* ctx, const WSweep& S, int nchunk, const WSlab& s
     for (int a = 0; a < naux; ++a) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux[a], ctx->ev_fork, 0));
   }
   for (int i = 0; i < S.nb; ++i) {
-    // strips of NT - 2 ns columns: the x-halo of a block is its step count (one-role kernel)
-    static const bool two_roles = getenv("AAC_WAVE_ROLES") && atoi(getenv("AAC_WAVE_ROLES")) == 2;
-    const int halo = (two_roles && S.b[i].ns >= 5) ? H : S.b[i].ns;
+    // strips of NT - 2 ns columns: the x-halo of a block is its step count
+    const int halo = S.b[i].ns;
     const int nstrip = (ctx->geo.nx + (NT - 2 * halo) - 1) / (NT - 2 * halo);
     const cudaStream_t s = i == 0 ? ctx->stream : ctx->aux[(i - 1) % naux];
-    const WROne P{S.b[i], two_roles && S.b[i].ns >= 5 ? S.nstrip : nstrip, S.ly[i]};
-    AAC_TRY(waver_launch_ns<H, NT, H>(ctx, P, P.nstrip * nchunk, sl, st, s, gen));
+    const WROne P{S.b[i], nstrip, S.ly[i]};
+    if (ctx->inner_f32)                 // mixed precision (AAC_F32): fp32 recurrence, fp64 storage
+      AAC_TRY((waver_launch_ns<H, NT, H, float>(ctx, P, P.nstrip * nchunk, sl, st, s, gen)));
+    else
+      AAC_TRY((waver_launch_ns<H, NT, H, double>(ctx, P, P.nstrip * nchunk, sl, st, s, gen)));
   }
   for (int a = 0; a < naux; ++a) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
@@ -1032,9 +1021,11 @@ static int nc_apply_t(aac_ctx* ctx, const NcPlan& P, const double* r, double* zb
   }
   // wavefront: one rank, or slabs of >= WAVE_MAXH rows with every block done in one pass (the
   // halo exchange covers hat w only)
-  if (DIM == 2 && ctx->wave_h > 0 && wave_pays(ctx, P) &&
+  if (DIM == 2 && ctx->wave_h > 0 && (wave_pays(ctx, P) || ctx->inner_f32) &&
       (ctx->nranks == 1 || (ctx->wave_hd > 0 && P.pmax - 1 <= WAVE_MAXH && ctx->wave_h == WAVE_MAXH)))
     return wave_passes(ctx, P, zbase, zjs, st);
+  if (ctx->inner_f32)
+    return aac_fail(ctx, AAC_EINVAL, "AAC_F32 (mixed precision) needs the 2D wavefront path (dim 2)");
   double* X = ctx->d_X;
   auto slot = [&](int s, int q) { return X + (long long)(s % 3) * L + (long long)q * N; };
   const double* hlo = ctx->d_halo;
@@ -1134,8 +1125,26 @@ static int nc_apply(aac_ctx* ctx, int method, int k, const double* r, double* z,
 
 #include "exact_host.cuh"   // exact P_alpha for the paper operator (N3): host side
 
+// method | AAC_F32: this call's NC inner solves in fp32 (reset on return)
+struct F32Scope {
+  aac_ctx* c;
+  F32Scope(aac_ctx* c_, bool on) : c(c_) { c->inner_f32 = on; }
+  ~F32Scope() { c->inner_f32 = false; }
+};
+
+static int split_f32(aac_ctx* ctx, int* method, bool* f32) {
+  *f32 = (*method & AAC_F32) != 0;
+  *method &= ~AAC_F32;
+  if (*f32 && *method != AAC_NC1 && *method != AAC_NC2)
+    return aac_fail(ctx, AAC_EINVAL, "AAC_F32 applies to the nested Chebyshev methods (AAC_NC1 / AAC_NC2)");
+  return AAC_OK;
+}
+
 extern "C" int aac_precond_apply(aac_ctx* ctx, int method, int k, const double* r, double* z) {
   if (!ctx || !r || !z || r == z) return aac_fail(ctx, AAC_EINVAL, "aac_precond_apply: bad pointers");
+  bool f32 = false;
+  AAC_TRY(split_f32(ctx, &method, &f32));
+  F32Scope fs(ctx, f32);
   if (k < 1 && method != AAC_EXACT) return aac_fail(ctx, AAC_EINVAL, "inner iteration count k must be >= 1");
   AAC_TRY(check_alpha(ctx));
   NvtxRange nv("aac_precond_apply");
@@ -1263,7 +1272,7 @@ static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
     if (ge.method == method && ge.k == k) { *out = &ge; return AAC_OK; }
   const long long l0 = ctx->launches;
   CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  int rc = arnoldi_step(ctx, method, k, 0);
+  int rc = arnoldi_step(ctx, method & ~AAC_F32, k, 0);       // (the key keeps the AAC_F32 flag)
   if (rc == AAC_OK) rc = publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState));
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
@@ -1285,6 +1294,9 @@ static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
 static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* x, double rtol,
                       int maxit, aac_gmres_info* info) {
   NvtxRange nv("aac_gmres");
+  bool f32 = false;
+  AAC_TRY(split_f32(ctx, &method, &f32));
+  F32Scope fs(ctx, f32);
   if (maxit < 1 || maxit > ctx->max_krylov)
     return aac_fail(ctx, AAC_EINVAL, "maxit must be in [1, max_krylov=%d]", ctx->max_krylov);
   if (!(rtol >= 0.0)) return aac_fail(ctx, AAC_EINVAL, "rtol must be >= 0");
@@ -1316,7 +1328,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   }
   GraphEntry* ge = nullptr;
   const bool graphs = ctx->use_graphs && !ctx->prof;
-  if (graphs) AAC_TRY(get_graph(ctx, method, k, &ge));
+  if (graphs) AAC_TRY(get_graph(ctx, method | (f32 ? AAC_F32 : 0), k, &ge));
   // Arnoldi steps. Graph path: replay one captured step per iteration and poll the state of
   // the PREVIOUS step (speculative: a step launched after convergence returns at once).
   int it = 0;

@@ -160,6 +160,7 @@ struct aac_ctx {
   bool prof = false;
   bool eager_poll = false;             // eager GMRES: read the state back after each forward step
   bool one_reduce = false;             // lagged normalisation: one reduction per Arnoldi step
+  bool inner_f32 = false;              // this call's NC inner solves in fp32 (method | AAC_F32)
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[KID_COUNT] = {0};

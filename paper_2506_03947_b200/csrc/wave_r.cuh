@@ -91,15 +91,13 @@ __device__ __forceinline__ void waver_load(const WBlk& B, const double* __restri
 // rows r-1 (dn), r (c), r+1 (up), its x-neighbours (xl_nb, xr_nb) and L_{i-1} at row r (m)):
 //   res = w - e c - i Im(Lambda) c + sum_f w_f c_nb(f),  x_new = c + a (c - m) + b res,
 // e = 1 + sum_f w_f - Re Lambda; the y+1 neighbour enters last (it is the newest value).
-template <bool CPLX>
-__device__ __forceinline__ void wr_level(double c0, double c1, double up0, double up1, double dn0, double dn1,
-                                         double m0, double m1, double l0, double l1, double rr0, double rr1,
-                                         double w0, double w1, double e, double fxl, double fxh, double fyl,
-                                         double fyh, double li, double ar, double ai, double br, double bi,
-                                         double& o0, double& o1) {
-  double q0 = fma(-e, c0, w0);
+template <bool CPLX, typename T>
+__device__ __forceinline__ void wr_level(T c0, T c1, T up0, T up1, T dn0, T dn1, T m0, T m1, T l0, T l1, T rr0,
+                                         T rr1, T w0, T w1, T e, T fxl, T fxh, T fyl, T fyh, T li, T ar, T ai,
+                                         T br, T bi, T& o0, T& o1) {
+  T q0 = fma(-e, c0, w0);
   if constexpr (CPLX) {
-    double q1 = fma(-e, c1, w1);
+    T q1 = fma(-e, c1, w1);
     q0 = fma(-li, c1, q0);
     q1 = fma(li, c0, q1);
     q0 = fma(fxl, l0, q0);
@@ -108,20 +106,20 @@ __device__ __forceinline__ void wr_level(double c0, double c1, double up0, doubl
     q1 = fma(fxh, rr1, q1);
     q0 = fma(fyl, dn0, q0);
     q1 = fma(fyl, dn1, q1);
-    const double dr = c0 - m0, di = c1 - m1;
-    const double X0 = fma(-ai, di, fma(ar, dr, c0));
-    const double X1 = fma(ai, dr, fma(ar, di, c1));
-    const double r0 = fma(fyh, up0, q0);
-    const double r1 = fma(fyh, up1, q1);
+    const T dr = c0 - m0, di = c1 - m1;
+    const T X0 = fma(-ai, di, fma(ar, dr, c0));
+    const T X1 = fma(ai, dr, fma(ar, di, c1));
+    const T r0 = fma(fyh, up0, q0);
+    const T r1 = fma(fyh, up1, q1);
     o0 = fma(-bi, r1, fma(br, r0, X0));
     o1 = fma(bi, r0, fma(br, r1, X1));
   } else {
     q0 = fma(fxl, l0, q0);
     q0 = fma(fxh, rr0, q0);
     q0 = fma(fyl, dn0, q0);
-    const double X0 = fma(ar, c0 - m0, c0);
+    const T X0 = fma(ar, c0 - m0, c0);
     o0 = fma(br, fma(fyh, up0, q0), X0);
-    o1 = 0.0;
+    o1 = T(0);
   }
 }
 
@@ -135,25 +133,25 @@ __device__ __forceinline__ void wr_level(double c0, double c1, double up0, doubl
 //                  moves). A 9-slot row ring with the step loop unrolled by 9 needs no moves but
 //                  measured slower (8.58 vs 8.36 ms per headline solve: a 58 KB loop body and
 //                  uniform-register spills).
-template <int NS, int NP>
+template <int NS, int NP, typename T>
 struct WRState {
-  double L[NS + 1][3][NP];
-  double Rw[NS + 1][NP], Re[NS + 1], Rxl[NS + 1], Rxh[NS + 1], Ryl[NS + 1];
+  T L[NS + 1][3][NP];
+  T Rw[NS + 1][NP], Re[NS + 1], Rxl[NS + 1], Rxh[NS + 1], Ryl[NS + 1];
 };
 
 template <int PH, int A>
 struct WSlot { static constexpr int v = ((A - PH) % 3 + 3) % 3; };
 
 // One step tau (tau mod 3 == PH) of the wavefront.
-template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, int PH>
-__device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1>& S, const WBlk& B,
+template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, int PH, typename T>
+__device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, const WBlk& B,
                                            const double* __restrict__ what, const Geo& g, const WSlab& sl,
-                                           double* xch, int t, int x, bool colin, bool colout, int y0,
+                                           T* xch, int t, int x, bool colin, bool colout, int y0,
                                            int y1, int tau, int tau1, double e0, double dB, WRRow& nxt) {
   constexpr int XW = WRGeom<NT>::XW;
   constexpr int NP = CPLX ? 2 : 1;
   constexpr int S0 = WSlot<PH, 0>::v, S1 = WSlot<PH, 1>::v, S2 = WSlot<PH, 2>::v;
-  double* xb = xch + (tau & 1) * (NS * NP * XW) + 1 + t;
+  T* xb = xch + (tau & 1) * (NS * NP * XW) + 1 + t;
   // (1) publish the newest row of every level (L_i at row tau - i; age 1 after this step's
   //     push) for the x-neighbours
 #pragma unroll
@@ -172,11 +170,13 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1>& S, const W
   }
   const WRRow cur = nxt;
   if (tau + 1 < tau1) waver_load<CPLX, GEN, VIRT>(B, what, g, sl, x, colin, tau + 1, nxt);
-  S.Rw[0][0] = cur.w0;
-  if (CPLX) S.Rw[0][1] = cur.w1;
-  S.Rxl[0] = cur.xl;
-  S.Rxh[0] = cur.xh;
-  S.Ryl[0] = cur.yl;
+  // (the operands are stored in fp64; T = float computes the recurrence in fp32: the
+  //  mixed-precision inner solve of AAC_F32, fp64 GMRES outside)
+  S.Rw[0][0] = T(cur.w0);
+  if (CPLX) S.Rw[0][1] = T(cur.w1);
+  S.Rxl[0] = T(cur.xl);
+  S.Rxh[0] = T(cur.xh);
+  S.Ryl[0] = T(cur.yl);
   {
     double dd = dB;
     if (GEN && g.dir) {
@@ -184,33 +184,34 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1>& S, const W
       dd += g.bdy * ((rg == 0) + (rg == sl.nyg - 1));
     }
     // (out of the domain: e = 1 - Re Lambda on zero iterates and zero weights -- harmless)
-    S.Re[0] = ((e0 + dd) + (cur.xl + cur.xh)) + (cur.yl + cur.yh);
+    S.Re[0] = T(((e0 + dd) + (cur.xl + cur.xh)) + (cur.yl + cur.yh));
   }
   if constexpr (VIRT) {                                  // x_0 = 0, x_1 = w / theta
-    S.L[1][S0][0] = B.sr * cur.w0 - B.si * cur.w1;
-    if (CPLX) S.L[1][S0][1] = B.sr * cur.w1 + B.si * cur.w0;
+    S.L[1][S0][0] = T(B.sr * cur.w0 - B.si * cur.w1);
+    if (CPLX) S.L[1][S0][1] = T(B.sr * cur.w1 + B.si * cur.w0);
   } else {
-    S.L[1][S0][0] = cur.s0;
-    S.L[0][S0][0] = cur.m0;
+    S.L[1][S0][0] = T(cur.s0);
+    S.L[0][S0][0] = T(cur.m0);
     if (CPLX) {
-      S.L[1][S0][1] = cur.s1;
-      S.L[0][S0][1] = cur.m1;
+      S.L[1][S0][1] = T(cur.s1);
+      S.L[0][S0][1] = T(cur.m1);
     }
   }
   __syncthreads();
   // (3) levels: L_{i+1} at row r = tau - i
-  const double li = B.li;
+  const T li = T(B.li);
 #pragma unroll
   for (int i = 1; i <= NS; ++i) {
-    const double* xr = xb + ((i - 1) * NP) * XW;
+    const T* xr = xb + ((i - 1) * NP) * XW;
     const int e1 = CPLX ? 1 : 0;
-    double o0, o1;
-    wr_level<CPLX>(S.L[i][S1][0], S.L[i][S1][e1], S.L[i][S0][0], S.L[i][S0][e1], S.L[i][S2][0], S.L[i][S2][e1],
-                   i == 1 ? (VIRT ? 0.0 : S.L[0][S1][0]) : S.L[i - 1][S2][0],
-                   i == 1 ? (VIRT ? 0.0 : S.L[0][S1][e1]) : S.L[i - 1][S2][e1],
-                   xr[-1], CPLX ? xr[XW - 1] : 0.0, xr[1], CPLX ? xr[XW + 1] : 0.0,
-                   S.Rw[i][0], S.Rw[i][e1], S.Re[i], S.Rxl[i], S.Rxh[i], S.Ryl[i], S.Ryl[i - 1], li,
-                   B.ar[i - 1], CPLX ? B.ai[i - 1] : 0.0, B.br[i - 1], CPLX ? B.bi[i - 1] : 0.0, o0, o1);
+    T o0, o1;
+    wr_level<CPLX, T>(S.L[i][S1][0], S.L[i][S1][e1], S.L[i][S0][0], S.L[i][S0][e1], S.L[i][S2][0], S.L[i][S2][e1],
+                      i == 1 ? (VIRT ? T(0) : S.L[0][S1][0]) : S.L[i - 1][S2][0],
+                      i == 1 ? (VIRT ? T(0) : S.L[0][S1][e1]) : S.L[i - 1][S2][e1],
+                      xr[-1], CPLX ? xr[XW - 1] : T(0), xr[1], CPLX ? xr[XW + 1] : T(0),
+                      S.Rw[i][0], S.Rw[i][e1], S.Re[i], S.Rxl[i], S.Rxh[i], S.Ryl[i], S.Ryl[i - 1], li,
+                      T(B.ar[i - 1]), CPLX ? T(B.ai[i - 1]) : T(0), T(B.br[i - 1]), CPLX ? T(B.bi[i - 1]) : T(0),
+                      o0, o1);
     if (i == NS) {
       const int r = tau - i;
       if (colout && r >= y0 && r < y1) {
@@ -230,21 +231,21 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1>& S, const W
 }
 
 // All ns steps of one block over this CTA's strip x row chunk.
-template <int NT, int NS, bool CPLX, bool GEN, bool VIRT>
+template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
 __device__ __forceinline__ void waver_block(const WBlk& B, const double* __restrict__ what, const Geo& g,
-                                            const WSlab& sl, double* xch, int t, int x, bool colin,
+                                            const WSlab& sl, T* xch, int t, int x, bool colin,
                                             bool colout, int y0, int y1) {
   constexpr int NP = CPLX ? 2 : 1;
-  WRState<NS, NP> S;
+  WRState<NS, NP, T> S;
 #pragma unroll
   for (int i = 0; i <= NS; ++i) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int e = 0; e < NP; ++e) S.L[i][a][e] = 0.0;
+      for (int e = 0; e < NP; ++e) S.L[i][a][e] = T(0);
 #pragma unroll
-    for (int e = 0; e < NP; ++e) S.Rw[i][e] = 0.0;
-    S.Re[i] = S.Rxl[i] = S.Rxh[i] = S.Ryl[i] = 0.0;
+    for (int e = 0; e < NP; ++e) S.Rw[i][e] = T(0);
+    S.Re[i] = S.Rxl[i] = S.Rxh[i] = S.Ryl[i] = T(0);
   }
   const double e0 = 1.0 - B.lr;                          // diagonal shift: 1 - Re Lambda
   double dB = 0.0;                                       // Dirichlet boundary faces (paper mode)
@@ -256,9 +257,9 @@ __device__ __forceinline__ void waver_block(const WBlk& B, const double* __restr
   WRRow nxt;
   waver_load<CPLX, GEN, VIRT>(B, what, g, sl, x, colin, tau0, nxt);
   for (int tau = tau0; tau < tau1; tau += 3) {
-    waver_step<NT, NS, CPLX, GEN, VIRT, 0>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau, tau1, e0, dB, nxt);
-    waver_step<NT, NS, CPLX, GEN, VIRT, 1>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 1, tau1, e0, dB, nxt);
-    waver_step<NT, NS, CPLX, GEN, VIRT, 2>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 2, tau1, e0, dB, nxt);
+    waver_step<NT, NS, CPLX, GEN, VIRT, 0, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau, tau1, e0, dB, nxt);
+    waver_step<NT, NS, CPLX, GEN, VIRT, 1, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 1, tau1, e0, dB, nxt);
+    waver_step<NT, NS, CPLX, GEN, VIRT, 2, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 2, tau1, e0, dB, nxt);
   }
 }
 
@@ -275,15 +276,16 @@ struct WROne {
 };
 
 // Shared memory: the x-exchange rows [2 buffers][NS levels][planes][NT + 2].
-template <int NT>
-constexpr size_t waver_smem(int ns, int np) { return (size_t)2 * ns * np * (NT + 2) * sizeof(double); }
+template <int NT, typename T>
+constexpr size_t waver_smem(int ns, int np) { return (size_t)2 * ns * np * (NT + 2) * sizeof(T); }
 
-template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT>
+template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
 __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_constant__ WROne P,
                                                             const double* __restrict__ what,
                                                             const IterState* st, WSlab sl) {
   if (st && st->done) return;
-  extern __shared__ __align__(16) double wsm[];
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  T* wsm = reinterpret_cast<T*>(wsm_raw);
   const WBlk& B = P.b;
   const int t = threadIdx.x;
   // x-halo of NS columns per side: a wrong edge value reaches one column further per level
@@ -300,207 +302,8 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   constexpr int XW = NT + 2;
   constexpr int NROW = 2 * NS * (CPLX ? 2 : 1);
   for (int k = t; k < NROW; k += NT) {
-    wsm[k * XW] = 0.0;
-    wsm[k * XW + XW - 1] = 0.0;
+    wsm[k * XW] = T(0);
+    wsm[k * XW + XW - 1] = T(0);
   }
-  waver_block<NT, NS, CPLX, GEN, VIRT>(B, what, g, sl, wsm, t, x, colin, colout, y0, y1);
-}
-
-// ------------------------------------------------------------------------------------------
-// Two warp roles per CTA (ns >= 5): the 255 registers a thread needs to hold all 8 levels of a
-// complex block cap the SM at 2 CTAs = 8 warps, and the wavefront is then latency-bound (ncu:
-// "wait" and long-scoreboard stalls, issue 31% with one warp per SMSP). Here warps 0..NT/32-1
-// (role A) run levels 1..NA and warps NT/32.. (role B) levels NA+1..ns of the SAME columns,
-// each with half the register state, so twice as many warps fit. B lags A by one step: A's
-// level NA at step tau works on row tau - NA and hands (L_NA, L_NA+1 and the row's operands)
-// over through shared memory; B's level i works on row tau - i - 1 at step tau + 1, so A and B
-// never wait on each other inside a step (one barrier per step, double-buffered hand-off).
-template <int NL, int NP>
-struct WR2State {                  // one role: levels j = 1..NL; index 0 = the level below
-  double L[NL + 1][3][NP];
-  double Rw[NL + 1][NP], Re[NL + 1], Rxl[NL + 1], Rxh[NL + 1], Ryl[NL + 1];
-};
-
-constexpr int WR2_HV = 10;         // hand-off values per column: c0 c1 o0 o1 w0 w1 e xl xh yl
-
-template <int NT, int NS, int NA, bool ROLEB, bool CPLX, bool GEN, bool VIRT, int PH>
-__device__ __forceinline__ void waver2_step(WR2State<ROLEB ? NS - NA : NA, CPLX ? 2 : 1>& S, const WBlk& B,
-                                            const double* __restrict__ what, const Geo& g, const WSlab& sl,
-                                            double* xch, double* hand, int t, int x, bool colin, bool colout,
-                                            int y0, int y1, int tau, int tau1, double e0, double dB,
-                                            WRRow& nxt) {
-  constexpr int NL = ROLEB ? NS - NA : NA;
-  constexpr int I0 = ROLEB ? NA + 1 : 1;                 // global level of j = 1
-  constexpr int XW = WRGeom<NT>::XW;
-  constexpr int NP = CPLX ? 2 : 1;
-  constexpr int S0 = WSlot<PH, 0>::v, S1 = WSlot<PH, 1>::v, S2 = WSlot<PH, 2>::v;
-  double* xb = xch + (tau & 1) * (NL * NP * XW) + 1 + t;
-  // (1) publish this role's newest rows for the x-neighbours
-#pragma unroll
-  for (int j = 1; j <= NL; ++j)
-#pragma unroll
-    for (int e = 0; e < NP; ++e) xb[((j - 1) * NP + e) * XW] = S.L[j][S1][e];
-  // (2) rows move one level down
-#pragma unroll
-  for (int j = NL; j >= 1; --j) {
-#pragma unroll
-    for (int e = 0; e < NP; ++e) S.Rw[j][e] = S.Rw[j - 1][e];
-    S.Re[j] = S.Re[j - 1];
-    S.Rxl[j] = S.Rxl[j - 1];
-    S.Rxh[j] = S.Rxh[j - 1];
-    S.Ryl[j] = S.Ryl[j - 1];
-  }
-  if constexpr (!ROLEB) {                                // A: row tau enters from memory
-    const WRRow cur = nxt;
-    if (tau + 1 < tau1) waver_load<CPLX, GEN, VIRT>(B, what, g, sl, x, colin, tau + 1, nxt);
-    S.Rw[0][0] = cur.w0;
-    if (CPLX) S.Rw[0][1] = cur.w1;
-    S.Rxl[0] = cur.xl;
-    S.Rxh[0] = cur.xh;
-    S.Ryl[0] = cur.yl;
-    double dd = dB;
-    if (GEN && g.dir) {
-      const int rg = tau + sl.lo;
-      dd += g.bdy * ((rg == 0) + (rg == sl.nyg - 1));
-    }
-    S.Re[0] = ((e0 + dd) + (cur.xl + cur.xh)) + (cur.yl + cur.yh);
-    if constexpr (VIRT) {                                // x_0 = 0, x_1 = w / theta
-      S.L[1][S0][0] = B.sr * cur.w0 - B.si * cur.w1;
-      if (CPLX) S.L[1][S0][1] = B.sr * cur.w1 + B.si * cur.w0;
-    } else {
-      S.L[1][S0][0] = cur.s0;
-      S.L[0][S0][0] = cur.m0;
-      if (CPLX) {
-        S.L[1][S0][1] = cur.s1;
-        S.L[0][S0][1] = cur.m1;
-      }
-    }
-  }
-  __syncthreads();
-  if constexpr (ROLEB) {                                 // B: row tau - NA - 1 enters from A
-    const double* hb = hand + ((tau - 1) & 1) * (WR2_HV * NT) + t;
-#pragma unroll
-    for (int e = 0; e < NP; ++e) {
-      S.L[0][S0][e] = hb[e * NT];                        // L_NA
-      S.L[1][S0][e] = hb[(2 + e) * NT];                  // L_NA+1
-      S.Rw[0][e] = hb[(4 + e) * NT];
-    }
-    S.Re[0] = hb[6 * NT];
-    S.Rxl[0] = hb[7 * NT];
-    S.Rxh[0] = hb[8 * NT];
-    S.Ryl[0] = hb[9 * NT];
-  }
-  // (3) levels
-  const double li = B.li;
-#pragma unroll
-  for (int j = 1; j <= NL; ++j) {
-    constexpr int e1 = CPLX ? 1 : 0;
-    const int i = I0 + j - 1;
-    const double* xr = xb + ((j - 1) * NP) * XW;
-    const bool zero_m = !ROLEB && VIRT && j == 1;        // x_0 = 0
-    double o0, o1;
-    wr_level<CPLX>(S.L[j][S1][0], S.L[j][S1][e1], S.L[j][S0][0], S.L[j][S0][e1], S.L[j][S2][0], S.L[j][S2][e1],
-                   zero_m ? 0.0 : (j == 1 ? S.L[0][S1][0] : S.L[j - 1][S2][0]),
-                   zero_m ? 0.0 : (j == 1 ? S.L[0][S1][e1] : S.L[j - 1][S2][e1]),
-                   xr[-1], CPLX ? xr[XW - 1] : 0.0, xr[1], CPLX ? xr[XW + 1] : 0.0,
-                   S.Rw[j][0], S.Rw[j][e1], S.Re[j], S.Rxl[j], S.Rxh[j], S.Ryl[j], S.Ryl[j - 1], li,
-                   B.ar[i - 1], CPLX ? B.ai[i - 1] : 0.0, B.br[i - 1], CPLX ? B.bi[i - 1] : 0.0, o0, o1);
-    if (j < NL) {                                        // push: overwrites the oldest row
-      S.L[j + 1][S0][0] = o0;
-      if (CPLX) S.L[j + 1][S0][1] = o1;
-    } else if constexpr (!ROLEB) {                       // A: hand row tau - NA over to B
-      double* hw = hand + (tau & 1) * (WR2_HV * NT) + t;
-#pragma unroll
-      for (int e = 0; e < NP; ++e) {
-        hw[e * NT] = S.L[j][S1][e];
-        hw[(4 + e) * NT] = S.Rw[j][e];
-      }
-      hw[2 * NT] = o0;
-      if (CPLX) hw[3 * NT] = o1;
-      hw[6 * NT] = S.Re[j];
-      hw[7 * NT] = S.Rxl[j];
-      hw[8 * NT] = S.Rxh[j];
-      hw[9 * NT] = S.Ryl[j];
-    } else {                                             // B: the result, row tau - ns - 1
-      const int r = tau - NS - 1;
-      if (colout && r >= y0 && r < y1) {
-        const long long p = (long long)r * g.nx + x;
-        B.out_last[p] = o0;
-        if (CPLX) B.out_last[g.N + p] = o1;
-        if (B.out_prev) {                                // L_ns at row r (age 1)
-          B.out_prev[p] = S.L[j][S1][0];
-          if (CPLX) B.out_prev[g.N + p] = S.L[j][S1][1];
-        }
-      }
-    }
-  }
-}
-
-template <int NT, int NS, int NA, bool ROLEB, bool CPLX, bool GEN, bool VIRT>
-__device__ __forceinline__ void waver2_role(const WBlk& B, const double* __restrict__ what, const Geo& g,
-                                            const WSlab& sl, double* xch, double* hand, int t, int x,
-                                            bool colin, bool colout, int y0, int y1) {
-  constexpr int NL = ROLEB ? NS - NA : NA;
-  constexpr int NP = CPLX ? 2 : 1;
-  WR2State<NL, NP> S;
-#pragma unroll
-  for (int j = 0; j <= NL; ++j) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int e = 0; e < NP; ++e) S.L[j][a][e] = 0.0;
-#pragma unroll
-    for (int e = 0; e < NP; ++e) S.Rw[j][e] = 0.0;
-    S.Re[j] = S.Rxl[j] = S.Rxh[j] = S.Ryl[j] = 0.0;
-  }
-  const double e0 = 1.0 - B.lr;
-  double dB = 0.0;
-  if (GEN && g.dir) dB = g.bdx * ((x == 0) + (x == g.nx - 1));
-  const int tau0 = y0 - NS, tau1 = y1 + NS + 1;          // (+1: B lags one step)
-  WRRow nxt;
-  if constexpr (!ROLEB) waver_load<CPLX, GEN, VIRT>(B, what, g, sl, x, colin, tau0, nxt);
-  for (int tau = tau0; tau < tau1; tau += 3) {
-    waver2_step<NT, NS, NA, ROLEB, CPLX, GEN, VIRT, 0>(S, B, what, g, sl, xch, hand, t, x, colin, colout, y0, y1, tau, tau1, e0, dB, nxt);
-    waver2_step<NT, NS, NA, ROLEB, CPLX, GEN, VIRT, 1>(S, B, what, g, sl, xch, hand, t, x, colin, colout, y0, y1, tau + 1, tau1, e0, dB, nxt);
-    waver2_step<NT, NS, NA, ROLEB, CPLX, GEN, VIRT, 2>(S, B, what, g, sl, xch, hand, t, x, colin, colout, y0, y1, tau + 2, tau1, e0, dB, nxt);
-  }
-}
-
-// Shared memory: A's and B's x-exchange rows, then the hand-off [2][WR2_HV][NT].
-template <int NT>
-constexpr size_t waver2_smem(int ns, int np) {
-  return ((size_t)2 * ns * np * (NT + 2) + (size_t)2 * WR2_HV * NT) * sizeof(double);
-}
-
-template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT>
-__global__ void __launch_bounds__(2 * NT, 2) k_waver2(Geo g, const __grid_constant__ WROne P,
-                                                      const double* __restrict__ what,
-                                                      const IterState* st, WSlab sl) {
-  static_assert(NS >= 2, "two roles need two levels");
-  if (st && st->done) return;
-  extern __shared__ __align__(16) double wsm[];
-  constexpr int NA = (NS + 1) / 2;
-  constexpr int NP = CPLX ? 2 : 1;
-  constexpr int XW = NT + 2;
-  const WBlk& B = P.b;
-  const bool roleb = threadIdx.x >= NT;
-  const int t = threadIdx.x - (roleb ? NT : 0);
-  constexpr int TX = NT - 2 * H;
-  const int strip = (int)blockIdx.x % P.nstrip, chunk = (int)blockIdx.x / P.nstrip;
-  const int x = strip * TX - H + t;
-  const bool colin = x >= 0 && x < g.nx;
-  const bool colout = t >= H && t < NT - H && x < g.nx;
-  const int y0 = chunk * P.ly;
-  const int y1 = min(y0 + P.ly, g.ny);
-  double* xa = wsm;                                      // [2][NA][NP][XW]
-  double* xbb = wsm + 2 * NA * NP * XW;                  // [2][NS-NA][NP][XW]
-  double* hand = wsm + 2 * NS * NP * XW;                 // [2][WR2_HV][NT]
-  for (int k = threadIdx.x; k < 2 * NS * NP; k += 2 * NT) {   // zero pads of the exchange rows
-    wsm[k * XW] = 0.0;
-    wsm[k * XW + XW - 1] = 0.0;
-  }
-  for (int k = threadIdx.x; k < 2 * WR2_HV * NT; k += 2 * NT) hand[k] = 0.0;
-  __syncthreads();
-  if (roleb) waver2_role<NT, NS, NA, true, CPLX, GEN, VIRT>(B, what, g, sl, xbb, hand, t, x, colin, colout, y0, y1);
-  else waver2_role<NT, NS, NA, false, CPLX, GEN, VIRT>(B, what, g, sl, xa, hand, t, x, colin, colout, y0, y1);
+  waver_block<NT, NS, CPLX, GEN, VIRT, T>(B, what, g, sl, wsm, t, x, colin, colout, y0, y1);
 }

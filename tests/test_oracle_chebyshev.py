@@ -15,6 +15,7 @@ import numpy as np
 import numpy.polynomial.chebyshev as npch
 import pytest
 
+import synth
 from oracle import chebyshev as ch
 from oracle import circulant as circ
 from oracle import operator as op
@@ -201,3 +202,19 @@ def test_paper_nc1_golden_is_self_consistent():
                 nx = int(key) if tab == "table3" else T["nx"]
                 for eta, (its, mv) in zip(T["eta"], cells):
                     assert its * (ell + ell * round(nx * eta)) == mv, (tab, a, key, eta)
+
+
+@pytest.mark.parametrize("method,k", [("nc1", 6), ("nc2", 8)])
+def test_nc_apply_f32_is_nc_apply_to_single_precision(method, k):
+    """The mixed-precision variant (fp32 recurrence) agrees with the fp64 nc_apply to fp32
+    rounding (unit 6e-8) amplified by at most kappa(Gamma_alpha) through the inverse transform
+    (reading R18), and is NOT bit-identical (it is fp32)."""
+    p = synth.make_problem("headline", shape=(1, 20, 17))
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    r = np.random.default_rng(8).standard_normal((p.ell,) + p.shape)
+    z64 = ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)
+    z32 = ch.nc_apply_f32(w, r, p.ell, p.alpha, 1.0, mu, al)
+    e = np.linalg.norm(z32 - z64) / np.linalg.norm(z64)
+    assert 1e-9 < e < 6e-8 * circ.gamma_condition(p.ell, p.alpha)
