@@ -153,8 +153,21 @@ static int comm_wait_event(aac_ctx* ctx, cudaEvent_t ev) {
   }
 }
 
-// cudaStreamSynchronize of the library stream with the same watch (NCCL contexts).
-static int comm_sync(aac_ctx* ctx) {
+// Profiling only: keep the library stream busy for `ns` nanoseconds (globaltimer) so that the
+// host enqueues the next launches, with their timing events, before the GPU reaches them --
+// otherwise the first event pair after a host sync measures the host's enqueue latency too.
+__global__ void k_prof_hold(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+// cudaStreamSynchronize of the library stream with the same watch (NCCL contexts). In profile
+// mode the stream is then held for 400 us (k_prof_hold; not counted as a launch).
+static int comm_sync_impl(aac_ctx* ctx) {
   if (!ctx->nccl_comm) {
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return AAC_OK;
@@ -162,6 +175,11 @@ static int comm_sync(aac_ctx* ctx) {
   if (!ctx->ev_sync) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_sync, cudaEventDisableTiming));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_sync, ctx->stream));
   return comm_wait_event(ctx, ctx->ev_sync);
+}
+static int comm_sync(aac_ctx* ctx) {
+  AAC_TRY(comm_sync_impl(ctx));
+  if (ctx->prof) k_prof_hold<<<1, 1, 0, ctx->stream>>>(400000ULL);
+  return AAC_OK;
 }
 
 // In-place all-reduce of n doubles on the context stream (no-op on one rank).

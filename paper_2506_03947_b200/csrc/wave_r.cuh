@@ -21,6 +21,20 @@
 
 #include "wave.cuh"
 
+#ifndef WR_PAIRX
+#define WR_PAIRX 1                                      // -DWR_PAIRX=0: one exchange row per plane
+#endif
+
+template <typename T> struct WRVec;
+template <> struct WRVec<double> {
+  using T2 = double2;
+  static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+template <> struct WRVec<float> {
+  using T2 = float2;
+  static __device__ __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+
 template <int NT>
 struct WRGeom {
   static constexpr int XW = NT + 2;                     // exchange row: zero pad at both ends
@@ -152,12 +166,21 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
   constexpr int NP = CPLX ? 2 : 1;
   constexpr int S0 = WSlot<PH, 0>::v, S1 = WSlot<PH, 1>::v, S2 = WSlot<PH, 2>::v;
   T* xb = xch + (tau & 1) * (NS * NP * XW) + 1 + t;
+  // complex blocks: the (Re, Im) pair of a column is one 2-vector in the exchange rows (one
+  // STS.128 + two LDS.128 per level instead of two STS.64 + four LDS.64)
+  using T2 = typename WRVec<T>::T2;
+  T2* xb2 = reinterpret_cast<T2*>(xch) + (tau & 1) * (NS * XW) + 1 + t;
   // (1) publish the newest row of every level (L_i at row tau - i; age 1 after this step's
   //     push) for the x-neighbours
 #pragma unroll
-  for (int i = 1; i <= NS; ++i)
+  for (int i = 1; i <= NS; ++i) {
+    if constexpr (CPLX && WR_PAIRX) {
+      xb2[(i - 1) * XW] = WRVec<T>::make(S.L[i][S1][0], S.L[i][S1][1]);
+    } else {
 #pragma unroll
-    for (int e = 0; e < NP; ++e) xb[((i - 1) * NP + e) * XW] = S.L[i][S1][e];
+      for (int e = 0; e < NP; ++e) xb[((i - 1) * NP + e) * XW] = S.L[i][S1][e];
+    }
+  }
   // (2) rows move one level down; row tau enters (L_0, L_1 and its operands)
 #pragma unroll
   for (int i = NS; i >= 1; --i) {
@@ -204,11 +227,18 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
   for (int i = 1; i <= NS; ++i) {
     const T* xr = xb + ((i - 1) * NP) * XW;
     const int e1 = CPLX ? 1 : 0;
+    T nl0, nl1, nr0, nr1;                                // x-neighbours (left, right)
+    if constexpr (CPLX && WR_PAIRX) {
+      const T2 a = xb2[(i - 1) * XW - 1], b = xb2[(i - 1) * XW + 1];
+      nl0 = a.x; nl1 = a.y; nr0 = b.x; nr1 = b.y;
+    } else {
+      nl0 = xr[-1]; nl1 = CPLX ? xr[XW - 1] : T(0); nr0 = xr[1]; nr1 = CPLX ? xr[XW + 1] : T(0);
+    }
     T o0, o1;
     wr_level<CPLX, T>(S.L[i][S1][0], S.L[i][S1][e1], S.L[i][S0][0], S.L[i][S0][e1], S.L[i][S2][0], S.L[i][S2][e1],
                       i == 1 ? (VIRT ? T(0) : S.L[0][S1][0]) : S.L[i - 1][S2][0],
                       i == 1 ? (VIRT ? T(0) : S.L[0][S1][e1]) : S.L[i - 1][S2][e1],
-                      xr[-1], CPLX ? xr[XW - 1] : T(0), xr[1], CPLX ? xr[XW + 1] : T(0),
+                      nl0, nl1, nr0, nr1,
                       S.Rw[i][0], S.Rw[i][e1], S.Re[i], S.Rxl[i], S.Rxh[i], S.Ryl[i], S.Ryl[i - 1], li,
                       T(B.ar[i - 1]), CPLX ? T(B.ai[i - 1]) : T(0), T(B.br[i - 1]), CPLX ? T(B.bi[i - 1]) : T(0),
                       o0, o1);
@@ -300,10 +330,19 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   const int y1 = min(y0 + P.ly, g.ny);
   // zero pads of the exchange rows (never written)
   constexpr int XW = NT + 2;
-  constexpr int NROW = 2 * NS * (CPLX ? 2 : 1);
-  for (int k = t; k < NROW; k += NT) {
-    wsm[k * XW] = T(0);
-    wsm[k * XW + XW - 1] = T(0);
+  if constexpr (CPLX && WR_PAIRX) {                     // rows of XW (Re, Im) pairs
+    using T2 = typename WRVec<T>::T2;
+    T2* w2 = reinterpret_cast<T2*>(wsm);
+    for (int k = t; k < 2 * NS; k += NT) {
+      w2[k * XW] = WRVec<T>::make(T(0), T(0));
+      w2[k * XW + XW - 1] = WRVec<T>::make(T(0), T(0));
+    }
+  } else {
+    constexpr int NROW = 2 * NS * (CPLX ? 2 : 1);
+    for (int k = t; k < NROW; k += NT) {
+      wsm[k * XW] = T(0);
+      wsm[k * XW + XW - 1] = T(0);
+    }
   }
   waver_block<NT, NS, CPLX, GEN, VIRT, T>(B, what, g, sl, wsm, t, x, colin, colout, y0, y1);
 }
