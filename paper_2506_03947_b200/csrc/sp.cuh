@@ -61,6 +61,11 @@ struct SpLevel {               // one multigrid level (device arrays)
   long long goff = 0;          // ... and its offset in the global arrays (points)
 };
 
+struct SpfRed {               // two-level reduction of the fused kernels (sp_fused.cuh):
+  double* gpart;               // group partials [nq][ngroups]
+  unsigned* gtick;             // group tickets (SPF_TICK_STRIDE apart), then the global one
+};
+
 struct SpPlan {
   int ell = 0, h = 0;
   std::vector<SpLevel> lev;
@@ -77,6 +82,7 @@ struct SpPlan {
   double* part = nullptr;      // partials [planes or blocks][tiles]
   unsigned* tick = nullptr;
   double* red = nullptr;       // multi-rank: local sums for the all-reduce (AAC_MAX_ELL)
+  SpfRed red2{};               // two-level reduction workspace of the fused kernels (sp_fused.cuh)
   int gather = -1;             // multi-rank: index of the gathered (first global) level
 };
 
@@ -200,7 +206,7 @@ __device__ __forceinline__ void sp_reduce(const SpStepCtx& S, double v, bool ste
   const int ntile = gridDim.x;
   if (t == 0) {
     double s = 0.0;
-    for (int w = 0; w < SP_T / 32; ++w) s += red[w];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
     S.part[(long long)blockIdx.y * ntile + blockIdx.x] = s;
     __threadfence();
     const unsigned tk = atomicAdd(S.tick, 1u);
@@ -347,7 +353,7 @@ __device__ __forceinline__ void sp_reduce_pair(const SpStepCtx& S, double va, do
   const int ntile = gridDim.x;
   if (t == 0) {
     double sa = 0.0, sb = 0.0;
-    for (int w = 0; w < SP_T / 32; ++w) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {     // (<= SP_T threads)
       sa += red[0][w];
       sb += red[1][w];
     }
@@ -921,6 +927,25 @@ __global__ void __launch_bounds__(SP_T) k_sp_upd2(long long N, int ell, SpVec v,
   }
 }
 
+// Real planes of K3 alone (the complex planes' update is formed inside the fused level-0
+// restriction, sp_fused.cuh): X += alpha P, R -= alpha Q for planes 0 and ell - 1.
+__global__ void __launch_bounds__(SP_T) k_sp_upd1_real(long long N, int ell, SpVec v, const SpBlk* blk,
+                                                       const IterState* st) {
+  if (st && st->done) return;
+  const int pl = blockIdx.y == 0 ? 0 : ell - 1, kb = sp_block_of(ell, pl);
+  const SpBlk& b = blk[kb];
+  if (b.stop == 1) return;
+  const double alpha = b.alpha;
+  const long long o0 = (long long)pl * N;
+  for (long long p = (long long)blockIdx.x * SP_T + threadIdx.x; p < N; p += (long long)gridDim.x * SP_T) {
+    const long long o = o0 + p;
+    v.X[o] = fma(alpha, v.P[o], v.X[o]);
+    v.R[o] = fma(-alpha, v.SZ[o], v.R[o]);
+  }
+}
+
+#include "sp_fused.cuh"
+
 // ------------------------------------------------------------------------------------------
 // host side
 static int sp_alloc(aac_ctx* ctx, SpPlan* P, double** p, long long n) {
@@ -1256,8 +1281,22 @@ static int sp_prepare_impl(aac_ctx* ctx, int k) {
   AAC_TRY(sp_alloc(ctx, P, &blk, (long long)(h + 1) * (sizeof(SpBlk) / sizeof(double) + 1)));
   P->blk = reinterpret_cast<SpBlk*>(blk);
   CUDA_TRY(ctx, cudaMemset(P->blk, 0, (h + 1) * sizeof(SpBlk)));
-  const long long ntile = (N + SP_T - 1) / SP_T;
+  long long ntile = (N + SP_T - 1) / SP_T;
+  if (P->lev.size() > 1) {                      // the fused level-0 kernels' tiles (sp_fused.cuh)
+    int nsx, nt;
+    spf_tiles(P->lev[1].g.nx, P->lev[1].g.ny, nsx, nt);
+    ntile = std::max<long long>(ntile, nt);
+  }
   AAC_TRY(sp_alloc(ctx, P, &P->part, ntile * ell + 8));
+  {                                             // fused kernels: group partials and tickets
+    const long long ng = (ntile + SPF_GROUP - 1) / SPF_GROUP;
+    AAC_TRY(sp_alloc(ctx, P, &P->red2.gpart, ng * ell + 8));
+    double* gt = nullptr;
+    const long long nticks = (ng + 1) * SPF_TICK_STRIDE;
+    AAC_TRY(sp_alloc(ctx, P, &gt, (nticks + 1) / 2));
+    CUDA_TRY(ctx, cudaMemset(gt, 0, (size_t)nticks * sizeof(unsigned)));
+    P->red2.gtick = reinterpret_cast<unsigned*>(gt);
+  }
   double* tk = nullptr;
   AAC_TRY(sp_alloc(ctx, P, &tk, 1));
   P->tick = reinterpret_cast<unsigned*>(tk);
@@ -1283,11 +1322,25 @@ static int sp_halo(aac_ctx* ctx, const Geo& g, const double* x) {
 // stencil); the restriction into the gathered level writes this rank's rows of the zeroed
 // global right-hand side, which an all-reduce completes on every rank; the global levels run
 // redundantly and the prolongation back reads this rank's rows of their result.
+// CTAs per SM of the fused kernels that reduce (AAC_SPF_CPS overrides; measured: 4).
+static int spf_cps() {
+  static const int v = getenv("AAC_SPF_CPS") ? atoi(getenv("AAC_SPF_CPS")) : 4;
+  return std::max(1, v);
+}
+
+// The fused 2D level kernels (sp_fused.cuh) run on one rank; AAC_SP_FUSED=0 selects the
+// per-step kernels (smoothing, restriction, prolongation + post-smoothing).
+static bool sp_fused_on(const aac_ctx* ctx, int dim) {
+  static const bool off = getenv("AAC_SP_FUSED") && atoi(getenv("AAC_SP_FUSED")) == 0;
+  return dim == 2 && ctx->nranks == 1 && !off;
+}
+
 template <int DIM>
-static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
+static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U = SpfUpd{}) {
   SpPlan* P = ctx->sp;
   const int ell = P->ell;
   const int nl = (int)P->lev.size();
+  const bool fused = sp_fused_on(ctx, DIM);
   const IterState* st = S.st;
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ell * ctx->geo.S;
@@ -1310,6 +1363,21 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     const bool gat = a.local && !c.local;                  // restriction into the gathered level
     const Geo& gcl = gat ? c.gl : c.g;                     // this rank's part of the coarse level
     const dim3 gf(grid1d(a.g.N, SP_T), ell), gc(grid1d(gcl.N, SP_T), ell);
+    if (fused) {                                           // smoothing + restriction in one pass
+      int nsx, nt;
+      spf_tiles(c.g.nx, c.g.ny, nsx, nt);
+      const SpfUpd u = l == 0 ? U : SpfUpd{};
+      // compulsory bytes: b (or the update operands + v_{j+1}), 1/D per block, wx, wy, cnt, b_c
+      const double nb = u.on ? (4.0 * (ell - 2) + 2.0) : (double)ell;
+      const double bytes = 8.0 * a.g.N * (nb + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
+      if (a.g.nx % 2 == 0)
+        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_restrict<true><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+                                          a.g, c.g, a.cnt, a.dinv, P->K, io, bl, c.b, u, nsx, st));
+      else
+        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_restrict<false><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+                                          a.g, c.g, a.cnt, a.dinv, P->K, io, bl, c.b, u, nsx, st));
+      continue;
+    }
     LAUNCH(ctx, KID_SP_MG, 16.0 * ell * a.g.N,
            k_mg_smooth0<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, a.dinv, P->K, io, bl, a.x, st));
     if (a.local) AAC_TRY(sp_halo(ctx, a.g, a.x));
@@ -1355,6 +1423,21 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S) {
     const bool gat = a.local && !c.local;
     const dim3 gf(grid1d(a.g.N, SP_T), ell);
     const dim3 gp(l == 0 ? std::min<unsigned>(gf.x, std::max(1, 8 * ctx->num_sms / ell)) : gf.x, ell);
+    if (fused) {
+      int nsx, nt;
+      spf_tiles(c.g.nx, c.g.ny, nsx, nt);
+      // level 0 (dot partials): grid-stride, ~SPF_CPS CTAs per SM -- the per-CTA fence and ticket
+      // of the reduction made one row pair per CTA (10 240 CTAs) 1.4x slower
+      if (l == 0) nt = nsx * std::min(c.g.ny, std::max(1, spf_cps() * ctx->num_sms / (nsx * (ell / 2))));
+      const double bytes = 8.0 * a.g.N * (2.0 * ell + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
+      if (a.g.nx % 2 == 0)
+        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_prolong_post<true><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+                                          a.g, c.g, a.cnt, a.dinv, io, bl, c.x2, a.x2, S, P->red2, l == 0 ? 1 : 0, nsx));
+      else
+        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_prolong_post<false><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+                                          a.g, c.g, a.cnt, a.dinv, io, bl, c.x2, a.x2, S, P->red2, l == 0 ? 1 : 0, nsx));
+      continue;
+    }
     if (ctx->nranks > 1 && a.local) {                      // slab level: prolong, halo, post
       LAUNCH(ctx, KID_SP_MG, 24.0 * ell * a.g.N,
              k_mg_prolong<DIM><<<gf, SP_T, 0, ctx->stream>>>(a.g, gat ? c.gl : c.g, a.x, c.x2, st, c.g.N,
@@ -1442,7 +1525,16 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     }
     static const bool no_row2d = getenv("AAC_SP_ROW2D") && atoi(getenv("AAC_SP_ROW2D")) == 0;
     const unsigned gsa = std::min<unsigned>(gt, std::max(1, 8 * ctx->num_sms / (h + 1)));
-    if (DIM == 2 && !no_row2d)
+    if (sp_fused_on(ctx, DIM)) {
+      const int nsx = ((ctx->geo.nx + 1) / 2 + SPF_T - 1) / SPF_T, nyp = (ctx->geo.ny + 1) / 2;
+      const int nry = std::min(nyp, std::max(1, spf_cps() * ctx->num_sms / (nsx * h)));
+      if (ctx->geo.nx % 2 == 0)
+        LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+               k_spf_apply<true><<<dim3(nsx * nry, h), SPF_T, 0, ctx->stream>>>(ctx->geo, vecs(), S, P->red2, nsx));
+      else
+        LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+               k_spf_apply<false><<<dim3(nsx * nry, h), SPF_T, 0, ctx->stream>>>(ctx->geo, vecs(), S, P->red2, nsx));
+    } else if (DIM == 2 && !no_row2d)
       LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
              k_sp_apply2<<<dim3(std::min<unsigned>(gsa, (unsigned)ctx->geo.ny), h + 1), SP_T, 0, ctx->stream>>>(
                  ctx->geo, vecs(), S));
@@ -1454,10 +1546,18 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     // took the saddle solve from 64.8 to 63.3 ms; a full one-element-per-thread grid was slower)
     static const int upd_env = getenv("AAC_SP_UPD_CAP") ? atoi(getenv("AAC_SP_UPD_CAP")) : 0;
     const unsigned upd_cap = upd_env > 0 ? (unsigned)upd_env : (unsigned)(4 * ctx->num_sms);
-    LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
-           k_sp_upd1<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(
-               N, ell, vecs(), P->blk, st));
-    AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
+    if (sp_fused_on(ctx, DIM)) {
+      // complex planes: v_{j+1} formed inside the level-0 restriction; real planes here
+      LAUNCH(ctx, KID_SP_VEC, 3.0 * V * 2 / ell,
+             k_sp_upd1_real<<<dim3(std::min<unsigned>(gt, upd_cap), 2), SP_T, 0, ctx->stream>>>(
+                 N, ell, vecs(), P->blk, st));
+      AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S, SpfUpd{P->SZ, Vc, Vp, P->blk, 1}));
+    } else {
+      LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
+             k_sp_upd1<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(
+                 N, ell, vecs(), P->blk, st));
+      AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S));
+    }
     AAC_TRY(finish(ell, 1));
     LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
            k_sp_upd2<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(

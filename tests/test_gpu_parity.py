@@ -327,6 +327,9 @@ SP_CASES = [
     ("2d256", dict(shape=(1, 24, 20), ell=12, alpha=0.3), 5),
     ("1d", {}, 4),
     ("3d", dict(shape=(12, 10, 9), ell=6), 3),
+    # several strips / row chunks of the fused 2D level kernels (sp_fused.cuh), odd and even nx
+    ("saddle", dict(shape=(1, 261, 517), ell=4, alpha=1e-2), 3),
+    ("saddle", dict(shape=(1, 200, 600), ell=6), 2),
 ]
 
 
@@ -361,10 +364,11 @@ print("ok", e)
 """
 
 
-@pytest.mark.parametrize("env", [dict(AAC_SP_ROW2D="0"), dict(AAC_SP_PAIR="0"), dict(AAC_SP_TAIL="0")])
+@pytest.mark.parametrize("env", [dict(AAC_SP_ROW2D="0", AAC_SP_FUSED="0"), dict(AAC_SP_PAIR="0", AAC_SP_FUSED="0"),
+                                 dict(AAC_SP_TAIL="0"), dict(AAC_SP_FUSED="0")])
 def test_sp_kernel_variants_parity(env):
     """The non-default SP kernel organisations (generic flat-index kernels in 2D, one plane per
-    CTA, no fused coarse tail) against the oracle on a ragged grid. A fresh process each: the
+    CTA, no fused coarse tail, the per-step level kernels instead of the fused ones) against the oracle on a ragged grid. A fresh process each: the
     library reads these switches once per process."""
     import subprocess
     import sys
