@@ -19,6 +19,7 @@
 #include "wave.cuh"
 #include "wave_r.cuh"
 #include "stencil.cuh"
+#include "stencil_tile.cuh"
 
 // saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
 static int sp_prepare(aac_ctx* ctx, int k);
@@ -478,9 +479,43 @@ static inline bool vec2(const aac_ctx* ctx) {
 
 // ------------------------------------------------------------------------------------------
 // calA apply
+// TMA-staged tile kernel (stencil_tile.cuh) on 2D one-rank Neumann grids with even nx, selected by
+// AAC_MATVEC_TILE=1 (measured slower at the headline: 48.5 us against 33.5 us for k_matvec,
+// ncu, cold L2 -- k_matvec's neighbour re-reads hit L1/L2, so staging saves no DRAM bytes, and
+// the one-thread row-copy ring of 2 CTAs per SM keeps too few bytes in flight).
+// x = xbase + j * xjs (j on the device if jdev).
+static bool matvec_tile_on(const aac_ctx* ctx) {
+  static const bool on = getenv("AAC_MATVEC_TILE") && atoi(getenv("AAC_MATVEC_TILE")) == 1;
+  return on && !ctx->varying && mt_ok(ctx->geo, ctx->dim, ctx->nranks);
+}
+
+template <typename K>
+static int smem_optin(aac_ctx* ctx, K kernel, size_t bytes);
+
+static int launch_matvec_tile(aac_ctx* ctx, const double* xbase, long long xjs, const int* jdev, double* y,
+                              double bytes) {
+  const Geo& g = ctx->geo;
+  MtGeo M;
+  M.ntx = (g.nx + MT_TC - 1) / MT_TC;
+  M.nty = (g.ny + MT_TR - 1) / MT_TR;
+  M.nitems = (long long)M.ntx * M.nty * ctx->ell;
+  const size_t smem = mt_smem();
+  AAC_TRY(smem_optin(ctx, k_matvec_tile, smem));
+  static thread_local int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_matvec_tile, MT_TC, smem);
+    if (occ < 1) occ = 1;
+  }
+  const long long grid = std::min<long long>(M.nitems, (long long)occ * ctx->num_sms);
+  LAUNCH(ctx, KID_MATVEC, bytes,
+         k_matvec_tile<<<(unsigned)grid, MT_TC, smem, ctx->stream>>>(g, M, ctx->ell, xbase, xjs, jdev, y));
+  return AAC_OK;
+}
+
 template <int DIM, int VEC>
 static int launch_matvec(aac_ctx* ctx, const double* x, double* y, double bytes) {
   const Geo& g = ctx->geo;
+  if (DIM == 2 && matvec_tile_on(ctx)) return launch_matvec_tile(ctx, x, 0, nullptr, y, bytes);
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
   const dim3 grid(grid1d(g.nx / VEC, 256), g.ny, g.nz);
@@ -1177,6 +1212,9 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
              ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, arnoldi_ctx(ctx)};
   if (!FUSED && ctx->varying) {      // varying blocks: each plane its own operator
     AAC_TRY(matvec_var(ctx, ctx->d_Z, L, reinterpret_cast<const int*>(ctx->d_st), ctx->d_W));
+    ctx->sweeps += ctx->ell;
+  } else if (!FUSED && DIM == 2 && matvec_tile_on(ctx)) {
+    AAC_TRY(launch_matvec_tile(ctx, ctx->d_Z, L, reinterpret_cast<const int*>(ctx->d_st), ctx->d_W, 2 * V + C));
     ctx->sweeps += ctx->ell;
   } else if (!FUSED) {               // w = calA Z_j by the stencil kernel (j read on the device)
     const bool v2 = vec2(ctx);

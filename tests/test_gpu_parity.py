@@ -48,7 +48,39 @@ CASES = [
     ("2d256", dict(n=256, alpha=1e-4)),
     ("3d", dict(shape=(9, 13, 11))),
     ("3d", dict(shape=(17, 17, 17), ell=4)),
+    # even nx, ragged 256-column / 8-row tiles of k_matvec_tile (516 = 2 x 256 + 4)
+    ("headline", dict(shape=(1, 131, 516))),
+    ("2d256", dict(shape=(1, 9, 600), ell=4)),
 ]
+
+
+_MATVEC_BITS = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth
+from paper_2506_03947_b200 import from_problem
+p = synth.make_problem("headline", shape=(1, 131, 516))
+s = from_problem(p, max_krylov=8)
+x = np.random.default_rng(7).standard_normal((p.ell,) + p.shape)
+y = s.matvec(torch.from_numpy(x.reshape(p.ell, -1)).cuda()).cpu().numpy()
+np.save({out!r}, y)
+"""
+
+
+def test_matvec_tile_bit_identical_to_register_kernel(tmp_path):
+    """k_matvec_tile (TMA-staged tiles, AAC_MATVEC_TILE=1) performs stencil_sv's operations in the
+    same order: its result equals k_matvec's (the default, a fresh process each) bit for bit."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"y{flag}.npy")
+        r = subprocess.run([sys.executable, "-c", _MATVEC_BITS.format(root=root, out=out)], capture_output=True,
+                           text=True, timeout=300, env={**os.environ, "AAC_MATVEC_TILE": flag})
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("name,kw", CASES)
