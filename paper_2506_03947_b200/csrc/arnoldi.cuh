@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
       long long k = 0;                          // item counter (ring stage / phase)
       for (long long r = 0; r < my_tiles; ++r) {
         const Tile T = tile_of(r);
-        for (int i = T.i0; i < T.i1; ++i, ++k) {
+        // V_j is not streamed: the consumers hold it in registers (u) already
+        for (int i = T.i0; i < min(T.i1, j); ++i, ++k) {
           const int s = (int)(k % AS);
           if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
           bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s]);
@@ -147,7 +148,8 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
           }
         }
       }
-      for (int i = T.i0; i < T.i1; ++i, ++k) {
+      const int ie = min(T.i1, j);                // V_i, i < j: from the ring
+      for (int i = T.i0; i < ie; ++i, ++k) {
         const int s = (int)(k % AS);
         if constexpr (TMA) mbar_wait(&full[s], (uint32_t)((k / AS) & 1));
         double sa = 0.0, ga = 0.0;
@@ -168,6 +170,21 @@ __global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams
         if (lane == 0) {
           acc[warp * nv2 + i] += sa;
           acc[warp * nv2 + nv + i] += ga;
+        }
+      }
+      if (T.i1 == nv) {                           // V_j = u, already in registers: the same
+        double sa = 0.0, ga = 0.0;                // values as streaming it, one read less
+        if (valid) {
+          FOR_PL(pl) {
+            sa = fma(u[pl], w[pl], sa);
+            ga = fma(u[pl], u[pl], ga);
+          }
+        }
+        sa = warp_sum(sa);
+        ga = warp_sum(ga);
+        if (lane == 0) {
+          acc[warp * nv2 + j] += sa;
+          acc[warp * nv2 + nv + j] += ga;
         }
       }
     }
