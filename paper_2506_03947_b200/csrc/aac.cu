@@ -349,7 +349,9 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   }
   // slab-decomposed wavefront (2D): face weights of the slab +- WAVE_MAXH rows, halo buffers
   if (ctx->nranks > 1 && g->dim == 2) {
-    const int hd = WAVE_MAXH;
+    // one row more than the deepest pass: the wavefront also produces the final iterates of the
+    // ghost rows -1 and ny, from which the step forms Z_j's halo without an exchange
+    const int hd = WAVE_MAXH + 1;
     bool thick = true;
     for (int r = 0; r < g->nranks; ++r) {
       int64_t rl, rh;
@@ -364,6 +366,7 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
       slab_weights(g, kx, ky, kz, c, elo, ehi, he, le, &gdummy);
       if (cudaMalloc((void**)&ctx->d_wext, (size_t)(le[0] + le[1]) * sizeof(double)) != cudaSuccess ||
           cudaMalloc((void**)&ctx->d_whalo, (size_t)2 * ell * hd * nx * sizeof(double)) != cudaSuccess ||
+          cudaMalloc((void**)&ctx->d_ghost, (size_t)2 * ell * nx * sizeof(double)) != cudaSuccess ||
           cudaMemcpy(ctx->d_wext, he.data(), (size_t)(le[0] + le[1]) * sizeof(double), cudaMemcpyHostToDevice) !=
               cudaSuccess ||
           cudaDeviceSynchronize() != cudaSuccess) {
@@ -414,6 +417,7 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   if (ctx->d_lam1) cudaFree(ctx->d_lam1);
   if (ctx->d_T) cudaFree(ctx->d_T);
   if (ctx->d_whalo) cudaFree(ctx->d_whalo);
+  if (ctx->d_ghost) cudaFree(ctx->d_ghost);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};
@@ -667,9 +671,9 @@ static Dft make_dft(const aac_ctx* ctx) {
 
 // z = Gamma^{-1} U y from per-block sources (streaming; one point per thread measured faster
 // than two: the per-block register arrays stay small)
-static int run_inverse(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zbase, long long zjs,
-                       const IterState* st) {
-  const long long N = ctx->geo.N;
+// The inverse transform over N points (planes N apart in source and destination).
+static int run_inverse_n(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zbase, long long zjs,
+                         const IterState* st, long long N) {
   const double V = 8.0 * ctx->ell * N;
   if (ctx->ell == 10)
     LAUNCH(ctx, KID_INV, 2 * V, k_inverse_exact<10><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
@@ -678,6 +682,11 @@ static int run_inverse(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zba
   else
     LAUNCH(ctx, KID_INV, 2 * V, k_inverse<1><<<grid1d(N, 256), 256, 0, ctx->stream>>>(N, D, F, zbase, zjs, st));
   return AAC_OK;
+}
+
+static int run_inverse(aac_ctx* ctx, const Dft& D, const NcFinal& F, double* zbase, long long zjs,
+                       const IterState* st) {
+  return run_inverse_n(ctx, D, F, zbase, zjs, st, ctx->geo.N);
 }
 
 #include "sp.cuh"
@@ -820,7 +829,7 @@ static int aux_streams(aac_ctx* ctx) {
 // fork and the join); every kernel counts in aac_launch_count.
 template <int H, int NT>
 static int waver_group(aac_ctx* ctx, const WSweep& S, int nchunk, const WSlab& sl, const IterState* st,
-                       double bytes) {
+                       double bytes, int ybeg, int yend) {
   AAC_TRY(aux_streams(ctx));
   const bool gen = ctx->geo.dir || ctx->nranks > 1;
   const int naux = std::min(aac_ctx::NAUX, S.nb - 1);
@@ -834,7 +843,7 @@ static int waver_group(aac_ctx* ctx, const WSweep& S, int nchunk, const WSlab& s
     const int halo = S.b[i].ns;
     const int nstrip = (ctx->geo.nx + (NT - 2 * halo) - 1) / (NT - 2 * halo);
     const cudaStream_t s = i == 0 ? ctx->stream : ctx->aux[(i - 1) % naux];
-    const WROne P{S.b[i], nstrip, S.ly[i]};
+    const WROne P{S.b[i], nstrip, S.ly[i], ybeg, yend};
     if (ctx->inner_f32)                 // mixed precision (AAC_F32): fp32 recurrence, fp64 storage
       AAC_TRY((waver_launch_ns<H, NT, H, float>(ctx, P, P.nstrip * nchunk, sl, st, s, gen)));
     else
@@ -874,6 +883,14 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
   const int ly_env = getenv("AAC_WAVE_LY") ? atoi(getenv("AAC_WAVE_LY")) : 0;
   const double* fin[AAC_MAX_BLK] = {};
   const int steps_max = P.pmax - 1;
+  // Ghost mode (several ranks, one pass, no passive block): the wavefront also computes x_{p_k}
+  // on the slab's ghost rows (-1, ny; the hat-w halo is one row deeper than the deepest pass),
+  // and their inverse transform below is Z_j's halo -- the step needs no exchange of Z_j.
+  static const bool ghost_off = getenv("AAC_WAVE_GHOST") && atoi(getenv("AAC_WAVE_GHOST")) == 0;
+  bool ghost = !old && !ghost_off && ctx->nranks > 1 && ctx->d_ghost && steps_max <= H &&
+               ctx->wave_hd >= steps_max + 1;
+  for (int kb = 0; kb <= h; ++kb) ghost = ghost && P.p[kb] >= 2;
+  const int ybeg = (ghost && g.has_lo) ? -1 : 0, yend = (ghost && g.has_hi) ? g.ny + 1 : g.ny;
   for (int pass = 0; pass * H < steps_max; ++pass) {
     const int s0 = 1 + pass * H;
     const int set = pass & 1, prev_set = set ^ 1;
@@ -904,6 +921,8 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       const bool final_pass = s0 + ns - 1 == steps;
       B.out_last = ctx->d_X + (long long)(2 * set) * L + (long long)q * N;
       B.out_prev = final_pass ? nullptr : ctx->d_X + (long long)(2 * set + 1) * L + (long long)q * N;
+      B.glo = ghost ? ctx->d_ghost + (long long)q * g.nx : nullptr;
+      B.ghi = ghost ? ctx->d_ghost + (long long)(ell + q) * g.nx : nullptr;
       if (final_pass) fin[kb] = B.out_last;
       for (int l = 0; l < ns; ++l) {
         const int s = s0 + l;
@@ -940,8 +959,9 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
       // per-block register wavefront: latency-bound at 2-3 CTAs per SM, so more, shorter chunks
       // pay for their warm-up rows -- about 64 rows, ny split evenly (measured at the headline:
       // 8.41 ms per solve at 64 rows, 8.46-8.57 at 40-72, 8.63 at 80, 9.21 at 160)
-      const int nch = std::max(1, (g.ny + 63) / 64);
-      ly0 = (g.ny + nch - 1) / nch;
+      const int rows = yend - ybeg;                    // (ghost mode: the slab + its ghost rows)
+      const int nch = std::max(1, (rows + 63) / 64);
+      ly0 = (rows + nch - 1) / nch;
       const long long slots = 2LL * ctx->num_sms;
       const long long cols = (long long)g.ny * nstrip * nb;
       if (cols / ly0 < slots) {                        // small grids: fill the resident slots
@@ -988,8 +1008,22 @@ static int wave_passes_t(aac_ctx* ctx, const NcPlan& P, double* zbase, long long
                   ? k_wave<H, NT, true><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)
                   : k_wave<H, NT, false><<<ncta, NT, smem, ctx->stream>>>(g, S, ctx->d_what, st, sl)));
     } else {
-      AAC_TRY(waver_group<H, NT>(ctx, S, (g.ny + S.ly[0] - 1) / S.ly[0], sl, st, 8.0 * N * passes + C));
+      AAC_TRY(waver_group<H, NT>(ctx, S, (yend - ybeg + S.ly[0] - 1) / S.ly[0], sl, st, 8.0 * N * passes + C,
+                                 ybeg, yend));
     }
+  }
+  if (ghost) {                                         // Z_j on the ghost rows -> d_halo
+    NcFinal G{};
+    for (int side = 0; side < 2; ++side) {
+      if (side == 0 ? !g.has_lo : !g.has_hi) continue;
+      for (int kb = 0; kb <= h; ++kb) {
+        G.tr[kb] = 1.0;
+        G.ti[kb] = 0.0;
+        G.src[kb] = ctx->d_ghost + (long long)(side * ell + plane_of_block(ell, kb)) * g.nx;
+      }
+      AAC_TRY(run_inverse_n(ctx, D, G, ctx->d_halo + (long long)side * ell * g.S, 0, st, g.nx));
+    }
+    ctx->z_ghost = true;
   }
   NcFinal F{};
   for (int kb = 0; kb <= h; ++kb) {
@@ -1275,6 +1309,7 @@ static int arnoldi_impl(aac_ctx* ctx, int host_j) {
 // forms V_j), then w = calA Z_j with the CGS2 projections and Gram column.
 static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   int rc = AAC_OK;
+  ctx->z_ghost = false;
   if (method == AAC_SP) {
     const double V = 8.0 * ctx->ell * ctx->geo.N;
     rc = forward_step(ctx, (host_j + 3) * V);
@@ -1286,7 +1321,9 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
     rc = nc_apply(ctx, method, k, nullptr, ctx->d_Z, true, host_j);
   }
   if (rc != AAC_OK) return rc;                         // error, or the solve finished
-  if (ctx->nranks > 1) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
+  // Z_j's halo: exchanged, unless the wavefront formed it from its ghost rows (ghost mode)
+  if (ctx->nranks > 1 && !ctx->z_ghost) AAC_TRY(halo_planes(ctx, ctx->d_Z + (long long)host_j * ctx->ell * ctx->geo.N));
+  ctx->z_ghost = false;
   AAC_TRY(arnoldi_impl(ctx, host_j));
   if (ctx->multi()) {
     AAC_TRY(comm_allreduce(ctx, ctx->d_red, 2 * (host_j + 1), ncclSum));

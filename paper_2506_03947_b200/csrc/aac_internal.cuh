@@ -132,6 +132,8 @@ struct aac_ctx {
   long long wext_x = 0;                // offset of wy in d_wext
   int wext_off = 0, wext_rows = 0;     // lo - elo, ehi - elo
   double* d_whalo = nullptr;           // [2][ell][hd][nx]
+  double* d_ghost = nullptr;           // [2][ell][nx]: final Chebyshev iterates of the slab ghost rows
+  bool z_ghost = false;                // this step's preconditioner wrote Z_j's halo rows (d_halo)
   int wave_hd = 0;                     // halo depth (0: slabs too thin, per-step sweeps)
   // plans
   NcPlan nc[2];                        // cached NC plans

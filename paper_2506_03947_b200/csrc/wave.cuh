@@ -36,6 +36,8 @@ struct WBlk {
   double sr, si, mr, mi;
   double* out_last;          // x_{s0+ns}   plane q
   double* out_prev;          // x_{s0+ns-1} plane q, or NULL (final pass)
+  double* glo;               // slab ghost rows (k_waver, single pass): x_{p_k} of local row -1 / ny,
+  double* ghi;               // plane q of [ell][nx] buffers (plane stride nx); NULL: none
   double lr, li;             // Lambda_k
   double ar[WAVE_MAXH], ai[WAVE_MAXH], br[WAVE_MAXH], bi[WAVE_MAXH];   // steps s0 .. s0+ns-1
 };

@@ -245,6 +245,12 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
     if (i == NS) {
       const int r = tau - i;
       if (colout && r >= y0 && r < y1) {
+        if (GEN && (r < 0 || r >= g.ny)) {               // slab ghost row (-1 or ny): the
+          double* gq = (r < 0 ? B.glo : B.ghi) + x;      // neighbour's boundary row of x_{p_k}
+          gq[0] = o0;
+          if (CPLX) gq[g.nx] = o1;
+          continue;
+        }
         const long long p = (long long)r * g.nx + x;
         B.out_last[p] = o0;
         if (CPLX) B.out_last[g.N + p] = o1;
@@ -303,6 +309,8 @@ struct WROne {
   WBlk b;
   int nstrip;                // strips of NT - 2H columns
   int ly;                    // rows per chunk
+  int ybeg, yend;            // output rows [ybeg, yend): [0, ny), or one slab ghost row more per
+                             // side with a neighbour (ghost mode)
 };
 
 // Shared memory: the x-exchange rows [2 buffers][NS levels][planes][NT + 2].
@@ -326,8 +334,8 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   const int x = strip * TX - HX + t;
   const bool colin = x >= 0 && x < g.nx;
   const bool colout = t >= HX && t < NT - HX && x < g.nx;
-  const int y0 = chunk * P.ly;
-  const int y1 = min(y0 + P.ly, g.ny);
+  const int y0 = P.ybeg + chunk * P.ly;
+  const int y1 = min(y0 + P.ly, P.yend);
   // zero pads of the exchange rows (never written)
   constexpr int XW = NT + 2;
   if constexpr (CPLX && WR_PAIRX) {                     // rows of XW (Re, Im) pairs

@@ -48,7 +48,9 @@ def main():
     prof = s.profile_read()
     s.profile(False)
     out["wave_flops"] = prof["cheb_sweep"]["model_flops"]     # > 0 only for the wavefront kernel
+    l0 = s.launch_count()
     xs, info = s.gmres(case["method"], case["k"], local(p.b), rtol=p.rtol, maxit=60)
+    out["gmres_launches"] = s.launch_count() - l0
     out["x"] = xs.cpu().numpy()
     out["iters"] = info["iters"]
     out["relres_true"] = info["relres_true"]

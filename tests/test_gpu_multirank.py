@@ -57,7 +57,7 @@ CASES = [
     (2, dict(name="headline", kw=dict(shape=(1, 40, 29)), method="nc2", k=8, k_sp=3, sp=True)),
     (3, dict(name="headline", kw=dict(shape=(1, 36, 33)), method="nc2", k=8, k_sp=3, sp=True)),
     (2, dict(name="headline", kw=dict(shape=(1, 37, 29)), method="nc2", k=8, k_sp=3, sp=False)),
-    # slabs thinner than the wavefront halo (8 rows): the per-step sweeps run instead
+    # slabs thinner than the wavefront halo (9 rows): the per-step sweeps run instead
     (4, dict(name="headline", kw=dict(shape=(1, 26, 21)), method="nc2", k=8, k_sp=3, sp=False)),
     (2, dict(name="3d", kw=dict(shape=(12, 9, 8)), method="nc1", k=10, k_sp=2, sp=True)),
     (3, dict(name="3d", kw=dict(shape=(7, 6, 9), ell=4), method="nc2", k=5, k_sp=2, sp=False)),
@@ -82,7 +82,7 @@ def test_multirank_slabs_match_oracle(tmp_path, world, case):
     rr = rng.standard_normal((p.ell,) + p.shape)
     assert _rel(_stitch(parts, "y", p), op.apply_allatonce(w, x)) <= 1e-12
     if p.dim == 2:                                             # which NC organisation ran
-        thick = min(d["hi"] - d["lo"] for d in parts) >= 8
+        thick = min(d["hi"] - d["lo"] for d in parts) >= 9       # WAVE_MAXH + 1 (ghost row)
         assert all((float(d["wave_flops"]) > 0) == thick for d in parts)
     for m in ("nc1", "nc2"):
         al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * case["k"], m, case["k"])
@@ -109,3 +109,27 @@ def test_multirank_slabs_match_oracle(tmp_path, world, case):
     its = {int(d["iters_sp"]) for d in parts}
     assert len(its) == 1 and abs(its.pop() - rs.iters) <= 1
     assert _rel(_stitch(parts, "x_sp", p), rs.x) <= 1e-9
+
+
+def test_multirank_ghost_rows_bit_identical(tmp_path):
+    """Ghost mode (the wavefront computes the slab ghost rows and Z_j's halo is formed locally,
+    no exchange of Z_j) reproduces the exchange path (AAC_WAVE_GHOST=0) bit for bit: the ghost
+    rows are the same point recurrences on the same inputs as the neighbour's own rows."""
+    case = dict(name="headline", kw=dict(shape=(1, 40, 29)), method="nc2", k=8, k_sp=3, sp=False)
+    outs = []
+    for flag in ("1", "0"):
+        d = tmp_path / f"g{flag}"
+        d.mkdir()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               os.path.join(HERE, "_mr_worker.py"), str(d), json.dumps(case)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "AAC_WAVE_GHOST": flag})
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        outs.append([dict(np.load(d / f"r{i}.npz")) for i in range(2)])
+    for a, b in zip(*outs):
+        for key in ("x", "z_nc1", "z_nc2"):
+            assert np.array_equal(a[key], b[key]), key
+        assert int(a["iters"]) == int(b["iters"])
+        # ghost mode ran: one ghost-row inverse transform per step on each rank (one neighbour)
+        assert int(a["gmres_launches"]) - int(b["gmres_launches"]) >= int(a["iters"])
