@@ -111,7 +111,10 @@ int aac_setup(const aac_grid* g, const double* kx, const double* ky, const doubl
  * torch.distributed "gloo") carry the slab decomposition -- used to verify the multi-rank
  * path with several processes sharing fewer GPUs than ranks, where NCCL cannot run.
  *  allreduce(user, buf, n, op): in-place all-reduce of n HOST doubles over all ranks,
- *                               op 0 = sum, 1 = max. Return 0 on success.
+ *                               op 0 = sum, 1 = max; op 2 = all-gather: buf holds nranks * n
+ *                               doubles, this rank's n at offset rank * n on entry, every
+ *                               rank's at its offset on return (the library then sums them in
+ *                               rank order). Return 0 on success.
  *  sendrecv(user, n, send_lo, recv_lo, send_hi, recv_hi): exchange n HOST doubles with
  *      the rank below (send_lo -> its recv_hi, its send_hi -> recv_lo) and the rank above;
  *      the pointers of a missing neighbour are NULL. Return 0 on success.

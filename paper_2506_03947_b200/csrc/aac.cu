@@ -395,6 +395,14 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   }
   ctx->mu_min = 1.0;
   ctx->mu_max = gmax;
+  // rank-ordered sums (comm.cuh): the gather buffer exists before any step graph is captured
+  if (ctx->multi() &&
+      cudaMalloc((void**)&ctx->d_gath, (size_t)ctx->nranks * AAC_GATHER_MAX * sizeof(double)) != cudaSuccess) {
+    ctx->d_gath = nullptr;
+    cudaGetLastError();
+    aac_destroy(ctx);
+    return aac_fail(nullptr, AAC_ENOMEM, "gather buffer allocation failed");
+  }
   *out = ctx;
   return AAC_OK;
 }
@@ -418,6 +426,7 @@ extern "C" void aac_destroy(aac_ctx* ctx) {
   if (ctx->d_T) cudaFree(ctx->d_T);
   if (ctx->d_whalo) cudaFree(ctx->d_whalo);
   if (ctx->d_ghost) cudaFree(ctx->d_ghost);
+  if (ctx->d_gath) cudaFree(ctx->d_gath);
   if (ctx->h_stat) cudaFreeHost(ctx->h_stat);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   cudaEvent_t evs[] = {ctx->ev_in, ctx->ev_out, ctx->ev_it[0], ctx->ev_it[1]};

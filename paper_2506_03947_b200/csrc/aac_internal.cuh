@@ -16,6 +16,7 @@
 
 #define AAC_MAX_ELL 16
 #define AAC_MAX_BLK (AAC_MAX_ELL / 2 + 1)
+#define AAC_GATHER_MAX 1024    // longest sum reduced by all-gather + rank-order sum
 
 // ------------------------------------------------------------------------------------------
 // Geometry of this rank's slab, passed BY VALUE to every stencil kernel.
@@ -132,6 +133,7 @@ struct aac_ctx {
   long long wext_x = 0;                // offset of wy in d_wext
   int wext_off = 0, wext_rows = 0;     // lo - elo, ehi - elo
   double* d_whalo = nullptr;           // [2][ell][hd][nx]
+  double* d_gath = nullptr;            // [nranks][AAC_GATHER_MAX]: rank-ordered sums (comm.cuh)
   double* d_ghost = nullptr;           // [2][ell][nx]: final Chebyshev iterates of the slab ghost rows
   bool z_ghost = false;                // this step's preconditioner wrote Z_j's halo rows (d_halo)
   int wave_hd = 0;                     // halo depth (0: slabs too thin, per-step sweeps)

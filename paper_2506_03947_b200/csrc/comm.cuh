@@ -20,6 +20,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -42,6 +43,7 @@ static int nccl_load(aac_ctx* ctx) {
   SYM("ncclCommInitRank", CommInitRank)
   SYM("ncclCommDestroy", CommDestroy)
   SYM("ncclAllReduce", AllReduce)
+  SYM("ncclAllGather", AllGather)
   SYM("ncclSend", Send)
   SYM("ncclRecv", Recv)
   SYM("ncclGroupStart", GroupStart)
@@ -183,9 +185,54 @@ static int comm_sync(aac_ctx* ctx) {
 }
 
 // In-place all-reduce of n doubles on the context stream (no-op on one rank).
+// d[i] = sum_{r < P} g[r * n + i], ranks in order (a fixed association on every rank and run).
+__global__ void k_rank_sum(const double* __restrict__ g, int P, int n, double* d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < P; ++r) s += g[(long long)r * n + i];
+    d[i] = s;
+  }
+}
+
+// Sums of at most AAC_GATHER_MAX doubles (the GMRES / CI / SP inner products) are all-gathered
+// and added in rank order (the reductions across ranks do not depend on NCCL's
+// algorithm or on the host group's order); longer sums (the zero-padded gathered multigrid
+// level, where every entry has one non-zero contribution, so any order is exact) and maxima use
+// the transport's all-reduce.
+static int comm_gather_sum(aac_ctx* ctx, double* d, int n) {
+  const int P = ctx->nranks;
+  if (!ctx->d_gath) {
+    if (cudaMalloc((void**)&ctx->d_gath, (size_t)P * AAC_GATHER_MAX * sizeof(double)) != cudaSuccess) {
+      ctx->d_gath = nullptr;
+      cudaGetLastError();
+      return aac_fail(ctx, AAC_ENOMEM, "gather buffer allocation failed");
+    }
+  }
+  double* mine = ctx->d_gath + (long long)ctx->rank * n;
+  CUDA_TRY(ctx, cudaMemcpyAsync(mine, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->host_tr) {
+    AAC_TRY(host_stage(ctx, (long long)P * n));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stage + (long long)ctx->rank * n, d, (size_t)n * sizeof(double),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->htr.allreduce(ctx->htr.user, ctx->h_stage, n, 2) != 0)
+      return aac_fail(ctx, AAC_ENCCL, "host transport all-gather failed");
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_gath, ctx->h_stage, (size_t)P * n * sizeof(double),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    NCCL_TRY(ctx, g_nccl.AllGather(mine, ctx->d_gath, (size_t)n, ncclFloat64, (ncclComm_t)ctx->nccl_comm,
+                                   ctx->stream));
+  }
+  k_rank_sum<<<1, 256, 0, ctx->stream>>>(ctx->d_gath, P, n, d);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->host_tr) CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // h_stage reused next call
+  return AAC_OK;
+}
+
 static int comm_allreduce(aac_ctx* ctx, double* d, int n, ncclRedOp_t op) {
   if (!ctx->multi() || n <= 0) return AAC_OK;
   if (!ctx->host_tr && !ctx->nccl_comm) return aac_fail(ctx, AAC_ENCCL, "NCCL communicator aborted");
+  if (op == ncclSum && n <= AAC_GATHER_MAX) return comm_gather_sum(ctx, d, n);
   if (ctx->host_tr) return host_allreduce(ctx, d, n, op == ncclMax ? 1 : 0);
   NCCL_TRY(ctx, g_nccl.AllReduce(d, d, (size_t)n, ncclFloat64, op, (ncclComm_t)ctx->nccl_comm,
                                  ctx->stream));

@@ -40,6 +40,12 @@ class HostTransport:
 
         def allreduce(user, buf, n, op):
             try:
+                if op == 2:                      # all-gather: rank r's n doubles at offset r * n
+                    t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n * self.nranks,)))
+                    parts = list(t.view(self.nranks, n).unbind(0))
+                    mine = parts[self.rank].clone()
+                    dist.all_gather(parts, mine, group=self.group)
+                    return 0
                 t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
                 dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM,
                                 group=self.group)
