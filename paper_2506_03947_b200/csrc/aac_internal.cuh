@@ -1,6 +1,7 @@
 // aac_internal.cuh -- context, geometry and launch plumbing of libaac (sm_100a, fp64).
 // Not part of the C ABI (include/aac.h is). See DESIGN.md §5 for the data layout.
 #pragma once
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -209,6 +210,25 @@ struct LaunchScope {
   LaunchScope(aac_ctx* c, int kid, double bytes);
   int end();
 };
+
+// Launch with programmatic stream serialisation (PDL): the kernel may be scheduled while its
+// predecessor drains and waits in griddep() (krylov.cuh); AAC_PDL=0 launches normally.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  static const bool off = getenv("AAC_PDL") && atoi(getenv("AAC_PDL")) == 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 #define LAUNCH(ctx, kid, bytes, ...)                                                         \
   do {                                                                                      \

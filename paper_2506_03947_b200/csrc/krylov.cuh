@@ -33,6 +33,15 @@ struct IterState {
 // host reads it after an event / stream sync. Unlike a D2H memcpy this needs no copy engine, so
 // the per-step poll never queues behind a large host transfer on another stream
 // (aac_gmres_host_batch moves whole vectors in and out while the solves run).
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialisation
+// attribute may start while its predecessor drains; it waits here for the predecessor's completion
+// (and memory flush) before touching anything, then lets its own successor launch. A no-op for
+// kernels launched normally.
+__device__ __forceinline__ void griddep() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_publish(const unsigned* __restrict__ src, unsigned* dst, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }

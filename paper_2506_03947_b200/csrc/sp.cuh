@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(SP_T) k_mg_prolong_post_pair2(Geo g, const dou
 // x_c = A_c(s)^{-1} b_c with the precomputed dense inverse of the plane's block (CTA per plane)
 __global__ void __launch_bounds__(SP_T) k_mg_coarse(int nc, const double* __restrict__ minv, int ell,
                                                     const double* bc, double* xc, const IterState* st) {
+  griddep();
   if (st && st->done) return;
   const int pl = blockIdx.x;
   const double* M = minv + (long long)sp_block_of(ell, pl) * nc * nc;
@@ -669,6 +670,7 @@ __device__ __forceinline__ void tail_xyz(const Geo& g, long long p, int& x, int&
 
 template <int DIM>
 __global__ void __launch_bounds__(SP_TAIL_T) k_mg_tail(MgTail T, SpConst K, const IterState* st) {
+  griddep();
   if (st && st->done) return;
   const int pl = blockIdx.x;
   const double s = K.s[pl];
@@ -746,6 +748,7 @@ struct SpVec {
 // complex planes: Vc = [Im w; Re w] (u-plane <- Im w, v-plane <- Re w), Vp = Wp = Wc = X = 0;
 // real planes: R = w, X = 0.
 __global__ void __launch_bounds__(SP_T) k_sp_init(long long N, int ell, SpVec v, const IterState* st) {
+  griddep();
   if (st && st->done) return;
   const long long p = (long long)blockIdx.x * SP_T + threadIdx.x;
   if (p >= N) return;
@@ -907,6 +910,7 @@ __global__ void __launch_bounds__(SP_T) k_sp_upd1(long long N, int ell, SpVec v,
 // real: P = Zr + beta P.
 __global__ void __launch_bounds__(SP_T) k_sp_upd2(long long N, int ell, SpVec v, const SpBlk* blk,
                                                   const IterState* st) {
+  griddep();
   if (st && st->done) return;
   const int pl = blockIdx.y, h = ell / 2, kb = sp_block_of(ell, pl);
   const SpBlk& b = blk[kb];
@@ -931,6 +935,7 @@ __global__ void __launch_bounds__(SP_T) k_sp_upd2(long long N, int ell, SpVec v,
 // restriction, sp_fused.cuh): X += alpha P, R -= alpha Q for planes 0 and ell - 1.
 __global__ void __launch_bounds__(SP_T) k_sp_upd1_real(long long N, int ell, SpVec v, const SpBlk* blk,
                                                        const IterState* st) {
+  griddep();
   if (st && st->done) return;
   const int pl = blockIdx.y == 0 ? 0 : ell - 1, kb = sp_block_of(ell, pl);
   const SpBlk& b = blk[kb];
@@ -1371,10 +1376,10 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U 
       const double nb = u.on ? (4.0 * (ell - 2) + 2.0) : (double)ell;
       const double bytes = 8.0 * a.g.N * (nb + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
       if (a.g.nx % 2 == 0)
-        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_restrict<true><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+        LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_restrict<true>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, P->K, io, bl, c.b, u, nsx, st));
       else
-        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_restrict<false><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+        LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_restrict<false>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, P->K, io, bl, c.b, u, nsx, st));
       continue;
     }
@@ -1411,7 +1416,7 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U 
     }
     T.minv = P->minv;
     T.nc = P->nc;
-    LAUNCH(ctx, KID_SP_MG, bytes, k_mg_tail<DIM><<<ell, SP_TAIL_T, 0, ctx->stream>>>(T, P->K, st));
+    LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_mg_tail<DIM>, dim3(ell), dim3(SP_TAIL_T), 0, ctx->stream, T, P->K, st));
   } else {
     LAUNCH(ctx, KID_SP_MG, 8.0 * ell * P->nc * P->nc,
            k_mg_coarse<<<ell, SP_T, 0, ctx->stream>>>(P->nc, P->minv, ell, cl.b, cl.x2, st));
@@ -1431,10 +1436,10 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U 
       if (l == 0) nt = nsx * std::min(c.g.ny, std::max(1, spf_cps() * ctx->num_sms / (nsx * (ell / 2))));
       const double bytes = 8.0 * a.g.N * (2.0 * ell + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
       if (a.g.nx % 2 == 0)
-        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_prolong_post<true><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+        LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_prolong_post<true>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, io, bl, c.x2, a.x2, S, P->red2, l == 0 ? 1 : 0, nsx));
       else
-        LAUNCH(ctx, KID_SP_MG, bytes, k_spf_prolong_post<false><<<dim3(nt, ell / 2), SPF_T, 0, ctx->stream>>>(
+        LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_prolong_post<false>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, io, bl, c.x2, a.x2, S, P->red2, l == 0 ? 1 : 0, nsx));
       continue;
     }
@@ -1507,7 +1512,7 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     return AAC_OK;
   };
   const unsigned gt = grid1d(N, SP_T);
-  LAUNCH(ctx, KID_SP_VEC, 2.0 * V, k_sp_init<<<gt, SP_T, 0, ctx->stream>>>(N, ell, vecs(), st));
+  LAUNCH(ctx, KID_SP_VEC, 2.0 * V, launch_pdl(k_sp_init, dim3(gt), dim3(SP_T), 0, ctx->stream, N, ell, vecs(), st));
   S.phase = 0;
   AAC_TRY(sp_vcycle<DIM>(ctx, io_for(true), S));          // z_1 = M v_1 ; p_0 = M r_0
   AAC_TRY(finish(ell, 1));
@@ -1530,10 +1535,10 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
       const int nry = std::min(nyp, std::max(1, spf_cps() * ctx->num_sms / (nsx * h)));
       if (ctx->geo.nx % 2 == 0)
         LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
-               k_spf_apply<true><<<dim3(nsx * nry, h), SPF_T, 0, ctx->stream>>>(ctx->geo, vecs(), S, P->red2, nsx));
+               launch_pdl(k_spf_apply<true>, dim3(nsx * nry, h), dim3(SPF_T), 0, ctx->stream, ctx->geo, vecs(), S, P->red2, nsx));
       else
         LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
-               k_spf_apply<false><<<dim3(nsx * nry, h), SPF_T, 0, ctx->stream>>>(ctx->geo, vecs(), S, P->red2, nsx));
+               launch_pdl(k_spf_apply<false>, dim3(nsx * nry, h), dim3(SPF_T), 0, ctx->stream, ctx->geo, vecs(), S, P->red2, nsx));
     } else if (DIM == 2 && !no_row2d)
       LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
              k_sp_apply2<<<dim3(std::min<unsigned>(gsa, (unsigned)ctx->geo.ny), h + 1), SP_T, 0, ctx->stream>>>(
@@ -1549,8 +1554,8 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     if (sp_fused_on(ctx, DIM)) {
       // complex planes: v_{j+1} formed inside the level-0 restriction; real planes here
       LAUNCH(ctx, KID_SP_VEC, 3.0 * V * 2 / ell,
-             k_sp_upd1_real<<<dim3(std::min<unsigned>(gt, upd_cap), 2), SP_T, 0, ctx->stream>>>(
-                 N, ell, vecs(), P->blk, st));
+             launch_pdl(k_sp_upd1_real, dim3(std::min<unsigned>(gt, upd_cap), 2), dim3(SP_T), 0, ctx->stream,
+                        N, ell, vecs(), P->blk, st));
       AAC_TRY(sp_vcycle<DIM>(ctx, io_for(false), S, SpfUpd{P->SZ, Vc, Vp, P->blk, 1}));
     } else {
       LAUNCH(ctx, KID_SP_VEC, 3.0 * V,
@@ -1560,8 +1565,8 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     }
     AAC_TRY(finish(ell, 1));
     LAUNCH(ctx, KID_SP_VEC, 4.0 * V,
-           k_sp_upd2<<<dim3(std::min<unsigned>(gt, upd_cap), ell), SP_T, 0, ctx->stream>>>(
-               N, ell, vecs(), P->blk, st));
+           launch_pdl(k_sp_upd2, dim3(std::min<unsigned>(gt, upd_cap), ell), dim3(SP_T), 0, ctx->stream,
+                      N, ell, vecs(), P->blk, st));
     // rotate: v_prev <- v <- v_next, z <- z_next, w_prev <- w <- w_next
     double* t = Vp; Vp = Vc; Vc = Vn; Vn = t;
     t = Zc; Zc = Zn; Zn = t;

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_restrict(Geo g, Geo gc, const 
                                                            const double* __restrict__ dinv, SpConst K, MgIo io,
                                                            const double* bl, double* bc, SpfUpd U, int nsx,
                                                            const IterState* st) {
+  griddep();
   if (st && st->done) return;
   int pa, pb;
   sp_pair(K.ell, blockIdx.y, pa, pb);
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_prolong_post(Geo g, Geo gc, co
                                                                const double* bl, const double* __restrict__ xc,
                                                                double* x2l, SpStepCtx S, SpfRed R, int level0,
                                                                int nsx) {
+  griddep();
   if (S.st && S.st->done) return;
   int pa, pb;
   sp_pair(S.K.ell, blockIdx.y, pa, pb);
@@ -475,6 +477,7 @@ __device__ __forceinline__ void spf_reduce_apply(const SpStepCtx& S, const SpfRe
 
 template <bool EVEN>
 __global__ void __launch_bounds__(SPF_T, 4) k_spf_apply(Geo g, SpVec v, SpStepCtx S, SpfRed R, int nsx) {
+  griddep();
   if (S.st && S.st->done) return;
   const int pair = blockIdx.y, ell = S.K.ell, h = ell / 2;
   const long long N = g.N;
