@@ -21,8 +21,17 @@ struct KAParams {
   ArnoldiCtx ac;
 };
 
-constexpr int AT = 256;          // tile points per CTA iteration (one per consumer thread)
-constexpr int AS = 4;            // bulk-copy pipeline stages for the basis tiles
+#ifndef ARN_AS
+#define ARN_AS 4
+#endif
+#ifndef ARN_OCC
+#define ARN_OCC 2
+#endif
+#ifndef ARN_AT
+#define ARN_AT 256
+#endif
+constexpr int AT = ARN_AT;       // tile points per CTA iteration (one per consumer thread)
+constexpr int AS = ARN_AS;       // bulk-copy pipeline stages for the basis tiles
 constexpr int AW = AT / 32;      // consumer warps; warp AW is the TMA producer
 
 // Dynamic shared memory layout: [AS][ELLC][AT] basis ring | [AW][2*ldh] acc | [2*ldh] tot
@@ -34,7 +43,7 @@ __host__ __device__ constexpr size_t arnoldi_ring_doubles() { return (size_t)AS 
 // FUSED: w = calA Z_j computed here (stencil) and stored; otherwise w is read from W (written
 // by k_matvec just before: one more read of W, but both kernels then run at full occupancy).
 template <int DIM, int ELLC, bool TMA, bool FUSED>
-__global__ void __launch_bounds__(AT + 32, 2) k_arnoldi(Geo g, int ell, KAParams P) {
+__global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KAParams P) {
   IterState* st = P.ac.st;
   if (st->done) return;
   const int j = st->j;
