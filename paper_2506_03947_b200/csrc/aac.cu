@@ -8,6 +8,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdlib>
+#include <type_traits>
 
 #include "aac_internal.cuh"
 #include "arnoldi.cuh"
@@ -795,8 +796,29 @@ static int forward_step(aac_ctx* ctx, double bytes) {
 // back into the library stream (a fork/join subgraph under graph capture).
 template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
 static int waver_launch_t(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
-                          cudaStream_t s) {
-  auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT, T>;
+                          cudaStream_t s, bool clu) {
+  if constexpr (!GEN && std::is_same<T, double>::value) {
+    if (clu) {                          // the strips of a row chunk as one cluster (no x-halo)
+      auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT, true, T>;
+      const size_t smem = waver_smem_clu<NT, T>(NS, CPLX ? 2 : 1);
+      AAC_TRY(smem_optin(ctx, kern, smem));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ncta);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)P.nstrip;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ctx->geo, P, (const double*)ctx->d_what, st, sl));
+      return AAC_OK;
+    }
+  }
+  auto kern = k_waver<H, NT, NS, CPLX, GEN, VIRT, false, T>;
   const size_t smem = waver_smem<NT, T>(NS, CPLX ? 2 : 1);
   AAC_TRY(smem_optin(ctx, kern, smem));
   kern<<<ncta, NT, smem, s>>>(ctx->geo, P, ctx->d_what, st, sl);
@@ -805,20 +827,20 @@ static int waver_launch_t(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& s
 
 template <int H, int NT, int NS, typename T>
 static int waver_launch_ns(aac_ctx* ctx, const WROne& P, int ncta, const WSlab& sl, const IterState* st,
-                           cudaStream_t s, bool gen) {
+                           cudaStream_t s, bool gen, bool clu) {
   if constexpr (NS >= 1) {
-    if (P.b.ns != NS) return waver_launch_ns<H, NT, NS - 1, T>(ctx, P, ncta, sl, st, s, gen);
+    if (P.b.ns != NS) return waver_launch_ns<H, NT, NS - 1, T>(ctx, P, ncta, sl, st, s, gen, clu);
     const bool c = P.b.np == 2, v = P.b.virt != 0;
     if (gen) {
-      if (c) return v ? waver_launch_t<H, NT, NS, true, true, true, T>(ctx, P, ncta, sl, st, s)
-                      : waver_launch_t<H, NT, NS, true, true, false, T>(ctx, P, ncta, sl, st, s);
-      return v ? waver_launch_t<H, NT, NS, false, true, true, T>(ctx, P, ncta, sl, st, s)
-               : waver_launch_t<H, NT, NS, false, true, false, T>(ctx, P, ncta, sl, st, s);
+      if (c) return v ? waver_launch_t<H, NT, NS, true, true, true, T>(ctx, P, ncta, sl, st, s, clu)
+                      : waver_launch_t<H, NT, NS, true, true, false, T>(ctx, P, ncta, sl, st, s, clu);
+      return v ? waver_launch_t<H, NT, NS, false, true, true, T>(ctx, P, ncta, sl, st, s, clu)
+               : waver_launch_t<H, NT, NS, false, true, false, T>(ctx, P, ncta, sl, st, s, clu);
     }
-    if (c) return v ? waver_launch_t<H, NT, NS, true, false, true, T>(ctx, P, ncta, sl, st, s)
-                    : waver_launch_t<H, NT, NS, true, false, false, T>(ctx, P, ncta, sl, st, s);
-    return v ? waver_launch_t<H, NT, NS, false, false, true, T>(ctx, P, ncta, sl, st, s)
-             : waver_launch_t<H, NT, NS, false, false, false, T>(ctx, P, ncta, sl, st, s);
+    if (c) return v ? waver_launch_t<H, NT, NS, true, false, true, T>(ctx, P, ncta, sl, st, s, clu)
+                    : waver_launch_t<H, NT, NS, true, false, false, T>(ctx, P, ncta, sl, st, s, clu);
+    return v ? waver_launch_t<H, NT, NS, false, false, true, T>(ctx, P, ncta, sl, st, s, clu)
+             : waver_launch_t<H, NT, NS, false, false, false, T>(ctx, P, ncta, sl, st, s, clu);
   }
   return aac_fail(ctx, AAC_EINVAL, "wavefront: bad step count %d", P.b.ns);
 }
@@ -831,6 +853,18 @@ static int aux_streams(aac_ctx* ctx) {
   }
   CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   return AAC_OK;
+}
+
+// Cluster wavefront (k_waver CLU, opt-in: AAC_WAVE_CLUSTER=1): the strips of a row chunk
+// exchange edge columns through distributed shared memory, so no strip recomputes an x-halo.
+// Needs all strips of a row in one cluster (ceil(nx / NT) <= 8, the portable cluster size).
+// Bit-identical to the halo kernel but measured slower at the headline (9.10-9.49 vs 8.31 ms per
+// solve): the per-step neighbour coupling costs more than the halo columns.
+static bool wave_cluster(const aac_ctx* ctx, int nt) {
+  const char* e = getenv("AAC_WAVE_CLUSTER");        // (read per pass: tests switch it)
+  const int env = e ? atoi(e) : 0;
+  const int nstrip = (ctx->geo.nx + nt - 1) / nt;
+  return env != 0 && ctx->dim == 2 && nstrip >= 2 && nstrip <= 8;
 }
 
 // All blocks of one wavefront pass: block 0 (the heaviest) on the library stream, the others
@@ -847,16 +881,18 @@ static int waver_group(aac_ctx* ctx, const WSweep& S, int nchunk, const WSlab& s
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
     for (int a = 0; a < naux; ++a) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux[a], ctx->ev_fork, 0));
   }
+  const bool clu = wave_cluster(ctx, NT) && !gen && !ctx->inner_f32;
   for (int i = 0; i < S.nb; ++i) {
-    // strips of NT - 2 ns columns: the x-halo of a block is its step count
-    const int halo = S.b[i].ns;
+    // strips of NT - 2 ns columns: the x-halo of a block is its step count; with a cluster
+    // (wave_cluster) strips of NT columns without a halo
+    const int halo = clu ? 0 : S.b[i].ns;
     const int nstrip = (ctx->geo.nx + (NT - 2 * halo) - 1) / (NT - 2 * halo);
     const cudaStream_t s = i == 0 ? ctx->stream : ctx->aux[(i - 1) % naux];
     const WROne P{S.b[i], nstrip, S.ly[i], ybeg, yend};
     if (ctx->inner_f32)                 // mixed precision (AAC_F32): fp32 recurrence, fp64 storage
-      AAC_TRY((waver_launch_ns<H, NT, H, float>(ctx, P, P.nstrip * nchunk, sl, st, s, gen)));
+      AAC_TRY((waver_launch_ns<H, NT, H, float>(ctx, P, P.nstrip * nchunk, sl, st, s, gen, false)));
     else
-      AAC_TRY((waver_launch_ns<H, NT, H, double>(ctx, P, P.nstrip * nchunk, sl, st, s, gen)));
+      AAC_TRY((waver_launch_ns<H, NT, H, double>(ctx, P, P.nstrip * nchunk, sl, st, s, gen, clu)));
   }
   for (int a = 0; a < naux; ++a) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));

@@ -19,6 +19,7 @@
 // discarded; out-of-domain points hold zero and carry zero face weights, so they stay zero.
 #pragma once
 
+#include "tma.cuh"
 #include "wave.cuh"
 
 #ifndef WR_PAIRX
@@ -39,6 +40,64 @@ template <int NT>
 struct WRGeom {
   static constexpr int XW = NT + 2;                     // exchange row: zero pad at both ends
 };
+
+// Thread-block cluster helpers (k_waver with CLU: the strips of one row chunk form a cluster and
+// exchange their edge columns through distributed shared memory instead of recomputing an x-halo).
+__device__ __forceinline__ uint32_t wr_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// st.async: store into a neighbour CTA's shared memory and complete `bytes` of the transaction
+// count of its mbarrier (the consumer waits on its own barrier at CTA scope -- no cluster-scope
+// acquire, which would invalidate L1 on every step). Predicated inside the asm (no branch: a
+// divergent branch per level made ptxas fence every level into its own reconvergence region),
+// and no "memory" clobber: the stores only touch the neighbour's pad slots, which this thread
+// never reads.
+#define WR_STA(TY, REGS, ...)                                                                         \
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %0, 0;\n@q st.async.shared::cluster.mbarrier::complete_tx::bytes" \
+               TY " [%1], " REGS ", [%2];\n}" ::"r"((int)p), "r"(a), "r"(bar), __VA_ARGS__)
+__device__ __forceinline__ void wr_st_async(bool p, uint32_t a, double v, uint32_t bar) {
+  WR_STA(".f64", "%3", "d"(v));
+}
+__device__ __forceinline__ void wr_st_async(bool p, uint32_t a, double2 v, uint32_t bar) {
+  WR_STA(".v2.f64", "{%3, %4}", "d"(v.x), "d"(v.y));
+}
+__device__ __forceinline__ void wr_st_async(bool p, uint32_t a, float v, uint32_t bar) {
+  WR_STA(".f32", "%3", "f"(v));
+}
+__device__ __forceinline__ void wr_st_async(bool p, uint32_t a, float2 v, uint32_t bar) {
+  WR_STA(".v2.f32", "{%3, %4}", "f"(v.x), "f"(v.y));
+}
+#undef WR_STA
+// Cluster-side state of a thread (k_waver CLU). Exchange rows and step barriers are indexed by
+// the step's phase mod 3 (three buffers): a strip sends the values of step tau + 1 during step
+// tau, as soon as each level produces them, so they have most of a step to cross the cluster.
+struct WRClu {
+  uint32_t rem;      // edge threads: the neighbour strip's exchange rows (shared::cluster), else 0
+  uint32_t rbar;     // the neighbour's step barriers (shared::cluster)
+  int roff;          // the neighbour's pad slot this thread fills (0 or XW - 1)
+  uint64_t* bar;     // this CTA's step barriers [3][WRC_G]
+  uint32_t tx0, tx1; // bytes the neighbours deliver per step to barrier group 0 / 1
+  int tau0, nend;    // first step; one past the last step the loop runs
+};
+// Barrier groups per step: levels 1..NS/2 and NS/2+1..NS complete separate barriers, so the
+// edge threads wait for the second half only before level NS/2 + 1 (followed by a CTA barrier:
+// the wait stays outside the branch-free level code).
+#ifndef WRC_SPLIT
+#define WRC_SPLIT 1                                      // 0: one barrier group per step
+#endif
+template <int NS> struct WRCG {
+  static constexpr int G = (WRC_SPLIT && NS >= 4) ? 2 : 1;
+  static constexpr int H0 = G == 2 ? NS / 2 : NS;
+};
+
+__device__ __forceinline__ void wr_cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void wr_cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 struct WRRow { double w0, w1, xl, xh, yl, yh, s0, s1, m0, m1; };
 
@@ -157,19 +216,41 @@ template <int PH, int A>
 struct WSlot { static constexpr int v = ((A - PH) % 3 + 3) % 3; };
 
 // One step tau (tau mod 3 == PH) of the wavefront.
-template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, int PH, typename T>
+template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, bool CLU, int PH, typename T>
 __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, const WBlk& B,
                                            const double* __restrict__ what, const Geo& g, const WSlab& sl,
                                            T* xch, int t, int x, bool colin, bool colout, int y0,
-                                           int y1, int tau, int tau1, double e0, double dB, WRRow& nxt) {
+                                           int y1, int tau, int tau1, double e0, double dB, WRRow& nxt,
+                                           const WRClu& C) {
   constexpr int XW = WRGeom<NT>::XW;
   constexpr int NP = CPLX ? 2 : 1;
   constexpr int S0 = WSlot<PH, 0>::v, S1 = WSlot<PH, 1>::v, S2 = WSlot<PH, 2>::v;
-  T* xb = xch + (tau & 1) * (NS * NP * XW) + 1 + t;
+  constexpr int NB = CLU ? 3 : 2;                       // exchange buffers
+  const int buf = CLU ? PH : (tau & 1);
+  T* xb = xch + buf * (NS * NP * XW) + 1 + t;
   // complex blocks: the (Re, Im) pair of a column is one 2-vector in the exchange rows (one
   // STS.128 + two LDS.128 per level instead of two STS.64 + four LDS.64)
   using T2 = typename WRVec<T>::T2;
-  T2* xb2 = reinterpret_cast<T2*>(xch) + (tau & 1) * (NS * XW) + 1 + t;
+  T2* xb2 = reinterpret_cast<T2*>(xch) + buf * (NS * XW) + 1 + t;
+  (void)NB;
+  // cluster: values of step tau + 1 go to the neighbour's buffer (PH + 1) % 3, completing bytes
+  // on its barrier PH (group of the level); sent only if step tau + 1 runs
+  constexpr int G = WRCG<NS>::G, H0 = WRCG<NS>::H0;
+  const bool snd = CLU && C.rem && tau + 1 < C.nend;
+  auto send = [&](int k, T v0, T v1) {                  // index k (1-based) of step tau + 1
+    if constexpr (CLU) {
+      constexpr int bn = (PH + 1) % 3;
+      const uint32_t rb = C.rbar + 8u * (uint32_t)(PH * G + (k > H0 ? 1 : 0));
+      if constexpr (CPLX && WR_PAIRX) {
+        wr_st_async(snd, C.rem + (uint32_t)(((bn * NS + (k - 1)) * XW + C.roff) * sizeof(T2)), WRVec<T>::make(v0, v1),
+                    rb);
+      } else {
+        wr_st_async(snd, C.rem + (uint32_t)(((bn * NS * NP + (k - 1) * NP) * XW + C.roff) * sizeof(T)), v0, rb);
+        if (CPLX)
+          wr_st_async(snd, C.rem + (uint32_t)(((bn * NS * NP + (k - 1) * NP + 1) * XW + C.roff) * sizeof(T)), v1, rb);
+      }
+    }
+  };
   // (1) publish the newest row of every level (L_i at row tau - i; age 1 after this step's
   //     push) for the x-neighbours
 #pragma unroll
@@ -180,6 +261,11 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
 #pragma unroll
       for (int e = 0; e < NP; ++e) xb[((i - 1) * NP + e) * XW] = S.L[i][S1][e];
     }
+  }
+  // cluster: the phases of step tau + 1 complete when the neighbours' bytes have landed
+  if (CLU && t == NT / 2 && tau + 1 < C.nend) {
+    mbar_arrive_expect_tx(C.bar + PH * G, C.tx0);
+    if (G == 2) mbar_arrive_expect_tx(C.bar + PH * G + 1, C.tx1);
   }
   // (2) rows move one level down; row tau enters (L_0, L_1 and its operands)
 #pragma unroll
@@ -220,11 +306,21 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
       S.L[0][S0][1] = T(cur.m1);
     }
   }
+  send(1, S.L[1][S0][0], CPLX ? S.L[1][S0][1] : T(0));
+  // cluster: step tau's values from the neighbours (barrier (PH + 2) % 3; none at the first step)
+  constexpr int BW = (PH + 2) % 3;
+  const bool rcv = CLU && C.rem && tau > C.tau0;
+  const uint32_t par = (uint32_t)(((tau - C.tau0 - 1) / 3) & 1);
+  if (rcv) mbar_wait(C.bar + BW * G, par);
   __syncthreads();
   // (3) levels: L_{i+1} at row r = tau - i
   const T li = T(B.li);
 #pragma unroll
   for (int i = 1; i <= NS; ++i) {
+    if (G == 2 && i == H0 + 1) {
+      if (rcv) mbar_wait(C.bar + BW * G + 1, par);
+      __syncthreads();
+    }
     const T* xr = xb + ((i - 1) * NP) * XW;
     const int e1 = CPLX ? 1 : 0;
     T nl0, nl1, nr0, nr1;                                // x-neighbours (left, right)
@@ -262,15 +358,16 @@ __device__ __forceinline__ void waver_step(WRState<NS, CPLX ? 2 : 1, T>& S, cons
     } else {                                             // push: overwrites the oldest row
       S.L[i + 1][S0][0] = o0;
       if (CPLX) S.L[i + 1][S0][1] = o1;
+      send(i + 1, o0, o1);
     }
   }
 }
 
 // All ns steps of one block over this CTA's strip x row chunk.
-template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
+template <int NT, int NS, bool CPLX, bool GEN, bool VIRT, bool CLU, typename T>
 __device__ __forceinline__ void waver_block(const WBlk& B, const double* __restrict__ what, const Geo& g,
                                             const WSlab& sl, T* xch, int t, int x, bool colin,
-                                            bool colout, int y0, int y1) {
+                                            bool colout, int y0, int y1, WRClu& C) {
   constexpr int NP = CPLX ? 2 : 1;
   WRState<NS, NP, T> S;
 #pragma unroll
@@ -290,12 +387,14 @@ __device__ __forceinline__ void waver_block(const WBlk& B, const double* __restr
   // rows past the chunk, which are never stored). Phase 0 at tau0 (shifted into [0, 3) so the
   // slot of a row never depends on the sign of tau).
   const int tau0 = y0 - NS, tau1 = y1 + NS;
+  C.tau0 = tau0;
+  C.nend = tau0 + 3 * ((tau1 - tau0 + 2) / 3);
   WRRow nxt;
   waver_load<CPLX, GEN, VIRT>(B, what, g, sl, x, colin, tau0, nxt);
   for (int tau = tau0; tau < tau1; tau += 3) {
-    waver_step<NT, NS, CPLX, GEN, VIRT, 0, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau, tau1, e0, dB, nxt);
-    waver_step<NT, NS, CPLX, GEN, VIRT, 1, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 1, tau1, e0, dB, nxt);
-    waver_step<NT, NS, CPLX, GEN, VIRT, 2, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 2, tau1, e0, dB, nxt);
+    waver_step<NT, NS, CPLX, GEN, VIRT, CLU, 0, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau, tau1, e0, dB, nxt, C);
+    waver_step<NT, NS, CPLX, GEN, VIRT, CLU, 1, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 1, tau1, e0, dB, nxt, C);
+    waver_step<NT, NS, CPLX, GEN, VIRT, CLU, 2, T>(S, B, what, g, sl, xch, t, x, colin, colout, y0, y1, tau + 2, tau1, e0, dB, nxt, C);
   }
 }
 
@@ -315,9 +414,21 @@ struct WROne {
 
 // Shared memory: the x-exchange rows [2 buffers][NS levels][planes][NT + 2].
 template <int NT, typename T>
-constexpr size_t waver_smem(int ns, int np) { return (size_t)2 * ns * np * (NT + 2) * sizeof(T); }
+__host__ __device__ constexpr size_t waver_smem(int ns, int np) { return (size_t)2 * ns * np * (NT + 2) * sizeof(T); }
+// + the two step barriers of the cluster kernel
+template <int NT, typename T>
+__host__ __device__ constexpr size_t waver_smem_clu(int ns, int np) {
+  return (size_t)3 * ns * np * (NT + 2) * sizeof(T) + 8 * 3 * ((WRC_SPLIT && ns >= 4) ? 2 : 1);
+}
 
-template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT, typename T>
+// CLU (one rank, nx <= 8 NT): the nstrip strips of a row chunk are one thread-block cluster and
+// the strips carry NO x-halo -- every step each strip's edge threads also store their columns
+// into the neighbouring strips' pad slots (st.async, completing bytes on the neighbour's step
+// barrier), and the edge threads wait on their own CTA's barrier (CTA scope) before the levels
+// read the pads. Only neighbours couple (no cluster-wide barrier per step: barrier.cluster with
+// its cluster-scope acquire measured 10.1 vs 8.3 ms per headline solve -- it also invalidates L1).
+// The points computed and their operands are those of the halo kernel: bit-identical results.
+template <int H, int NT, int NS, bool CPLX, bool GEN, bool VIRT, bool CLU, typename T>
 __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_constant__ WROne P,
                                                             const double* __restrict__ what,
                                                             const IterState* st, WSlab sl) {
@@ -327,7 +438,7 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   const WBlk& B = P.b;
   const int t = threadIdx.x;
   // x-halo of NS columns per side: a wrong edge value reaches one column further per level
-  constexpr int HX = NS;
+  constexpr int HX = CLU ? 0 : NS;
   constexpr int TX = NT - 2 * HX;
   const int cta = (int)blockIdx.x;
   const int strip = cta % P.nstrip, chunk = cta / P.nstrip;
@@ -336,21 +447,51 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   const bool colout = t >= HX && t < NT - HX && x < g.nx;
   const int y0 = P.ybeg + chunk * P.ly;
   const int y1 = min(y0 + P.ly, P.yend);
-  // zero pads of the exchange rows (never written)
+  // zero pads of the exchange rows (never written without a cluster; with one, written by the
+  // neighbouring strips only -- the strips at the domain edges keep zero there)
   constexpr int XW = NT + 2;
   if constexpr (CPLX && WR_PAIRX) {                     // rows of XW (Re, Im) pairs
     using T2 = typename WRVec<T>::T2;
     T2* w2 = reinterpret_cast<T2*>(wsm);
-    for (int k = t; k < 2 * NS; k += NT) {
+    for (int k = t; k < (CLU ? 3 : 2) * NS; k += NT) {
       w2[k * XW] = WRVec<T>::make(T(0), T(0));
       w2[k * XW + XW - 1] = WRVec<T>::make(T(0), T(0));
     }
   } else {
-    constexpr int NROW = 2 * NS * (CPLX ? 2 : 1);
+    constexpr int NROW = (CLU ? 3 : 2) * NS * (CPLX ? 2 : 1);
     for (int k = t; k < NROW; k += NT) {
       wsm[k * XW] = T(0);
       wsm[k * XW + XW - 1] = T(0);
     }
   }
-  waver_block<NT, NS, CPLX, GEN, VIRT, T>(B, what, g, sl, wsm, t, x, colin, colout, y0, y1);
+  WRClu C{0u, 0u, 0, nullptr, 0u, 0u, 0, 0};
+  if constexpr (CLU) {
+    constexpr int G = WRCG<NS>::G, H0 = WRCG<NS>::H0;
+    C.bar = reinterpret_cast<uint64_t*>(wsm_raw + waver_smem_clu<NT, T>(NS, CPLX ? 2 : 1) - 8 * 3 * G);
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(wsm);
+    const uint32_t bb = (uint32_t)__cvta_generic_to_shared(C.bar);
+    if (t == 0 && strip > 0) {
+      C.rem = wr_mapa(lb, (uint32_t)(strip - 1));
+      C.rbar = wr_mapa(bb, (uint32_t)(strip - 1));
+      C.roff = XW - 1;
+    } else if (t == NT - 1 && strip < P.nstrip - 1) {
+      C.rem = wr_mapa(lb, (uint32_t)(strip + 1));
+      C.rbar = wr_mapa(bb, (uint32_t)(strip + 1));
+      C.roff = 0;
+    }
+    const int nnb = (strip > 0) + (strip < P.nstrip - 1);
+    C.tx0 = (uint32_t)(nnb * H0 * (CPLX ? 2 : 1) * (int)sizeof(T));
+    C.tx1 = (uint32_t)(nnb * (NS - H0) * (CPLX ? 2 : 1) * (int)sizeof(T));
+    if (t == 0) {
+      for (int k = 0; k < 3 * G; ++k) mbar_init(C.bar + k, 1);
+      fence_mbar_init();
+    }
+    wr_cluster_arrive();                                 // barriers initialised and pads zeroed
+    wr_cluster_wait();                                   // everywhere before any neighbour writes
+  }
+  waver_block<NT, NS, CPLX, GEN, VIRT, CLU, T>(B, what, g, sl, wsm, t, x, colin, colout, y0, y1, C);
+  if constexpr (CLU) {                                   // (every store into this CTA was waited
+    wr_cluster_arrive();                                 //  for; keep the cluster alive anyway until
+    wr_cluster_wait();                                   //  all strips are done)
+  }
 }

@@ -475,6 +475,35 @@ def test_precond_sweep_organisations(monkeypatch, kw, method, k, h, ly):
     s.close()
 
 
+# The cluster wavefront (k_waver CLU: the strips of a row chunk exchange edge columns through
+# distributed shared memory, no x-halo) computes the same points from the same operands as the
+# halo kernel: bit-identical, for 2..8 strips per row, ragged last strips and short chunks.
+CLUSTER = [
+    (dict(shape=(1, 96, 1024)), "nc2", 8, "0"),     # 8 full strips (the headline width)
+    (dict(shape=(1, 70, 1000)), "nc2", 8, "16"),    # 8 strips, ragged last strip, 5 chunks
+    (dict(shape=(1, 40, 300)), "nc1", 20, "0"),     # 3 strips, two passes (nc1 k=20)
+    (dict(shape=(1, 33, 129)), "nc2", 8, "9"),      # 2 strips, the second one column wide
+]
+
+
+@pytest.mark.parametrize("kw,method,k,ly", CLUSTER)
+def test_cluster_wavefront_bit_identical(monkeypatch, kw, method, k, ly):
+    monkeypatch.setenv("AAC_WAVE_LY", ly)
+    p = synth.make_problem("headline", **kw)
+    r = np.random.default_rng(11).standard_normal((p.ell,) + p.shape)
+    z = {}
+    for clu in ("1", "0"):
+        monkeypatch.setenv("AAC_WAVE_CLUSTER", clu)
+        s = _solver(p)
+        z[clu] = s.precond_apply(method, k, _dev(r, p.ell)).cpu().numpy()
+        s.close()
+    assert np.array_equal(z["1"], z["0"])
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    assert _rel(z["1"], ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)) <= 1e-12
+
+
 # ---------------------------------------------------------------- full-size 3D (configs[4])
 def _sub_weights(w, lo, hi):
     """Face weights of the box [lo, hi) of the full grid (faces inside the box only): the box
