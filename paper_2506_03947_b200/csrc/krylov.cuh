@@ -37,9 +37,12 @@ struct IterState {
 // attribute may start while its predecessor drains; it waits here for the predecessor's completion
 // (and memory flush) before touching anything, then lets its own successor launch. A no-op for
 // kernels launched normally.
+#ifndef GRIDDEP_EARLY
+#define GRIDDEP_EARLY 1
+#endif
 __device__ __forceinline__ void griddep() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (GRIDDEP_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __global__ void k_publish(const unsigned* __restrict__ src, unsigned* dst, int n) {

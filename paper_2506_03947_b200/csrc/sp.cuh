@@ -1533,7 +1533,22 @@ static int sp_solve_t(aac_ctx* ctx, int k, double* zbase, long long zjs, const I
     if (sp_fused_on(ctx, DIM)) {
       const int nsx = ((ctx->geo.nx + 1) / 2 + SPF_T - 1) / SPF_T, nyp = (ctx->geo.ny + 1) / 2;
       const int nry = std::min(nyp, std::max(1, spf_cps() * ctx->num_sms / (nsx * h)));
-      if (ctx->geo.nx % 2 == 0)
+      static const bool tma_off = getenv("AAC_SPF_TMA") && atoi(getenv("AAC_SPF_TMA")) == 0;
+      if (ctx->geo.nx % 2 == 0 && !tma_off) {
+        // rows staged by the bulk-copy engine; ~SPT_MINB CTAs per SM, chunks of nyc aggregate rows
+        static thread_local bool attr = false;
+        if (!attr) {
+          CUDA_TRY(ctx, cudaFuncSetAttribute(k_spf_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)spt_smem()));
+          attr = true;
+        }
+        const int nch = std::min(nyp, std::max(1, SPT_MINB * ctx->num_sms / (nsx * h)));
+        const int nyc = (nyp + nch - 1) / nch;
+        const int nchr = (nyp + nyc - 1) / nyc;
+        LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
+               launch_pdl(k_spf_apply_tma, dim3(nsx * nchr, h), dim3(SPF_T), spt_smem(), ctx->stream, ctx->geo, vecs(),
+                          S, P->red2, nsx, nyc));
+      } else if (ctx->geo.nx % 2 == 0)
         LAUNCH(ctx, KID_SP_STENCIL, 2.0 * V,
                launch_pdl(k_spf_apply<true>, dim3(nsx * nry, h), dim3(SPF_T), 0, ctx->stream, ctx->geo, vecs(), S, P->red2, nsx));
       else

@@ -18,7 +18,12 @@
 // association of the fixed-order dot reduction).
 #pragma once
 
+#include "tma.cuh"
+
 constexpr int SPF_T = 128;                     // threads = aggregate columns per CTA
+#ifndef SPF_MINB
+#define SPF_MINB 4                             // __launch_bounds__ min CTAs per SM (register cap)
+#endif
 
 struct SpfUpd {                                // level 0, inner iteration: v_{j+1} on the fly
   const double* SZ;
@@ -119,39 +124,60 @@ struct SpfW {
   double wyP0, wyP1;
 };
 
+// Raw loads of the face weights and counts (issued first; spf_wfin forms SpfW from them -- its
+// shuffles wait for the loads, so a kernel issues its other loads in between).
+struct SpfWRaw {
+  double2 xa, xb, ya, yb, ka, kb, yp;
+  double xa2, xb2;
+};
+
 template <bool EVEN, bool CNT = true>
-__device__ __forceinline__ void spf_weights(const Geo& g, const double* cnt, const SpfGeom& G, SpfW& W) {
+__device__ __forceinline__ void spf_wload(const Geo& g, const double* cnt, const SpfGeom& G, SpfWRaw& R) {
   const int nx = g.nx;
-  const double2 xa = spf_l2<EVEN>(g.wx + G.rA, G, nx), xb = spf_l2<EVEN>(g.wx + G.rB, G, nx);
-  const double2 ya = spf_l2<EVEN>(g.wy + G.rA, G, nx), yb = spf_l2<EVEN>(g.wy + G.rB, G, nx);
-  const double2 ka = CNT ? spf_l2<EVEN>(cnt + G.rA, G, nx) : make_double2(1.0, 1.0);
-  const double2 kb = CNT ? spf_l2<EVEN>(cnt + G.rB, G, nx) : make_double2(1.0, 1.0);
-  const double2 yp = spf_l2<EVEN>(g.wy + G.rB + nx, G, nx);   // row y0 + 2 or the zero padding row
+  R.xa = spf_l2<EVEN>(g.wx + G.rA, G, nx);
+  R.xb = spf_l2<EVEN>(g.wx + G.rB, G, nx);
+  R.ya = spf_l2<EVEN>(g.wy + G.rA, G, nx);
+  R.yb = spf_l2<EVEN>(g.wy + G.rB, G, nx);
+  R.ka = CNT ? spf_l2<EVEN>(cnt + G.rA, G, nx) : make_double2(1.0, 1.0);
+  R.kb = CNT ? spf_l2<EVEN>(cnt + G.rB, G, nx) : make_double2(1.0, 1.0);
+  R.yp = spf_l2<EVEN>(g.wy + G.rB + nx, G, nx);   // row y0 + 2 or the zero padding row
   // face (c0+1 | c0+2): lane + 1's wx[c0'], lane 31 loads it (c0 + 2 <= nx: wx has nx + 1 entries
   // per row position in the padded layout)
   const int c2 = min(G.c0 + 2, nx);
-  const double xa2 = __ldg(g.wx + G.rA + c2), xb2 = __ldg(g.wx + G.rB + c2);
+  R.xa2 = __ldg(g.wx + G.rA + c2);
+  R.xb2 = __ldg(g.wx + G.rB + c2);
+}
+
+__device__ __forceinline__ void spf_wfin(const Geo& g, const SpfGeom& G, const SpfWRaw& R, SpfW& W) {
+  const int nx = g.nx;
   const bool in = G.v0;
   // (lane + 1 outside the level: its clamped load is not a face of this row -- shuffle zero)
-  const double na = __shfl_down_sync(0xffffffffu, in ? xa.x : 0.0, 1);
-  const double nb = __shfl_down_sync(0xffffffffu, in ? xb.x : 0.0, 1);
-  W.wxA0 = in ? xa.x : 0.0;
-  W.wxA1 = in ? xa.y : 0.0;
-  W.wxA2 = G.lane == 31 ? (G.c0 + 2 <= nx ? xa2 : 0.0) : na;
-  W.wyA0 = in ? ya.x : 0.0;
-  W.wyA1 = in ? ya.y : 0.0;
-  W.kA0 = ka.x;
-  W.kA1 = ka.y;
+  const double na = __shfl_down_sync(0xffffffffu, in ? R.xa.x : 0.0, 1);
+  const double nb = __shfl_down_sync(0xffffffffu, in ? R.xb.x : 0.0, 1);
+  W.wxA0 = in ? R.xa.x : 0.0;
+  W.wxA1 = in ? R.xa.y : 0.0;
+  W.wxA2 = G.lane == 31 ? (G.c0 + 2 <= nx ? R.xa2 : 0.0) : na;
+  W.wyA0 = in ? R.ya.x : 0.0;
+  W.wyA1 = in ? R.ya.y : 0.0;
+  W.kA0 = R.ka.x;
+  W.kA1 = R.ka.y;
   const bool inB = in && G.r1;
-  W.wxB0 = inB ? xb.x : 0.0;
-  W.wxB1 = inB ? xb.y : 0.0;
-  W.wxB2 = G.lane == 31 ? (G.c0 + 2 <= nx && G.r1 ? xb2 : 0.0) : (G.r1 ? nb : 0.0);
-  W.wyB0 = inB ? yb.x : 0.0;
-  W.wyB1 = inB ? yb.y : 0.0;
-  W.kB0 = kb.x;
-  W.kB1 = kb.y;
-  W.wyP0 = inB ? yp.x : 0.0;
-  W.wyP1 = inB ? yp.y : 0.0;
+  W.wxB0 = inB ? R.xb.x : 0.0;
+  W.wxB1 = inB ? R.xb.y : 0.0;
+  W.wxB2 = G.lane == 31 ? (G.c0 + 2 <= nx && G.r1 ? R.xb2 : 0.0) : (G.r1 ? nb : 0.0);
+  W.wyB0 = inB ? R.yb.x : 0.0;
+  W.wyB1 = inB ? R.yb.y : 0.0;
+  W.kB0 = R.kb.x;
+  W.kB1 = R.kb.y;
+  W.wyP0 = inB ? R.yp.x : 0.0;
+  W.wyP1 = inB ? R.yp.y : 0.0;
+}
+
+template <bool EVEN, bool CNT = true>
+__device__ __forceinline__ void spf_weights(const Geo& g, const double* cnt, const SpfGeom& G, SpfW& W) {
+  SpfWRaw R;
+  spf_wload<EVEN, CNT>(g, cnt, G, R);
+  spf_wfin(g, G, R, W);
 }
 
 // ---- reductions of the fused kernels ----------------------------------------------------------
@@ -265,7 +291,7 @@ __device__ __forceinline__ void spf_reduce_pair(const SpStepCtx& S, const SpfRed
 // A_l(s) u = m u + sum_f w_f (u - u_nb), m = (1 + s) cnt -- k_mg_smooth0 + k_mg_restrict_pair.
 // A neighbour outside the level is the point itself (its face weight is zero).
 template <bool EVEN>
-__global__ void __launch_bounds__(SPF_T, 4) k_spf_restrict(Geo g, Geo gc, const double* __restrict__ cnt,
+__global__ void __launch_bounds__(SPF_T, SPF_MINB) k_spf_restrict(Geo g, Geo gc, const double* __restrict__ cnt,
                                                            const double* __restrict__ dinv, SpConst K, MgIo io,
                                                            const double* bl, double* bc, SpfUpd U, int nsx,
                                                            const IterState* st) {
@@ -361,7 +387,7 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_restrict(Geo g, Geo gc, const 
 // u = x + P x_c (x = omega b / D), x2 = u + omega (b - A_l(s) u) / D; level 0: x2 -> io.out
 // and the per-plane dot <x2, b> (scalar step B by the last CTA) -- k_mg_prolong_post_pair2.
 template <bool EVEN>
-__global__ void __launch_bounds__(SPF_T, 4) k_spf_prolong_post(Geo g, Geo gc, const double* __restrict__ cnt,
+__global__ void __launch_bounds__(SPF_T, SPF_MINB) k_spf_prolong_post(Geo g, Geo gc, const double* __restrict__ cnt,
                                                                const double* __restrict__ dinv, MgIo io,
                                                                const double* bl, const double* __restrict__ xc,
                                                                double* x2l, SpStepCtx S, SpfRed R, int level0,
@@ -476,7 +502,7 @@ __device__ __forceinline__ void spf_reduce_apply(const SpStepCtx& S, const SpfRe
 }
 
 template <bool EVEN>
-__global__ void __launch_bounds__(SPF_T, 4) k_spf_apply(Geo g, SpVec v, SpStepCtx S, SpfRed R, int nsx) {
+__global__ void __launch_bounds__(SPF_T, SPF_MINB) k_spf_apply(Geo g, SpVec v, SpStepCtx S, SpfRed R, int nsx) {
   griddep();
   if (S.st && S.st->done) return;
   const int pair = blockIdx.y, ell = S.K.ell, h = ell / 2;
@@ -499,8 +525,6 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_apply(Geo g, SpVec v, SpStepCt
   const bool idle = real ? (stop0 && stop1) : stop0;
   for (int Y = blockIdx.x / nsx; Y < nyp && !idle; Y += nry) {
     const SpfGeom G = spf_geom(g, nsx, Y);
-    SpfW W;
-    spf_weights<EVEN, false>(g, nullptr, G, W);
     // u of rows M, A, B, P and of the warp-edge column of rows A, B, for one plane
     auto rows = [&](const double* u, double2& a, double2& b, double2& mm, double2& pp, double& ea, double& eb) {
       a = spf_l2<EVEN>(u + G.rA, G, nx);
@@ -514,6 +538,11 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_apply(Geo g, SpVec v, SpStepCt
     double ea0, eb0, ea1, eb1;
     rows(u0p, a0, b0, m0, p0, ea0, eb0);
     rows(u1p, a1, b1, m1, p1, ea1, eb1);
+    // the weights after the planes' loads: their shuffles wait for the weight loads only
+    SpfWRaw WR;
+    spf_wload<EVEN, false>(g, nullptr, G, WR);
+    SpfW W;
+    spf_wfin(g, G, WR, W);
     // (A u) at the four points of one plane in apply_Av's order: c + sum_f w_f (c - nb_f)
     auto av4 = [&](const double2& A, const double2& B, const double2& M, const double2& P, double ea, double eb,
                    double out[4]) {
@@ -577,6 +606,183 @@ __global__ void __launch_bounds__(SPF_T, 4) k_spf_apply(Geo g, SpVec v, SpStepCt
     if (stop1) dot1 = 0.0;
   }
   spf_reduce_apply(S, R, dot0, dot1, pair);
+}
+
+// ---- K1 with the rows staged by the bulk-copy engine (even nx) --------------------------------
+// k_spf_apply keeps ~16 warps per SM (128 registers) and every operand of an aggregate row in
+// registers: ncu shows it latency-bound (long-scoreboard stalls, 2.1 TB/s). Here a CTA owns a
+// strip of 2 SPF_T fine columns (+2 halo columns each side) and a chunk of aggregate rows of one
+// plane pair, and marches down the chunk: thread 0 streams each fine row (u of both planes, the
+// x- and y-face weights) through a ring of SPT_D row slots with cp.async.bulk + one mbarrier per
+// slot, so the bytes in flight are bounded by shared memory, not registers; the x-neighbours
+// come from the staged row (no shuffles, no warp-edge loads) and every row is loaded once per
+// chunk instead of twice. The arithmetic per point is k_spf_apply's, in its order (columns
+// outside the level hold zero and carry zero face weights, rows outside it are selected away).
+#ifndef SPT_MINB
+#define SPT_MINB 3
+#endif
+constexpr int SPT_D = 8;                       // row slots
+constexpr int SPT_W = 2 * SPF_T + 4;           // staged columns: cb - 2 .. cb + 2 SPF_T + 1
+constexpr int SPT_NA = 4;                      // arrays per row: u (plane a), u (plane b), wx, wy
+
+__host__ __device__ constexpr size_t spt_smem() {
+  return (size_t)SPT_D * SPT_NA * SPT_W * sizeof(double) + SPT_D * sizeof(uint64_t);
+}
+
+__global__ void __launch_bounds__(SPF_T, SPT_MINB) k_spf_apply_tma(Geo g, SpVec v, SpStepCtx S, SpfRed R, int nsx,
+                                                                   int nyc) {
+  // (programmatic dependent launch: wait for the predecessor here, but let the successor launch
+  //  only at the end -- its early CTAs would otherwise compete with this smem-heavy grid: measured
+  //  53.7 vs 48.8 ms per saddle solve)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (S.st && S.st->done) return;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SPT_D * SPT_NA * SPT_W);
+  const int pair = blockIdx.y, ell = S.K.ell, h = ell / 2;
+  const int nx = g.nx, ny = g.ny, t = threadIdx.x;
+  const bool real = pair == 0;
+  const int q[2] = {real ? 0 : 2 * pair - 1, real ? ell - 1 : 2 * pair};
+  const int kbs[2] = {real ? 0 : pair, real ? h : pair};
+  const bool stop0 = S.blk[kbs[0]].stop != 0, stop1 = S.blk[kbs[1]].stop != 0;
+  const double invg = real || stop0 ? 0.0 : 1.0 / S.blk[pair].gamma;
+  const double* u0p = (real ? v.P : v.Zc) + (long long)q[0] * g.N;
+  const double* u1p = (real ? v.P : v.Zc) + (long long)q[1] * g.N;
+  const double ms[2] = {1.0 + S.K.s[q[0]], 1.0 + S.K.s[q[1]]};
+  const double lr = S.K.lre[pair], li = S.K.lim[pair];
+  double* sz0 = v.SZ + (long long)q[0] * g.N;
+  double* sz1 = v.SZ + (long long)q[1] * g.N;
+  double dot0 = 0.0, dot1 = 0.0;
+  const int strip = blockIdx.x % nsx, chunk = blockIdx.x / nsx;
+  const int nyp = (ny + 1) / 2;
+  const int Y0 = chunk * nyc, Y1 = min(Y0 + nyc, nyp);
+  const bool idle = (real ? (stop0 && stop1) : stop0) || Y0 >= Y1;
+  const int cs = strip * 2 * SPF_T - 2;          // fine column of staged column 0
+  const int clo = max(cs, 0), chi = min(cs + SPT_W, nx);
+  const uint32_t bytes = (uint32_t)(chi - clo) * 8u;
+  const int off = clo - cs;
+  // columns outside the level: zero in every slot (the bulk copies never write them)
+  for (int k = t; k < SPT_D * SPT_NA * SPT_W; k += SPF_T) {
+    const int c = cs + k % SPT_W;
+    if (c < 0 || c >= nx) sm[k] = 0.0;
+  }
+  if (t == 0) {
+    for (int s = 0; s < SPT_D; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int r0 = 2 * Y0 - 1, nrow = 2 * (Y1 - Y0) + 2;   // fine rows r0 .. r0 + nrow - 1
+  auto issue = [&](int i) {                      // relative row i into slot i % SPT_D
+    const int r = r0 + i, s = i % SPT_D;
+    double* d = sm + (size_t)s * SPT_NA * SPT_W + off;
+    if (r >= 0 && r < ny) {
+      mbar_arrive_expect_tx(&bar[s], 4u * bytes);
+      const long long ro = (long long)r * nx + clo;
+      bulk_g2s(d, u0p + ro, bytes, &bar[s]);
+      bulk_g2s(d + SPT_W, u1p + ro, bytes, &bar[s]);
+      bulk_g2s(d + 2 * SPT_W, g.wx + ro, bytes, &bar[s]);
+      bulk_g2s(d + 3 * SPT_W, g.wy + ro, bytes, &bar[s]);
+    } else {
+      mbar_arrive(&bar[s]);                      // (row outside the level: never read)
+    }
+  };
+  if (!idle) {
+    if (t == 0)
+      for (int i = 0; i < min(SPT_D, nrow); ++i) issue(i);
+    const int c0 = 2 * (strip * SPF_T + t);
+    const bool v0 = c0 < nx, v1 = c0 + 1 < nx;
+    const int j0 = c0 - cs;                      // staged column of c0
+    for (int Y = Y0; Y < Y1; ++Y) {
+      const int k = Y - Y0;
+      for (int i = (k == 0 ? 0 : 2 * k + 2); i <= 2 * k + 3; ++i)
+        mbar_wait(&bar[i % SPT_D], (uint32_t)((i / SPT_D) & 1));
+      const int y0 = 2 * Y;
+      const bool r1 = y0 + 1 < ny, rm = Y > 0, rp = y0 + 2 < ny;
+      const double* sM = sm + (size_t)((2 * k) % SPT_D) * SPT_NA * SPT_W;
+      const double* sA = sm + (size_t)((2 * k + 1) % SPT_D) * SPT_NA * SPT_W;
+      const double* sB = r1 ? sm + (size_t)((2 * k + 2) % SPT_D) * SPT_NA * SPT_W : sA;
+      const double* sP = sm + (size_t)((2 * k + 3) % SPT_D) * SPT_NA * SPT_W;
+      // face weights (k_spf_apply's SpfW without the counts)
+      const bool inB = v0 && r1;
+      const double* wxA = sA + 2 * SPT_W + j0;
+      const double* wyA = sA + 3 * SPT_W + j0;
+      const double* wxB = sB + 2 * SPT_W + j0;
+      const double* wyB = sB + 3 * SPT_W + j0;
+      const double wxA0 = v0 ? wxA[0] : 0.0, wxA1 = v0 ? wxA[1] : 0.0;
+      const double wxA2 = c0 + 2 < nx ? wxA[2] : 0.0;
+      const double wyA0 = v0 ? wyA[0] : 0.0, wyA1 = v0 ? wyA[1] : 0.0;
+      const double wxB0 = inB ? wxB[0] : 0.0, wxB1 = inB ? wxB[1] : 0.0;
+      const double wxB2 = (c0 + 2 < nx && r1) ? wxB[2] : 0.0;
+      const double wyB0 = inB ? wyB[0] : 0.0, wyB1 = inB ? wyB[1] : 0.0;
+      const double wyP0 = (inB && rp) ? sP[3 * SPT_W + j0] : 0.0;
+      const double wyP1 = (inB && rp) ? sP[3 * SPT_W + j0 + 1] : 0.0;
+      auto one = [&](double c, double xw, double xe, double xn, double xs, double fw, double fe, double fn, double fs) {
+        double acc = c;
+        acc = fma(fw, c - xw, acc);
+        acc = fma(fe, c - xe, acc);
+        acc = fma(fn, c - xn, acc);
+        acc = fma(fs, c - xs, acc);
+        return acc;
+      };
+      double cv[2][4], Av[2][4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double* a = sA + e * SPT_W + j0;
+        const double* b = sB + e * SPT_W + j0;
+        const double* m = (rm ? sM : sA) + e * SPT_W + j0;
+        const double* pp = (rp ? sP : sB) + e * SPT_W + j0;
+        const double a0 = a[0], a1 = a[1], b0 = b[0], b1 = b[1];
+        cv[e][0] = a0; cv[e][1] = a1; cv[e][2] = b0; cv[e][3] = b1;
+        Av[e][0] = one(a0, a[-1], a1, m[0], b0, wxA0, wxA1, wyA0, wyB0);
+        Av[e][1] = one(a1, a0, a[2], m[1], b1, wxA1, wxA2, wyA1, wyB1);
+        Av[e][2] = one(b0, b[-1], b1, a0, pp[0], wxB0, wxB1, wyB0, wyP0);
+        Av[e][3] = one(b1, b0, b[2], a1, pp[1], wxB1, wxB2, wyB1, wyP1);
+      }
+      const bool ok[4] = {v0, v1, v0 && r1, v1 && r1};
+      double o0[4], o1[4];
+      if (real) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          o0[i] = Av[0][i] + (ms[0] - 1.0) * cv[0][i];
+          o1[i] = Av[1][i] + (ms[1] - 1.0) * cv[1][i];
+          if (ok[i]) {
+            dot0 = fma(cv[0][i], o0[i], dot0);
+            dot1 = fma(cv[1][i], o1[i], dot1);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double us = cv[0][i] * invg, vs = cv[1][i] * invg;
+          const double Au = Av[0][i] * invg, Avv = Av[1][i] * invg;
+          const double Su = li * us + (Avv - lr * vs);
+          const double Sv = (Au - lr * us) - li * vs;
+          o0[i] = Su;
+          o1[i] = Sv;
+          if (ok[i]) dot0 = fma(Sv, vs, fma(Su, us, dot0));
+        }
+      }
+      const long long rA = (long long)y0 * nx, rB = rA + nx;
+      if (!stop0) {
+        spf_st2<true>(sz0 + rA, c0, v0, v1, o0[0], o0[1]);
+        if (r1) spf_st2<true>(sz0 + rB, c0, v0, v1, o0[2], o0[3]);
+      }
+      if (real ? !stop1 : !stop0) {
+        spf_st2<true>(sz1 + rA, c0, v0, v1, o1[0], o1[1]);
+        if (r1) spf_st2<true>(sz1 + rB, c0, v0, v1, o1[2], o1[3]);
+      }
+      __syncthreads();                           // rows 2k, 2k + 1 are free
+      if (t == 0) {
+        if (2 * k + SPT_D < nrow) issue(2 * k + SPT_D);
+        if (2 * k + 1 + SPT_D < nrow) issue(2 * k + 1 + SPT_D);
+      }
+    }
+  }
+  if (real) {
+    if (stop0) dot0 = 0.0;
+    if (stop1) dot1 = 0.0;
+  }
+  spf_reduce_apply(S, R, dot0, dot1, pair);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Tiles of the fused kernels on a level of `ncx` x `ncy` aggregates: strips of SPF_T aggregate
