@@ -410,6 +410,21 @@ def test_sp_kernel_variants_parity(env):
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("tma", ["1", "0"])
+@pytest.mark.parametrize("shape", [(1, 37, 530), (1, 64, 256), (1, 5, 6)])
+def test_sp_k1_staged_rows_parity(tma, shape):
+    """K1 with the rows streamed through the bulk-copy ring (k_spf_apply_tma, even n_x: ragged
+    last strip, odd n_y, chunk boundaries, a grid smaller than one strip) and the register K1
+    (AAC_SPF_TMA=0) against the oracle. A fresh process each (the switch is read once)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _SP_VARIANT.format(root=root).replace("shape=(1, 37, 53)", f"shape={shape!r}")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "AAC_SPF_TMA": tma})
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
+
+
 def test_sp_gmres_parity():
     from oracle import saddle
     p = synth.make_problem("saddle", shape=(1, 64, 48))
