@@ -1375,7 +1375,23 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U 
       // compulsory bytes: b (or the update operands + v_{j+1}), 1/D per block, wx, wy, cnt, b_c
       const double nb = u.on ? (4.0 * (ell - 2) + 2.0) : (double)ell;
       const double bytes = 8.0 * a.g.N * (nb + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
-      if (a.g.nx % 2 == 0)
+      // (AAC_SPF_TMA=2: also the staged-row level-0 restriction -- measured slower: 133 vs 95 us)
+      static const bool rtma_on = getenv("AAC_SPF_TMA") && atoi(getenv("AAC_SPF_TMA")) == 2;
+      if (l == 0 && a.g.nx % 2 == 0 && rtma_on) {
+        // level 0: rows staged by the bulk-copy engine (k_spf_restrict_tma), ~2 CTAs per SM
+        static thread_local bool attr = false;
+        if (!attr) {
+          CUDA_TRY(ctx, cudaFuncSetAttribute(k_spf_restrict_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)spr_smem()));
+          attr = true;
+        }
+        const int nyp = (a.g.ny + 1) / 2;
+        const int nch = std::min(nyp, std::max(1, 2 * ctx->num_sms / (nsx * (ell / 2))));
+        const int nyc = (nyp + nch - 1) / nch, nchr = (nyp + nyc - 1) / nyc;
+        LAUNCH(ctx, KID_SP_MG, bytes,
+               launch_pdl(k_spf_restrict_tma, dim3(nsx * nchr, ell / 2), dim3(SPF_T), spr_smem(), ctx->stream, a.g,
+                          c.g, (const double*)a.cnt, (const double*)a.dinv, P->K, io, c.b, u, nsx, nyc, st));
+      } else if (a.g.nx % 2 == 0)
         LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_restrict<true>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, P->K, io, bl, c.b, u, nsx, st));
       else
@@ -1435,7 +1451,23 @@ static int sp_vcycle(aac_ctx* ctx, const MgIo& io, SpStepCtx S, const SpfUpd& U 
       // of the reduction made one row pair per CTA (10 240 CTAs) 1.4x slower
       if (l == 0) nt = nsx * std::min(c.g.ny, std::max(1, spf_cps() * ctx->num_sms / (nsx * (ell / 2))));
       const double bytes = 8.0 * a.g.N * (2.0 * ell + (ell / 2 + 1) + 3.0) + 8.0 * ell * c.g.N;
-      if (a.g.nx % 2 == 0)
+      // (AAC_SPF_TMA=2: also the staged-row level-0 prolongation -- measured slower: 83 vs 65 us)
+      static const bool ptma_on = getenv("AAC_SPF_TMA") && atoi(getenv("AAC_SPF_TMA")) == 2;
+      if (l == 0 && a.g.nx % 4 == 0 && ptma_on) {
+        // level 0: rows staged by the bulk-copy engine (k_spf_prolong_tma), ~2 CTAs per SM
+        static thread_local bool attr = false;
+        if (!attr) {
+          CUDA_TRY(ctx, cudaFuncSetAttribute(k_spf_prolong_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)spp_smem()));
+          attr = true;
+        }
+        const int nyp = (a.g.ny + 1) / 2;
+        const int nch = std::min(nyp, std::max(1, 2 * ctx->num_sms / (nsx * (ell / 2))));
+        const int nyc = (nyp + nch - 1) / nch, nchr = (nyp + nyc - 1) / nyc;
+        LAUNCH(ctx, KID_SP_MG, bytes,
+               launch_pdl(k_spf_prolong_tma, dim3(nsx * nchr, ell / 2), dim3(SPF_T), spp_smem(), ctx->stream, a.g, c.g,
+                          (const double*)a.cnt, (const double*)a.dinv, io, (const double*)c.x2, S, P->red2, nsx, nyc));
+      } else if (a.g.nx % 2 == 0)
         LAUNCH(ctx, KID_SP_MG, bytes, launch_pdl(k_spf_prolong_post<true>, dim3(nt, ell / 2), dim3(SPF_T), 0, ctx->stream,
                                           a.g, c.g, a.cnt, a.dinv, io, bl, c.x2, a.x2, S, P->red2, l == 0 ? 1 : 0, nsx));
       else

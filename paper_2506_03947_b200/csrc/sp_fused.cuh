@@ -785,6 +785,346 @@ __global__ void __launch_bounds__(SPF_T, SPT_MINB) k_spf_apply_tma(Geo g, SpVec 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ---- level-0 restriction with the rows staged by the bulk-copy engine (even nx) ---------------
+// k_spf_restrict at level 0 (one aggregate row per CTA, every operand in registers) as a
+// row-marching kernel in the organisation of k_spf_apply_tma: per fine row the b operands of
+// both planes (or the update operands SZ, V_j, V_{j-1} of v_{j+1}), 1/D of their blocks and the
+// weights wx, wy, cnt stream through an SPR_D-slot ring; the arithmetic per point is
+// k_spf_restrict's, in its order.
+constexpr int SPR_D = 4;                       // row slots
+constexpr int SPR_NA = 11;                     // [plane 0: a0 a1 a2 d][plane 1: a0 a1 a2 d][wx wy cnt]
+
+__host__ __device__ constexpr size_t spr_smem() {
+  return (size_t)SPR_D * SPR_NA * SPT_W * sizeof(double) + SPR_D * sizeof(uint64_t);
+}
+
+__global__ void __launch_bounds__(SPF_T, 2) k_spf_restrict_tma(Geo g, Geo gc, const double* __restrict__ cnt,
+                                                               const double* __restrict__ dinv, SpConst K, MgIo io,
+                                                               double* bc, SpfUpd U, int nsx, int nyc,
+                                                               const IterState* st) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // (dependents triggered at the end)
+  if (st && st->done) return;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SPR_D * SPR_NA * SPT_W);
+  int pa, pb;
+  sp_pair(K.ell, blockIdx.y, pa, pb);
+  const int pls[2] = {pa, pb};
+  const int nx = g.nx, ny = g.ny, t = threadIdx.x;
+  const long long N = g.N;
+  bool upd[2];
+  int kbs[2];
+  const double* src[2][4];
+  double dc[2], vcf[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int pl = pls[e];
+    kbs[e] = sp_block_of(K.ell, pl);
+    upd[e] = U.on && kbs[e] != 0 && kbs[e] != K.ell / 2 && U.blk[kbs[e]].stop != 1;
+    const long long o = (long long)pl * N;
+    src[e][0] = upd[e] ? U.SZ + o : io.in[pl];
+    src[e][1] = upd[e] ? U.Vc + o : nullptr;
+    src[e][2] = upd[e] ? U.Vp + o : nullptr;
+    src[e][3] = dinv + (long long)kbs[e] * N;
+    dc[e] = upd[e] ? U.blk[kbs[e]].dcoef : 0.0;
+    vcf[e] = upd[e] ? U.blk[kbs[e]].vcoef : 0.0;
+  }
+  const bool dsame = kbs[0] == kbs[1];           // one 1/D row for both planes
+  const int strip = blockIdx.x % nsx, chunk = blockIdx.x / nsx;
+  const int nyp = (ny + 1) / 2;
+  const int Y0 = chunk * nyc, Y1 = min(Y0 + nyc, nyp);
+  const bool idle = Y0 >= Y1;
+  const int cs = strip * 2 * SPF_T - 2;
+  const int clo = max(cs, 0), chi = min(cs + SPT_W, nx);
+  const uint32_t bytes = (uint32_t)(chi - clo) * 8u;
+  const int off = clo - cs;
+  for (int k = t; k < SPR_D * SPR_NA * SPT_W; k += SPF_T) {
+    const int c = cs + k % SPT_W;
+    if (c < 0 || c >= nx) sm[k] = 0.0;
+  }
+  if (t == 0) {
+    for (int s = 0; s < SPR_D; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int r0 = 2 * Y0 - 1, nrow = 2 * (Y1 - Y0) + 2;
+  int ncopy = 3;                                 // arrays per row: wx, wy, cnt + the planes'
+#pragma unroll
+  for (int e = 0; e < 2; ++e) ncopy += (upd[e] ? 3 : 1) + ((e == 1 && dsame) ? 0 : 1);
+  auto issue = [&](int i) {
+    const int r = r0 + i, s = i % SPR_D;
+    double* d = sm + (size_t)s * SPR_NA * SPT_W + off;
+    if (r >= 0 && r < ny) {
+      mbar_arrive_expect_tx(&bar[s], (uint32_t)ncopy * bytes);
+      const long long ro = (long long)r * nx + clo;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int na = upd[e] ? 3 : 1;
+        for (int a = 0; a < na; ++a) bulk_g2s(d + (e * 4 + a) * SPT_W, src[e][a] + ro, bytes, &bar[s]);
+        if (!(e == 1 && dsame)) bulk_g2s(d + (e * 4 + 3) * SPT_W, src[e][3] + ro, bytes, &bar[s]);
+      }
+      bulk_g2s(d + 8 * SPT_W, g.wx + ro, bytes, &bar[s]);
+      bulk_g2s(d + 9 * SPT_W, g.wy + ro, bytes, &bar[s]);
+      bulk_g2s(d + 10 * SPT_W, cnt + ro, bytes, &bar[s]);
+    } else {
+      mbar_arrive(&bar[s]);
+    }
+  };
+  if (!idle) {
+    if (t == 0)
+      for (int i = 0; i < min(SPR_D, nrow); ++i) issue(i);
+    const int X = strip * SPF_T + t, c0 = 2 * X;
+    const bool v0 = c0 < nx, v1 = c0 + 1 < nx;
+    const int j0 = c0 - cs;
+    for (int Y = Y0; Y < Y1; ++Y) {
+      const int k = Y - Y0;
+      for (int i = (k == 0 ? 0 : 2 * k + 2); i <= 2 * k + 3; ++i)
+        mbar_wait(&bar[i % SPR_D], (uint32_t)((i / SPR_D) & 1));
+      const int y0 = 2 * Y;
+      const bool r1 = y0 + 1 < ny, rm = Y > 0, rp = y0 + 2 < ny;
+      const double* sA = sm + (size_t)((2 * k + 1) % SPR_D) * SPR_NA * SPT_W;
+      const double* sB = r1 ? sm + (size_t)((2 * k + 2) % SPR_D) * SPR_NA * SPT_W : sA;
+      const double* sM = rm ? sm + (size_t)((2 * k) % SPR_D) * SPR_NA * SPT_W : sA;
+      const double* sP = rp ? sm + (size_t)((2 * k + 3) % SPR_D) * SPR_NA * SPT_W : sB;
+      const double* sPw = sm + (size_t)((2 * k + 3) % SPR_D) * SPR_NA * SPT_W;
+      const bool inB = v0 && r1;
+      const double* wxA = sA + 8 * SPT_W + j0;
+      const double* wyA = sA + 9 * SPT_W + j0;
+      const double* wxB = sB + 8 * SPT_W + j0;
+      const double* wyB = sB + 9 * SPT_W + j0;
+      const double wxA0 = v0 ? wxA[0] : 0.0, wxA1 = v0 ? wxA[1] : 0.0;
+      const double wxA2 = c0 + 2 < nx ? wxA[2] : 0.0;
+      const double wyA0 = v0 ? wyA[0] : 0.0, wyA1 = v0 ? wyA[1] : 0.0;
+      const double wxB0 = inB ? wxB[0] : 0.0, wxB1 = inB ? wxB[1] : 0.0;
+      const double wxB2 = (c0 + 2 < nx && r1) ? wxB[2] : 0.0;
+      const double wyB0 = inB ? wyB[0] : 0.0, wyB1 = inB ? wyB[1] : 0.0;
+      const double wyP0 = (inB && rp) ? sPw[9 * SPT_W + j0] : 0.0;
+      const double wyP1 = (inB && rp) ? sPw[9 * SPT_W + j0 + 1] : 0.0;
+      const double kA0 = sA[10 * SPT_W + j0], kA1 = sA[10 * SPT_W + j0 + 1];
+      const double kB0 = sB[10 * SPT_W + j0], kB1 = sB[10 * SPT_W + j0 + 1];
+      double acc[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double m = 1.0 + K.s[pls[e]];
+        const int dd = (e == 1 && dsame) ? 3 : e * 4 + 3;
+        // b at staged column jj of a row (the update formed exactly as k_sp_upd1 does)
+        auto bval = [&](const double* row, int jj) {
+          const double a0 = row[(e * 4) * SPT_W + jj];
+          if (!upd[e]) return a0;
+          return a0 - dc[e] * row[(e * 4 + 1) * SPT_W + jj] - vcf[e] * row[(e * 4 + 2) * SPT_W + jj];
+        };
+        auto xval = [&](const double* row, int jj, double b) { return SP_OMEGA * b * row[dd * SPT_W + jj]; };
+        const double bA0 = bval(sA, j0), bA1 = bval(sA, j0 + 1), bB0 = bval(sB, j0), bB1 = bval(sB, j0 + 1);
+        const double bM0 = bval(sM, j0), bM1 = bval(sM, j0 + 1), bP0 = bval(sP, j0), bP1 = bval(sP, j0 + 1);
+        if (upd[e]) {                            // v_{j+1} of the own points
+          double* vn = const_cast<double*>(io.in[pls[e]]);
+          spf_st2<true>(vn + (long long)y0 * nx, c0, v0, v1, bA0, bA1);
+          if (r1) spf_st2<true>(vn + (long long)(y0 + 1) * nx, c0, v0, v1, bB0, bB1);
+        }
+        const double xA0 = xval(sA, j0, bA0), xA1 = xval(sA, j0 + 1, bA1);
+        const double xB0 = xval(sB, j0, bB0), xB1 = xval(sB, j0 + 1, bB1);
+        const double xM0 = xval(sM, j0, bM0), xM1 = xval(sM, j0 + 1, bM1);
+        const double xP0 = xval(sP, j0, bP0), xP1 = xval(sP, j0 + 1, bP1);
+        const double wA = xval(sA, j0 - 1, bval(sA, j0 - 1)), eA = xval(sA, j0 + 2, bval(sA, j0 + 2));
+        const double wB = xval(sB, j0 - 1, bval(sB, j0 - 1)), eB = xval(sB, j0 + 2, bval(sB, j0 + 2));
+        auto res = [&](double c, double b, double xw, double xe, double xn, double xs, double fw, double fe, double fn,
+                       double fs, double kk) {
+          double a = c;
+          a = fma(fw, c - xw, a);
+          a = fma(fe, c - xe, a);
+          a = fma(fn, c - xn, a);
+          a = fma(fs, c - xs, a);
+          a = a + (m * kk - 1.0) * c;
+          return b - a;
+        };
+        double s = 0.0;
+        if (v0) s += res(xA0, bA0, wA, xA1, xM0, xB0, wxA0, wxA1, wyA0, wyB0, kA0);
+        if (v1) s += res(xA1, bA1, xA0, eA, xM1, xB1, wxA1, wxA2, wyA1, wyB1, kA1);
+        if (r1) {
+          if (v0) s += res(xB0, bB0, wB, xB1, xA0, xP0, wxB0, wxB1, wyB0, wyP0, kB0);
+          if (v1) s += res(xB1, bB1, xB0, eB, xA1, xP1, wxB1, wxB2, wyB1, wyP1, kB1);
+        }
+        acc[e] = s;
+      }
+      if (X < gc.nx) {
+        const long long oc = (long long)Y * gc.nx + X;
+        bc[(long long)pa * gc.N + oc] = acc[0];
+        bc[(long long)pb * gc.N + oc] = acc[1];
+      }
+      __syncthreads();
+      if (t == 0) {
+        if (2 * k + SPR_D < nrow) issue(2 * k + SPR_D);
+        if (2 * k + 1 + SPR_D < nrow) issue(2 * k + 1 + SPR_D);
+      }
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---- level-0 prolongation + post-smoothing with the rows staged by the bulk-copy engine -------
+// k_spf_prolong_post at level 0 (nx % 4 == 0: the coarse rows are 16-byte aligned too) as a
+// row-marching kernel: per fine row b and 1/D of both planes, wx, wy, cnt, and the coarse row
+// (r / 2) of x_c of both planes stream through an SPP_D-slot ring. Arithmetic per point as
+// k_spf_prolong_post.
+constexpr int SPP_D = 6;
+constexpr int SPC_W = SPF_T + 4;               // staged coarse columns: X0 - 2 .. X0 + SPF_T + 1
+constexpr int SPP_SLOT = 7 * SPT_W + 2 * SPC_W; // [b0 d0 b1 d1 wx wy cnt][xc0 xc1]
+
+__host__ __device__ constexpr size_t spp_smem() {
+  return (size_t)SPP_D * SPP_SLOT * sizeof(double) + SPP_D * sizeof(uint64_t);
+}
+
+__global__ void __launch_bounds__(SPF_T, 2) k_spf_prolong_tma(Geo g, Geo gc, const double* __restrict__ cnt,
+                                                              const double* __restrict__ dinv, MgIo io,
+                                                              const double* __restrict__ xc, SpStepCtx S, SpfRed R,
+                                                              int nsx, int nyc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // (dependents triggered at the end)
+  if (S.st && S.st->done) return;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SPP_D * SPP_SLOT);
+  int pa, pb;
+  sp_pair(S.K.ell, blockIdx.y, pa, pb);
+  const int pls[2] = {pa, pb};
+  const int nx = g.nx, ny = g.ny, t = threadIdx.x;
+  const long long N = g.N;
+  const double* bsrc[2] = {io.in[pa], io.in[pb]};
+  const double* dsrc[2] = {dinv + (long long)sp_block_of(S.K.ell, pa) * N, dinv + (long long)sp_block_of(S.K.ell, pb) * N};
+  const double* csrc[2] = {xc + (long long)pa * gc.N, xc + (long long)pb * gc.N};
+  const bool dsame = dsrc[0] == dsrc[1];
+  const int strip = blockIdx.x % nsx, chunk = blockIdx.x / nsx;
+  const int nyp = (ny + 1) / 2;
+  const int Y0 = chunk * nyc, Y1 = min(Y0 + nyc, nyp);
+  const bool idle = Y0 >= Y1;
+  const int cs = strip * 2 * SPF_T - 2;
+  const int clo = max(cs, 0), chi = min(cs + SPT_W, nx);
+  const uint32_t bytes = (uint32_t)(chi - clo) * 8u;
+  const int off = clo - cs;
+  const int xs = strip * SPF_T - 2;              // coarse column of staged coarse column 0
+  const int xlo = max(xs, 0), xhi = min(xs + SPC_W, gc.nx);
+  const uint32_t cbytes = (uint32_t)(xhi - xlo) * 8u;
+  const int coff = xlo - xs;
+  for (int k = t; k < SPP_D * SPP_SLOT; k += SPF_T) {
+    const int q = k % SPP_SLOT;
+    bool out;
+    if (q < 7 * SPT_W) {
+      const int c = cs + q % SPT_W;
+      out = c < 0 || c >= nx;
+    } else {
+      const int c = xs + (q - 7 * SPT_W) % SPC_W;
+      out = c < 0 || c >= gc.nx;
+    }
+    if (out) sm[k] = 0.0;
+  }
+  if (t == 0) {
+    for (int s = 0; s < SPP_D; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int r0 = 2 * Y0 - 1, nrow = 2 * (Y1 - Y0) + 2;
+  const uint32_t tx = (uint32_t)(dsame ? 6 : 7) * bytes + 2u * cbytes;
+  auto issue = [&](int i) {
+    const int r = r0 + i, s = i % SPP_D;
+    double* d = sm + (size_t)s * SPP_SLOT;
+    if (r >= 0 && r < ny) {
+      mbar_arrive_expect_tx(&bar[s], tx);
+      const long long ro = (long long)r * nx + clo;
+      bulk_g2s(d + off, bsrc[0] + ro, bytes, &bar[s]);
+      bulk_g2s(d + SPT_W + off, dsrc[0] + ro, bytes, &bar[s]);
+      bulk_g2s(d + 2 * SPT_W + off, bsrc[1] + ro, bytes, &bar[s]);
+      if (!dsame) bulk_g2s(d + 3 * SPT_W + off, dsrc[1] + ro, bytes, &bar[s]);
+      bulk_g2s(d + 4 * SPT_W + off, g.wx + ro, bytes, &bar[s]);
+      bulk_g2s(d + 5 * SPT_W + off, g.wy + ro, bytes, &bar[s]);
+      bulk_g2s(d + 6 * SPT_W + off, cnt + ro, bytes, &bar[s]);
+      const long long co = (long long)(r >> 1) * gc.nx + xlo;
+      bulk_g2s(d + 7 * SPT_W + coff, csrc[0] + co, cbytes, &bar[s]);
+      bulk_g2s(d + 7 * SPT_W + SPC_W + coff, csrc[1] + co, cbytes, &bar[s]);
+    } else {
+      mbar_arrive(&bar[s]);
+    }
+  };
+  double dot[2] = {0.0, 0.0};
+  if (!idle) {
+    if (t == 0)
+      for (int i = 0; i < min(SPP_D, nrow); ++i) issue(i);
+    const int X = strip * SPF_T + t, c0 = 2 * X;
+    const bool v0 = c0 < nx, v1 = c0 + 1 < nx;
+    const int j0 = c0 - cs, jc = X - xs;         // staged fine / coarse column of this thread
+    for (int Y = Y0; Y < Y1; ++Y) {
+      const int k = Y - Y0;
+      for (int i = (k == 0 ? 0 : 2 * k + 2); i <= 2 * k + 3; ++i)
+        mbar_wait(&bar[i % SPP_D], (uint32_t)((i / SPP_D) & 1));
+      const int y0 = 2 * Y;
+      const bool r1 = y0 + 1 < ny, rm = Y > 0, rp = y0 + 2 < ny;
+      const double* sA = sm + (size_t)((2 * k + 1) % SPP_D) * SPP_SLOT;
+      const double* sB = r1 ? sm + (size_t)((2 * k + 2) % SPP_D) * SPP_SLOT : sA;
+      const double* sM = sm + (size_t)((2 * k) % SPP_D) * SPP_SLOT;
+      const double* sP = sm + (size_t)((2 * k + 3) % SPP_D) * SPP_SLOT;
+      const bool inB = v0 && r1;
+      const double* wxA = sA + 4 * SPT_W + j0;
+      const double* wyA = sA + 5 * SPT_W + j0;
+      const double* wxB = sB + 4 * SPT_W + j0;
+      const double* wyB = sB + 5 * SPT_W + j0;
+      const double wxA0 = v0 ? wxA[0] : 0.0, wxA1 = v0 ? wxA[1] : 0.0;
+      const double wxA2 = c0 + 2 < nx ? wxA[2] : 0.0;
+      const double wyA0 = v0 ? wyA[0] : 0.0, wyA1 = v0 ? wyA[1] : 0.0;
+      const double wxB0 = inB ? wxB[0] : 0.0, wxB1 = inB ? wxB[1] : 0.0;
+      const double wxB2 = (c0 + 2 < nx && r1) ? wxB[2] : 0.0;
+      const double wyB0 = inB ? wyB[0] : 0.0, wyB1 = inB ? wyB[1] : 0.0;
+      const double wyP0 = (inB && rp) ? sP[5 * SPT_W + j0] : 0.0;
+      const double wyP1 = (inB && rp) ? sP[5 * SPT_W + j0 + 1] : 0.0;
+      const double kA0 = sA[6 * SPT_W + j0], kA1 = sA[6 * SPT_W + j0 + 1];
+      const double kB0 = sB[6 * SPT_W + j0], kB1 = sB[6 * SPT_W + j0 + 1];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double m1 = 1.0 + S.K.s[pls[e]];
+        const int ob = 2 * e * SPT_W, od = (e == 1 && dsame) ? SPT_W : (2 * e + 1) * SPT_W;
+        const int oc = 7 * SPT_W + e * SPC_W;
+        // u = omega b / D + P x_c at staged fine column jj of a row (coarse column jj_c)
+        auto uval = [&](const double* row, int jj, int jjc) {
+          return SP_OMEGA * row[ob + jj] * row[od + jj] + row[oc + jjc];
+        };
+        const double uA0 = uval(sA, j0, jc), uA1 = uval(sA, j0 + 1, jc);
+        const double uB0 = uval(sB, j0, jc), uB1 = uval(sB, j0 + 1, jc);
+        const double uM0 = rm ? uval(sM, j0, jc) : uA0, uM1 = rm ? uval(sM, j0 + 1, jc) : uA1;
+        const double uP0 = rp ? uval(sP, j0, jc) : uB0, uP1 = rp ? uval(sP, j0 + 1, jc) : uB1;
+        const double wA = uval(sA, j0 - 1, jc - 1), eA = uval(sA, j0 + 2, jc + 1);
+        const double wB = uval(sB, j0 - 1, jc - 1), eB = uval(sB, j0 + 2, jc + 1);
+        auto post = [&](double u0, double b, double d, double uw, double ue, double un, double us, double fw, double fe,
+                        double fn, double fs, double kk) {
+          double a = (m1 * kk) * u0;
+          a = fma(fw, u0 - uw, a);
+          a = fma(fe, u0 - ue, a);
+          a = fma(fn, u0 - un, a);
+          a = fma(fs, u0 - us, a);
+          return u0 + SP_OMEGA * (b - a) * d;
+        };
+        const double bA0 = sA[ob + j0], bA1 = sA[ob + j0 + 1], bB0 = sB[ob + j0], bB1 = sB[ob + j0 + 1];
+        const double oA0 = post(uA0, bA0, sA[od + j0], wA, uA1, uM0, uB0, wxA0, wxA1, wyA0, wyB0, kA0);
+        const double oA1 = post(uA1, bA1, sA[od + j0 + 1], uA0, eA, uM1, uB1, wxA1, wxA2, wyA1, wyB1, kA1);
+        double* oq = io.out[pls[e]];
+        spf_st2<true>(oq + (long long)y0 * nx, c0, v0, v1, oA0, oA1);
+        double s = dot[e];
+        if (v0) s = fma(oA0, bA0, s);
+        if (v1) s = fma(oA1, bA1, s);
+        if (r1) {
+          const double oB0 = post(uB0, bB0, sB[od + j0], wB, uB1, uA0, uP0, wxB0, wxB1, wyB0, wyP0, kB0);
+          const double oB1 = post(uB1, bB1, sB[od + j0 + 1], uB0, eB, uA1, uP1, wxB1, wxB2, wyB1, wyP1, kB1);
+          spf_st2<true>(oq + (long long)(y0 + 1) * nx, c0, v0, v1, oB0, oB1);
+          if (v0) s = fma(oB0, bB0, s);
+          if (v1) s = fma(oB1, bB1, s);
+        }
+        dot[e] = s;
+      }
+      __syncthreads();
+      if (t == 0) {
+        if (2 * k + SPP_D < nrow) issue(2 * k + SPP_D);
+        if (2 * k + 1 + SPP_D < nrow) issue(2 * k + 1 + SPP_D);
+      }
+    }
+  }
+  spf_reduce_pair(S, R, dot[0], dot[1], pa, pb);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Tiles of the fused kernels on a level of `ncx` x `ncy` aggregates: strips of SPF_T aggregate
 // columns x one aggregate row.
 static inline void spf_tiles(int ncx, int ncy, int& nsx, int& ntile) {

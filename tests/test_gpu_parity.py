@@ -410,11 +410,13 @@ def test_sp_kernel_variants_parity(env):
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("tma", ["1", "0"])
-@pytest.mark.parametrize("shape", [(1, 37, 530), (1, 64, 256), (1, 5, 6)])
-def test_sp_k1_staged_rows_parity(tma, shape):
-    """K1 with the rows streamed through the bulk-copy ring (k_spf_apply_tma, even n_x: ragged
-    last strip, odd n_y, chunk boundaries, a grid smaller than one strip) and the register K1
+@pytest.mark.parametrize("tma", ["1", "0", "2"])
+@pytest.mark.parametrize("shape", [(1, 37, 530), (1, 37, 532), (1, 64, 256), (1, 21, 16)])
+def test_sp_staged_rows_parity(tma, shape):
+    """The SP level-0 kernels with the rows streamed through a bulk-copy ring (K1
+    k_spf_apply_tma for even n_x, the default; with AAC_SPF_TMA=2 also the restriction
+    k_spf_restrict_tma and, for n_x % 4 == 0, the prolongation k_spf_prolong_tma: ragged last
+    strips, odd n_y, chunk boundaries, a grid smaller than one strip) and the register kernels
     (AAC_SPF_TMA=0) against the oracle. A fresh process each (the switch is read once)."""
     import subprocess
     import sys
