@@ -621,7 +621,10 @@ __global__ void __launch_bounds__(SPF_T, SPF_MINB) k_spf_apply(Geo g, SpVec v, S
 #ifndef SPT_MINB
 #define SPT_MINB 3
 #endif
-constexpr int SPT_D = 8;                       // row slots
+#ifndef SPT_DSLOT
+#define SPT_DSLOT 8
+#endif
+constexpr int SPT_D = SPT_DSLOT;               // row slots
 constexpr int SPT_W = 2 * SPF_T + 4;           // staged columns: cb - 2 .. cb + 2 SPF_T + 1
 constexpr int SPT_NA = 4;                      // arrays per row: u (plane a), u (plane b), wx, wy
 
