@@ -1317,7 +1317,7 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
     if (occ < 1) occ = 1;
   }
   const long long ntile = (long long)((g.nx + AT - 1) / AT) * g.ny * g.nz;
-  const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ntile);
+  const int grid = (int)std::min<long long>((long long)occ * ctx->num_sms, ARN_NGF > 2 ? ntile * ARN_NGF / 2 : ntile);
   // algorithmic bytes: Z_j + C in (fused) or W in (split), W out (fused), basis V_0..V_j in
   const double bytes = FUSED ? (host_j + 3) * V + C : (host_j + 2) * V;
   LAUNCH(ctx, KID_ARNOLDI, bytes, (k_arnoldi<DIM, ELLC, TMA, FUSED><<<grid, AT + 32, smem, ctx->stream>>>(g, ctx->ell, P)));
@@ -1372,7 +1372,7 @@ static int arnoldi_step(aac_ctx* ctx, int method, int k, int host_j) {
   AAC_TRY(arnoldi_impl(ctx, host_j));
   if (ctx->multi()) {
     AAC_TRY(comm_allreduce(ctx, ctx->d_red, 2 * (host_j + 1), ncclSum));
-    LAUNCH(ctx, KID_SCALAR, 0, k_scalar_cgs2<<<1, 1, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
+    LAUNCH(ctx, KID_SCALAR, 0, k_scalar_cgs2<<<1, 128, 0, ctx->stream>>>(arnoldi_ctx(ctx)));
   }
   return AAC_OK;
 }

@@ -30,6 +30,9 @@ struct KAParams {
 #ifndef ARN_AT
 #define ARN_AT 256
 #endif
+#ifndef ARN_NGF
+#define ARN_NGF 2                // small grids: ~ARN_NGF work units (tile, vector group) per CTA
+#endif
 constexpr int AT = ARN_AT;       // tile points per CTA iteration (one per consumer thread)
 constexpr int AS = ARN_AS;       // bulk-copy pipeline stages for the basis tiles
 constexpr int AW = AT / 32;      // consumer warps; warp AW is the TMA producer
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
   // into ng groups over more CTAs (each re-reads its tile of W and V_j; the partial sums of a
   // CTA are zero outside its groups) -- the per-tile chain of j+1 dependent stages is the
   // latency that bounds a small problem.
-  long long ngl = (2LL * gridDim.x + ntile - 1) / ntile;
+  long long ngl = ((long long)ARN_NGF * gridDim.x + ntile - 1) / ntile;
   ngl = ngl < 1 ? 1 : (ngl > nv ? nv : ngl);
   const int ng = FUSED ? 1 : (int)ngl;
   const int gsz = (nv + ng - 1) / ng;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
           acc[warp * nv2 + nv + i] += ga;
         }
       }
-      if (T.i1 == nv) {                           // V_j = u, already in registers: the same
+      if (T.i0 < T.i1 && T.i1 == nv) {          // V_j = u, already in registers: the same
         double sa = 0.0, ga = 0.0;                // values as streaming it, one read less
         if (valid) {
           FOR_PL(pl) {
@@ -217,19 +220,19 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
   const int nwarps = blockDim.x >> 5;
   for (int k = warp; k < nv2; k += nwarps) {   // fixed order: lane-strided, then warp tree
     double sum = 0.0;
-    for (int c = lane; c < (int)gridDim.x; c += 32) sum += __ldcg(P.part + (long long)c * nv2 + k);
+    sum = strided_sum_ordered(P.part + k, nv2, lane, 32, (int)gridDim.x);   // (batched loads)
     sum = warp_sum(sum);
     if (lane == 0) tot[k] = sum;
   }
   __syncthreads();
-  if (t == 0) {
-    st->tick = 0;
-    if (P.ac.local_only) {
+  if (t == 0) st->tick = 0;
+  if (P.ac.local_only) {
+    if (t == 0)
       for (int k = 0; k < nv2; ++k) P.ac.red[k] = tot[k];
-    } else if (P.ac.one_reduce) {
-      arnoldi_lagged_step(P.ac, j, tot, tot + nv);
-    } else {
-      arnoldi_cgs2_step(P.ac, j, tot, tot + nv);
-    }
+  } else {
+    // (lagged: the normalisation of the previous vector first -- it sets sigma_j)
+    if (P.ac.one_reduce && t == 0) arnoldi_norm_step(P.ac, j, tot[nv + j]);
+    __syncthreads();
+    arnoldi_cgs2_step_cta(P.ac, j, tot, tot + nv);
   }
 }

@@ -79,12 +79,30 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// s = sum over c = start, start + step, ... < n of base[c * stride], in ascending c (the order of the
+// plain loop), with the loads issued KU at a time: the values were written by other CTAs and sit
+// in L2, and a loop that adds each value before loading the next pays one L2 round trip per value.
+template <int KU = 8>
+__device__ __forceinline__ double strided_sum_ordered(const double* base, long long stride, int start, int step,
+                                                      int n) {
+  double s = 0.0;
+  int c = start;
+  for (; c + (KU - 1) * step < n; c += KU * step) {
+    double v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) v[u] = __ldcg(base + (long long)(c + u * step) * stride);
+#pragma unroll
+    for (int u = 0; u < KU; ++u) s += v[u];
+  }
+  for (; c < n; c += step) s += __ldcg(base + (long long)c * stride);
+  return s;
+}
+
 // Fixed-order sum of n values by one CTA (lane-strided, warp tree, warps in order).
 __device__ double block_sum_fixed(const double* v, int n) {
   __shared__ double wsum[32];
-  double s = 0.0;
-  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < n; i += blockDim.x * blockDim.y)
-    s += __ldcg(v + i);                      // written by other CTAs: bypass L1
+  // written by other CTAs: bypass L1 (loads batched, same order as a plain strided loop)
+  double s = strided_sum_ordered(v, 1, threadIdx.x + threadIdx.y * blockDim.x, blockDim.x * blockDim.y, n);
   s = warp_sum(s);
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   const int nw = (blockDim.x * blockDim.y + 31) >> 5;
@@ -153,6 +171,30 @@ __device__ void arnoldi_cgs2_step(const ArnoldiCtx& ac, int j, const double* s, 
   ac.st->j = j + 1;
 }
 
+// The same CGS2 coefficients computed by all threads of the calling CTA (thread i: h1_i, the Gram
+// entries (i, j), then c_i = h1_i + (h1_i - (G h1)_i) with the sum over k in ascending order, as the
+// one-thread version): O(j) per thread instead of O(j^2) on one thread -- the serial form was
+// the last CTA's tail of every Arnoldi launch (at the 2d256 config, 39 steps: ~9% of a solve).
+__device__ void arnoldi_cgs2_step_cta(const ArnoldiCtx& ac, int j, const double* s, const double* gg) {
+  const int ld = ac.ldh;
+  const double sj = ac.sigma[j];
+  double* h1 = ac.red + 2 * ld;              // scratch
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    h1[i] = ac.sigma[i] * sj * s[i];
+    const double gij = ac.sigma[i] * sj * gg[i];
+    ac.G[(long long)j * ld + i] = gij;
+    ac.G[(long long)i * ld + j] = gij;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k <= j; ++k) t = fma(ac.G[(long long)k * ld + i], h1[k], t);
+    ac.c[i] = h1[i] + (h1[i] - t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ac.st->j = j + 1;
+}
+
 // One-reduce Arnoldi step (not in the paper, GMRES is the north star's). The
 // projection pass already measures the Gram column <V_i, V_j>, i <= j, whose last entry is
 // ||V_j||^2 -- so the norm of the vector formed by the previous update need not be reduced on
@@ -171,11 +213,14 @@ __global__ void k_scalar_norm(ArnoldiCtx ac) {
   if (ac.st->done) return;
   arnoldi_norm_step(ac, ac.st->j, ac.red[0]);
 }
-__global__ void k_scalar_cgs2(ArnoldiCtx ac) {
-  if (ac.st->done) return;
-  const int j = ac.st->j;
-  if (ac.one_reduce) arnoldi_lagged_step(ac, j, ac.red, ac.red + (j + 1));
-  else arnoldi_cgs2_step(ac, j, ac.red, ac.red + (j + 1));
+__global__ void k_scalar_cgs2(ArnoldiCtx ac) {       // one CTA
+  const bool done = ac.st->done;                     // (read by every thread before thread 0's
+  const int j = ac.st->j;                            //  norm step may set it)
+  __syncthreads();
+  if (done) return;
+  if (ac.one_reduce && threadIdx.x == 0) arnoldi_norm_step(ac, j, ac.red[(j + 1) + j]);
+  __syncthreads();
+  arnoldi_cgs2_step_cta(ac, j, ac.red, ac.red + (j + 1));
 }
 
 // y = R^{-1} g for the m x m upper-triangular rotated Hessenberg; y_i *= sigma_i so that
