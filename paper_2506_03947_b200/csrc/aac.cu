@@ -1484,7 +1484,7 @@ static int gmres_impl(aac_ctx* ctx, int method, int k, const double* b, double* 
   }
   double* yy = ctx->d_giv + 3 * ldh;
   LAUNCH(ctx, KID_SCALAR, 0,
-         k_backsub<<<1, 1, 0, ctx->stream>>>(ctx->d_st, ldh, ctx->d_H, ctx->d_giv + 2 * ldh, ctx->d_giv + 4 * ldh, yy));
+         k_backsub<<<1, 32, 0, ctx->stream>>>(ctx->d_st, ldh, ctx->d_H, ctx->d_giv + 2 * ldh, ctx->d_giv + 4 * ldh, yy));
   AAC_TRY(publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState)));
   AAC_TRY(comm_sync(ctx));
   const IterState fin = *ctx->h_st;

@@ -231,8 +231,7 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
       for (int k = 0; k < nv2; ++k) P.ac.red[k] = tot[k];
   } else {
     // (lagged: the normalisation of the previous vector first -- it sets sigma_j)
-    if (P.ac.one_reduce && t == 0) arnoldi_norm_step(P.ac, j, tot[nv + j]);
-    __syncthreads();
+    if (P.ac.one_reduce) arnoldi_norm_step_cta(P.ac, j, tot[nv + j]);
     arnoldi_cgs2_step_cta(P.ac, j, tot, tot + nv);
   }
 }

@@ -152,6 +152,54 @@ __device__ void arnoldi_norm_step(const ArnoldiCtx& ac, int j, double nrm2) {
   if (st->relres <= st->rtol || nu == 0.0 || j >= st->maxit) st->done = 1;
 }
 
+// arnoldi_norm_step by a whole CTA: the column's entries, cos and sin of the previous rotations
+// are staged in shared memory by all threads, thread 0 runs the (inherently serial) rotation chain
+// on them, and the column goes back to H in parallel. The serial version reloads h from global
+// memory at every rotation (one L2 round trip per rotation in the last CTA's tail).
+__device__ void arnoldi_norm_step_cta(const ArnoldiCtx& ac, int j, double nrm2) {
+  constexpr int CAP = 256;
+  __shared__ double sh_h[CAP + 2], sh_cs[CAP], sh_sn[CAP];
+  if (j == 0 || j > CAP) {
+    if (threadIdx.x == 0) arnoldi_norm_step(ac, j, nrm2);
+    __syncthreads();
+    return;
+  }
+  const int col = j - 1;
+  for (int i = threadIdx.x; i < j; i += blockDim.x) sh_h[i] = ac.c[i];
+  for (int i = threadIdx.x; i < col; i += blockDim.x) {
+    sh_cs[i] = ac.cs[i];
+    sh_sn[i] = ac.sn[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    IterState* st = ac.st;
+    const double nu = sqrt(nrm2);
+    ac.sigma[j] = nu > 0.0 ? 1.0 / nu : 0.0;
+    double* h = sh_h;
+    h[j] = nu;
+    for (int i = 0; i < col; ++i) {
+      const double t = sh_cs[i] * h[i] + sh_sn[i] * h[i + 1];
+      h[i + 1] = -sh_sn[i] * h[i] + sh_cs[i] * h[i + 1];
+      h[i] = t;
+    }
+    const double r = hypot(h[col], h[col + 1]);
+    ac.cs[col] = h[col] / r;
+    ac.sn[col] = h[col + 1] / r;
+    h[col] = r;
+    h[col + 1] = 0.0;
+    ac.g[col + 1] = -ac.sn[col] * ac.g[col];
+    ac.g[col] = ac.cs[col] * ac.g[col];
+    st->hn = nu;
+    st->m = j;
+    st->relres = fabs(ac.g[col + 1]) / st->beta;
+    if (st->relres <= st->rtol || nu == 0.0 || j >= st->maxit) st->done = 1;
+  }
+  __syncthreads();
+  double* hc = ac.H + (long long)col * ac.ldh;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) hc[i] = sh_h[i];
+  __syncthreads();
+}
+
 // CGS2 coefficients of column j from the raw sums s_i = <V_i, W>, gg_i = <V_i, V_j>.
 __device__ void arnoldi_cgs2_step(const ArnoldiCtx& ac, int j, const double* s, const double* gg) {
   const int ld = ac.ldh;
@@ -218,23 +266,27 @@ __global__ void k_scalar_cgs2(ArnoldiCtx ac) {       // one CTA
   const int j = ac.st->j;                            //  norm step may set it)
   __syncthreads();
   if (done) return;
-  if (ac.one_reduce && threadIdx.x == 0) arnoldi_norm_step(ac, j, ac.red[(j + 1) + j]);
-  __syncthreads();
+  if (ac.one_reduce) arnoldi_norm_step_cta(ac, j, ac.red[(j + 1) + j]);
   arnoldi_cgs2_step_cta(ac, j, ac.red, ac.red + (j + 1));
 }
 
 // y = R^{-1} g for the m x m upper-triangular rotated Hessenberg; y_i *= sigma_i so that
 // x = sum_i y_i Z_i with the RAW preconditioned vectors Z_i = P^{-1} V_i(raw).
+// One warp: row i's sum over k > i split over the lanes (lane-strided, then the warp tree), y_i by
+// lane 0 -- m steps of a warp reduction instead of m^2 / 2 dependent global loads on one thread.
 __global__ void k_backsub(const IterState* st, int ldh, const double* __restrict__ H,
                           const double* __restrict__ g, const double* __restrict__ sigma,
-                          double* __restrict__ y) {
+                          double* y) {
   const int m = st->m;
+  const int lane = threadIdx.x & 31;
   for (int i = m - 1; i >= 0; --i) {
-    double s = g[i];
-    for (int k = i + 1; k < m; ++k) s -= H[(long long)k * ldh + i] * y[k];
-    y[i] = s / H[(long long)i * ldh + i];
+    double s = 0.0;
+    for (int k = i + 1 + lane; k < m; k += 32) s = fma(H[(long long)k * ldh + i], y[k], s);
+    s = warp_sum(s);
+    if (lane == 0) y[i] = (g[i] - s) / H[(long long)i * ldh + i];
+    __syncwarp();
   }
-  for (int i = 0; i < m; ++i) y[i] *= sigma[i];
+  for (int i = lane; i < m; i += 32) y[i] *= sigma[i];
 }
 
 // x = sum_{i<m} y[i] Z_i

@@ -229,10 +229,11 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   if (last) {
     __threadfence();
     const double tot = block_sum_fixed(U.part, gridDim.x);
-    if (t == 0) {
-      st->tick = 0;
-      if (U.ac.local_only) U.ac.red[0] = tot;
-      else arnoldi_norm_step(U.ac, j, tot);
+    if (t == 0) st->tick = 0;
+    if (U.ac.local_only) {
+      if (t == 0) U.ac.red[0] = tot;
+    } else {
+      arnoldi_norm_step_cta(U.ac, j, tot);
     }
   }
 }
