@@ -21,6 +21,7 @@
 #include "wave_r.cuh"
 #include "stencil.cuh"
 #include "stencil_tile.cuh"
+#include "stencil_rows.cuh"
 
 // saddle-point inner solver (sp.cuh, included below once make_dft / shift_of_block exist)
 static int sp_prepare(aac_ctx* ctx, int k);
@@ -526,10 +527,52 @@ static int launch_matvec_tile(aac_ctx* ctx, const double* xbase, long long xjs, 
   return AAC_OK;
 }
 
+// Row-marching kernel (stencil_rows.cuh) on 2D grids with even nx (one rank or slabs), opt-in:
+// AAC_MATVEC_ROWS=1 (AAC_MATVEC_RY sets the rows per thread). Measured slower at the headline
+// (profiles/r02/ab_matvec_rows: 62-89 us per apply at 2-16 rows per thread against 37.9 us for
+// k_matvec, graph replay): each row step waits one DRAM latency for its south rows with only
+// 12 warps per SM (168 registers), where k_matvec's short-lived CTAs keep more bytes in flight.
+// Returns 0 when not selected or not applicable (the caller launches k_matvec).
+static int matvec_rows_ry(const aac_ctx* ctx) {
+  static const int off = !(getenv("AAC_MATVEC_ROWS") && atoi(getenv("AAC_MATVEC_ROWS")) == 1);
+  static const int ry_env = getenv("AAC_MATVEC_RY") ? atoi(getenv("AAC_MATVEC_RY")) : 0;
+  if (off || ctx->dim != 2 || ctx->varying || (ctx->geo.nx % 2) != 0) return 0;
+  const int ell = ctx->ell;
+  if (!(ell == 2 || ell == 4 || ell == 6 || ell == 8 || ell == 10 || ell == 12)) return 0;
+  if (ry_env > 0) return ry_env;
+  // rows per thread: the most that still gives two waves of resident CTAs (MR_MINB per SM)
+  const long long strips = (ctx->geo.nx / 2 + MR_NT - 1) / MR_NT;
+  int ry = 16;
+  while (ry > 1 && strips * ((ctx->geo.ny + ry - 1) / ry) < 2LL * MR_MINB * ctx->num_sms) ry /= 2;
+  return ry;
+}
+
+static int launch_matvec_rows(aac_ctx* ctx, int ry, const double* xbase, long long xjs, const int* jdev,
+                              double* y, const double* hlo, const double* hhi, double bytes) {
+  const Geo& g = ctx->geo;
+  const dim3 grid((unsigned)((g.nx / 2 + MR_NT - 1) / MR_NT), (unsigned)((g.ny + ry - 1) / ry));
+#define MR_CASE(E)                                                                                  \
+  case E:                                                                                           \
+    LAUNCH(ctx, KID_MATVEC, bytes,                                                                  \
+           k_matvec_rows<E><<<grid, MR_NT, 0, ctx->stream>>>(g, xbase, xjs, jdev, y, hlo, hhi, ry)); \
+    return AAC_OK;
+  switch (ctx->ell) {
+    MR_CASE(2) MR_CASE(4) MR_CASE(6) MR_CASE(8) MR_CASE(10) MR_CASE(12)
+    default: break;
+  }
+#undef MR_CASE
+  return aac_fail(ctx, AAC_EINVAL, "k_matvec_rows: unsupported ell %d", ctx->ell);
+}
+
 template <int DIM, int VEC>
 static int launch_matvec(aac_ctx* ctx, const double* x, double* y, double bytes) {
   const Geo& g = ctx->geo;
   if (DIM == 2 && matvec_tile_on(ctx)) return launch_matvec_tile(ctx, x, 0, nullptr, y, bytes);
+  if (DIM == 2) {
+    if (const int ry = matvec_rows_ry(ctx))
+      return launch_matvec_rows(ctx, ry, x, 0, nullptr, y, ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S,
+                                bytes);
+  }
   const double* hlo = ctx->d_halo;
   const double* hhi = ctx->d_halo + (long long)ctx->ell * g.S;
   const dim3 grid(grid1d(g.nx / VEC, 256), g.ny, g.nz);
@@ -1294,6 +1337,10 @@ static int launch_arnoldi(aac_ctx* ctx, int host_j) {
     ctx->sweeps += ctx->ell;
   } else if (!FUSED && DIM == 2 && matvec_tile_on(ctx)) {
     AAC_TRY(launch_matvec_tile(ctx, ctx->d_Z, L, reinterpret_cast<const int*>(ctx->d_st), ctx->d_W, 2 * V + C));
+    ctx->sweeps += ctx->ell;
+  } else if (!FUSED && DIM == 2 && matvec_rows_ry(ctx)) {
+    AAC_TRY(launch_matvec_rows(ctx, matvec_rows_ry(ctx), ctx->d_Z, L, reinterpret_cast<const int*>(ctx->d_st),
+                               ctx->d_W, ctx->d_halo, ctx->d_halo + (long long)ctx->ell * g.S, 2 * V + C));
     ctx->sweeps += ctx->ell;
   } else if (!FUSED) {               // w = calA Z_j by the stencil kernel (j read on the device)
     const bool v2 = vec2(ctx);

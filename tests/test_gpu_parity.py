@@ -83,6 +83,45 @@ def test_matvec_tile_bit_identical_to_register_kernel(tmp_path):
     assert np.array_equal(outs[0], outs[1])
 
 
+_MATVEC_BITS_KW = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth
+from paper_2506_03947_b200 import from_problem
+p = synth.make_problem({name!r}, **{kw!r})
+s = from_problem(p, max_krylov=8)
+x = np.random.default_rng(7).standard_normal((p.ell,) + p.shape)
+y = s.matvec(torch.from_numpy(x.reshape(p.ell, -1)).cuda()).cpu().numpy()
+np.save({out!r}, y)
+"""
+
+
+@pytest.mark.parametrize("name,kw,ry", [
+    ("headline", dict(shape=(1, 131, 516)), ""), ("headline", dict(shape=(1, 131, 516)), "3"),
+    ("headline", dict(shape=(1, 130, 67 + 1)), "1"), ("2d256", dict(shape=(1, 9, 600), ell=4), "16"),
+    ("2d256", dict(shape=(1, 2, 2), ell=2), ""), ("2d256", dict(shape=(1, 41, 40), ell=12, alpha=0.3), "5"),
+    ("headline", dict(shape=(1, 64, 64), c=0.0), ""),
+])
+def test_matvec_rows_bit_identical_to_register_kernel(tmp_path, name, kw, ry):
+    """k_matvec_rows (row-marching, 2D with even nx, opt-in AAC_MATVEC_ROWS=1; AAC_MATVEC_RY rows per thread,
+    ragged last chunks) performs stencil_sv's operations in the same order: its result equals
+    k_matvec's (AAC_MATVEC_ROWS=0) bit for bit, a fresh process each."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"y{flag}.npy")
+        env = {**os.environ, "AAC_MATVEC_ROWS": flag}
+        if ry:
+            env["AAC_MATVEC_RY"] = ry
+        r = subprocess.run([sys.executable, "-c", _MATVEC_BITS_KW.format(root=root, name=name, kw=kw, out=out)],
+                           capture_output=True, text=True, timeout=300, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("name,kw", CASES)
 def test_matvec_parity(name, kw):
     p = synth.make_problem(name, **kw)
