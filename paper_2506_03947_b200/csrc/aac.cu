@@ -298,6 +298,10 @@ static int setup_impl(const aac_grid* g, const double* kx, const double* ky, con
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   if (getenv("AAC_NO_GRAPH")) ctx->use_graphs = false;
+  {
+    const int rev = getenv("AAC_REV") ? atoi(getenv("AAC_REV")) : AAC_REV_DEFAULT;
+    cudaMemcpyToSymbol(c_rev, &rev, sizeof(int));
+  }
   // wavefront temporal blocking (2D, one rank): depth 8 by default, AAC_WAVE_H=0 disables
   ctx->wave_h = getenv("AAC_WAVE_H") ? atoi(getenv("AAC_WAVE_H")) : 8;
   if (ctx->wave_h != 0 && ctx->wave_h != 4) ctx->wave_h = 8;

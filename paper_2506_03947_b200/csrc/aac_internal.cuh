@@ -19,6 +19,27 @@
 #define AAC_MAX_BLK (AAC_MAX_ELL / 2 + 1)
 #define AAC_GATHER_MAX 1024    // longest sum reduced by all-gather + rank-order sum
 
+// Traversal direction of the streaming kernels of a GMRES step (AAC_REV bit mask, set once at
+// aac_setup): a kernel that walks the grid in the direction OPPOSITE to its producer starts on
+// the producer's most recent output, which is still in the 126 MB L2 (the vectors are 84 MB at
+// the headline, so a same-direction consumer starts on lines already evicted). The logical
+// CTA index is flipped, so every CTA computes the same points in the same order and the
+// cross-CTA partial sums keep their slots: bit-identical to the forward order (k_arnoldi's
+// persistent CTAs walk their own tiles backwards too, which reorders their private sums).
+// bit 0 k_matvec, 1 k_arnoldi, 2 k_fwd_upd, 3 k_waver, 4 k_inverse.
+__constant__ int c_rev;
+#define AAC_REV_MATVEC 1
+#define AAC_REV_ARNOLDI 2
+#define AAC_REV_FWD 4
+#define AAC_REV_WAVE 8
+#define AAC_REV_INV 16
+#define AAC_L2_ARNOLDI 32   // basis stream of k_arnoldi with an L2 evict_first policy
+#define AAC_L2_FWD 64       // ... of k_fwd_upd (bit 7: W too)
+#define AAC_L2_FWD_W 128
+#ifndef AAC_REV_DEFAULT
+#define AAC_REV_DEFAULT (AAC_REV_MATVEC | AAC_REV_FWD)   // measured best of the 32 masks at the headline (8.18 vs 8.34-8.44 ms per solve)
+#endif
+
 // ------------------------------------------------------------------------------------------
 // Geometry of this rank's slab, passed BY VALUE to every stencil kernel.
 // Points p = (z*ny + y)*nx + x of the local slab (x fastest). The slab axis is y for dim 2

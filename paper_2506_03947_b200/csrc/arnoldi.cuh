@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
   const long long my_tiles = blockIdx.x < nunit ? (nunit - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   struct Tile { long long base; int x0, y, z, len, i0, i1; };
   auto tile_of = [&](long long r) {
-    const long long u = blockIdx.x + r * gridDim.x;
+    long long u = blockIdx.x + r * gridDim.x;
+    if (c_rev & AAC_REV_ARNOLDI) u = nunit - 1 - u;
     const unsigned tix = (unsigned)(u / ng);
     const int gi = (int)(u - (long long)tix * ng);
     const unsigned row = tix / cpr, ch = tix - row * cpr;
@@ -100,13 +101,15 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
   if (warp == AW) {                             // ---- producer warp
     if (TMA && lane == 0) {
       long long k = 0;                          // item counter (ring stage / phase)
+      const bool hint = c_rev & AAC_L2_ARNOLDI;
+      const uint64_t pol = l2_policy_evict_first();
       for (long long r = 0; r < my_tiles; ++r) {
         const Tile T = tile_of(r);
         // V_j is not streamed: the consumers hold it in registers (u) already
         for (int i = T.i0; i < min(T.i1, j); ++i, ++k) {
           const int s = (int)(k % AS);
           if (k >= AS) mbar_wait(&empty[s], (uint32_t)(((k / AS) - 1) & 1));
-          bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s]);
+          bulk_planes(ring + (long long)s * ELLC * AT, AT, P.V + (long long)i * P.L + T.base, N, ell, T.len, &full[s], hint, pol);
         }
       }
     }

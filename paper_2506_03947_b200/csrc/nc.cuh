@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   const int j = st->j;
   const int ell = D.ell;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const long long base = (long long)blockIdx.x * FT;
+  const unsigned bid = (c_rev & AAC_REV_FWD) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  const long long base = (long long)bid * FT;
   const int len = (int)((N - base) < FT ? (N - base) : FT);
   const int lb = len & ~1;
   const long long L = U.L;
@@ -164,10 +165,12 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   double nrm = 0.0;
   if (warp == FW) {                                 // ---- producer warp
     if (TMA && lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
       for (int k = 0; k < nitems; ++k) {
         const int s = k % FS;
         if (k >= FS) mbar_wait(&empty[s], (uint32_t)(((k / FS) - 1) & 1));
-        bulk_planes(sm + (long long)s * ELLC * FT, FT, src_of(k) + base, N, ell, len, &full[s]);
+        const bool hint = k == 0 ? (c_rev & AAC_L2_FWD_W) : (c_rev & AAC_L2_FWD);
+        bulk_planes(sm + (long long)s * ELLC * FT, FT, src_of(k) + base, N, ell, len, &full[s], hint, pol);
       }
     }
   } else {                                          // ---- consumer warps
@@ -211,11 +214,11 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
   if (t == 0) {
     double tot = 0.0;
     for (int w2 = 0; w2 < FW; ++w2) tot += red[w2];
-    U.part[blockIdx.x] = tot;
+    U.part[bid] = tot;
     __threadfence();
     // two-level ticket: thousands of CTAs taking a ticket on ONE counter serialise in L2;
     // the last CTA of each group of 32 takes the global ticket (and resets its group counter)
-    const unsigned gid = blockIdx.x >> 5;
+    const unsigned gid = bid >> 5;
     const unsigned gsz = min(32u, gridDim.x - (gid << 5));
     bool lst = false;
     if (atomicAdd(&U.grp[gid], 1u) == gsz - 1) {
@@ -416,7 +419,8 @@ __global__ void __launch_bounds__(256) k_inverse(long long N, Dft D, NcFinal F,
                                                  const IterState* st) {
   if (st && st->done) return;
   double* z = zbase + (st ? (long long)st->j * zjs : 0LL);
-  const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  const unsigned bid = (c_rev & AAC_REV_INV) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  const long long p = ((long long)bid * blockDim.x + threadIdx.x) * VEC;
   if (p >= N) return;
   const int ell = D.ell, h = ell / 2;
   double yr[AAC_MAX_BLK][VEC], yi[AAC_MAX_BLK][VEC];

@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
   // grid (x-chunks, ny, nz): no index division
   const int xx = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (xx >= g.nx) return;
+  const bool rev = c_rev & AAC_REV_MATVEC;
   PtV<DIM, VEC> q;
-  load_ptv_xyz<DIM, VEC>(g, xx, blockIdx.y, blockIdx.z, q);
+  load_ptv_xyz<DIM, VEC>(g, xx, rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y,
+                         rev ? gridDim.z - 1 - blockIdx.z : blockIdx.z, q);
   const long long p = q.p;
   double prev[VEC];
 #pragma unroll

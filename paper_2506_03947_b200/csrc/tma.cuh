@@ -52,11 +52,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// L2 eviction policy for data read once per kernel (the Krylov basis stream): evict_first keeps
+// the stream from displacing the vectors the neighbouring kernels hand over through L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // Copy `len` doubles of each of `np` planes (src + pl*pstride) into dst[pl*tile ...]: the
 // 16-byte-multiple prefix goes through the bulk engine; an odd last element (len odd) is left
 // to the consumer (read from global). Returns the bytes the barrier must expect.
 __device__ __forceinline__ uint32_t bulk_planes(double* dst, int tile, const double* src,
-                                                long long pstride, int np, int len, uint64_t* bar) {
+                                                long long pstride, int np, int len, uint64_t* bar,
+                                                bool hint = false, uint64_t pol = 0) {
   const int lb = len & ~1;
   const uint32_t bytes = (uint32_t)lb * 8u;
   if (bytes == 0) {
@@ -64,6 +82,10 @@ __device__ __forceinline__ uint32_t bulk_planes(double* dst, int tile, const dou
     return 0;
   }
   mbar_arrive_expect_tx(bar, bytes * (uint32_t)np);
-  for (int pl = 0; pl < np; ++pl) bulk_g2s(dst + pl * tile, src + pl * pstride, bytes, bar);
+  if (hint) {
+    for (int pl = 0; pl < np; ++pl) bulk_g2s_hint(dst + pl * tile, src + pl * pstride, bytes, bar, pol);
+  } else {
+    for (int pl = 0; pl < np; ++pl) bulk_g2s(dst + pl * tile, src + pl * pstride, bytes, bar);
+  }
   return bytes * np;
 }

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(NT, CPLX ? 2 : 3) k_waver(Geo g, const __grid_
   // x-halo of NS columns per side: a wrong edge value reaches one column further per level
   constexpr int HX = CLU ? 0 : NS;
   constexpr int TX = NT - 2 * HX;
-  const int cta = (int)blockIdx.x;
+  const int cta = (!CLU && (c_rev & AAC_REV_WAVE)) ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
   const int strip = cta % P.nstrip, chunk = cta / P.nstrip;
   const int x = strip * TX - HX + t;
   const bool colin = x >= 0 && x < g.nx;
