@@ -560,6 +560,43 @@ def test_cluster_wavefront_bit_identical(monkeypatch, kw, method, k, ly):
     assert _rel(z["1"], ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)) <= 1e-12
 
 
+# -------------------------------------------------- traversal direction masks
+@pytest.mark.parametrize("kw,method,k", [
+    (dict(shape=(1, 150, 301)), "nc2", 8),          # wavefront, ragged strips and chunks
+    (dict(shape=(1, 61, 47)), "nc1", 20),           # two passes
+])
+def test_traversal_direction_masks(monkeypatch, kw, method, k):
+    """AAC_REV flips the LOGICAL CTA index of the streaming kernels: calA, the preconditioner
+    and a whole GMRES solve are bit-identical for every mask that leaves k_arnoldi alone
+    (its persistent CTAs walk their tiles backwards, which reorders their private sums:
+    there the iteration count must agree and the solution to rounding), and all match the
+    oracle."""
+    p = synth.make_problem("headline", **kw)
+    rng = np.random.default_rng(17)
+    r = rng.standard_normal((p.ell,) + p.shape)
+    out = {}
+    for m in ("0", "5", "29", "31"):
+        monkeypatch.setenv("AAC_REV", m)
+        s = _solver(p)
+        y = s.matvec(_dev(r, p.ell)).cpu().numpy()
+        z = s.precond_apply(method, k, _dev(r, p.ell)).cpu().numpy()
+        x, info = s.gmres(method, k, _dev(p.b, p.ell), rtol=p.rtol, maxit=60)
+        out[m] = (y, z, x.cpu().numpy(), info["iters"])
+        s.close()
+    for m in ("5", "29"):                              # k_arnoldi forward in 0, 5, 29
+        for a, b in zip(out["0"][:3], out[m][:3]):
+            assert np.array_equal(a, b)
+        assert out[m][3] == out["0"][3]
+    assert np.array_equal(out["31"][0], out["0"][0]) and np.array_equal(out["31"][1], out["0"][1])
+    assert out["31"][3] == out["0"][3]
+    assert _rel(out["31"][2], out["0"][2]) <= 1e-12
+    w = op.weights(p)
+    mu = op.gershgorin_max(w)
+    al = ch.allocate(p.ell, 1.0, mu, p.alpha, p.ell * k, method, k)
+    assert _rel(out["5"][0], op.apply_allatonce(w, r)) <= 1e-12
+    assert _rel(out["5"][1], ch.nc_apply(w, r, p.ell, p.alpha, 1.0, mu, al)) <= 1e-12
+
+
 # ---------------------------------------------------------------- full-size 3D (configs[4])
 def _sub_weights(w, lo, hi):
     """Face weights of the box [lo, hi) of the full grid (faces inside the box only): the box
