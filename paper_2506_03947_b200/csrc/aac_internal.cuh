@@ -36,8 +36,12 @@ __constant__ int c_rev;
 #define AAC_L2_ARNOLDI 32   // basis stream of k_arnoldi with an L2 evict_first policy
 #define AAC_L2_FWD 64       // ... of k_fwd_upd (bit 7: W too)
 #define AAC_L2_FWD_W 128
+#define AAC_L2_FWD_VJ 256    // k_fwd_upd stores V_j with a streaming (evict-first) store
 #ifndef AAC_REV_DEFAULT
-#define AAC_REV_DEFAULT (AAC_REV_MATVEC | AAC_REV_FWD)   // measured best of the 32 masks at the headline (8.18 vs 8.34-8.44 ms per solve)
+// measured best at the headline: k_matvec and k_fwd_upd reversed (8.34 -> 8.18 ms per solve, all
+// 32 direction masks tried), k_fwd_upd's input streams evict_first and its V_j store streaming so
+// that hat w stays in L2 for the wavefront (8.15; 2d256 3.98 -> 3.92 ms)
+#define AAC_REV_DEFAULT (AAC_REV_MATVEC | AAC_REV_FWD | AAC_L2_FWD | AAC_L2_FWD_W | AAC_L2_FWD_VJ)
 #endif
 
 // ------------------------------------------------------------------------------------------

@@ -198,7 +198,11 @@ __global__ void __launch_bounds__(FT + 32) k_fwd_upd(long long N, Dft D, double*
       const long long p = base + t;
       if (j > 0) {
         double* vj = U.V + (long long)j * L;
-        FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
+        if (c_rev & AAC_L2_FWD_VJ) {                 // (streaming store: next read four kernels later)
+          FOR_PL(pl) __stcs(vj + (long long)pl * N + p, w[pl]);
+        } else {
+          FOR_PL(pl) vj[(long long)pl * N + p] = w[pl];
+        }
       }
       FOR_PL(pl) nrm = fma(w[pl], w[pl], nrm);
       if (ell == ELLC) dft_store_exact<ELLC>(D, N, p, w, what);

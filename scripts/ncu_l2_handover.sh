@@ -5,7 +5,8 @@
 set -u
 O=gpurun_out/ncu_l2; mkdir -p $O
 CMD="python scripts/one_solve.py headline 1"
-for m in 0 5 21; do
+export MASKS=${MASKS:-"0 5 21"}
+for m in $MASKS; do
   AAC_REV=$m timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
     --cache-control none --clock-control none \
     -k regex:"k_fwd_upd|k_waver|k_inverse|k_matvec|k_arnoldi" -s 60 -c 20 --csv --log-file $O/rev$m.csv $CMD > $O/rev$m.log 2>&1
@@ -13,7 +14,8 @@ for m in 0 5 21; do
 done
 python - <<'P'
 import csv, collections
-for m in (0, 5, 21):
+import os
+for m in os.environ.get("MASKS", "0 5 21").split():
     rows = [r for r in csv.reader(open(f"gpurun_out/ncu_l2/rev{m}.csv")) if len(r) > 10]
     h = rows[0]; ik = h.index("Kernel Name"); im = h.index("Metric Name"); iv = h.index("Metric Value"); iid = h.index("ID")
     per = collections.OrderedDict()

@@ -575,7 +575,7 @@ def test_traversal_direction_masks(monkeypatch, kw, method, k):
     rng = np.random.default_rng(17)
     r = rng.standard_normal((p.ell,) + p.shape)
     out = {}
-    for m in ("0", "5", "29", "31"):
+    for m in ("0", "5", "29", "453", "31"):       # 453: the default (5 + the L2 policy bits)
         monkeypatch.setenv("AAC_REV", m)
         s = _solver(p)
         y = s.matvec(_dev(r, p.ell)).cpu().numpy()
@@ -583,7 +583,7 @@ def test_traversal_direction_masks(monkeypatch, kw, method, k):
         x, info = s.gmres(method, k, _dev(p.b, p.ell), rtol=p.rtol, maxit=60)
         out[m] = (y, z, x.cpu().numpy(), info["iters"])
         s.close()
-    for m in ("5", "29"):                              # k_arnoldi forward in 0, 5, 29
+    for m in ("5", "29", "453"):                       # k_arnoldi forward in 0, 5, 29, 453
         for a, b in zip(out["0"][:3], out[m][:3]):
             assert np.array_equal(a, b)
         assert out[m][3] == out["0"][3]
