@@ -37,6 +37,7 @@ __constant__ int c_rev;
 #define AAC_L2_FWD 64       // ... of k_fwd_upd (bit 7: W too)
 #define AAC_L2_FWD_W 128
 #define AAC_L2_FWD_VJ 256    // k_fwd_upd stores V_j with a streaming (evict-first) store
+#define AAC_L2_MATVEC_W 512  // k_matvec stores w with an L2 evict_last policy
 #ifndef AAC_REV_DEFAULT
 // measured best at the headline: k_matvec and k_fwd_upd reversed (8.34 -> 8.18 ms per solve, all
 // 32 direction masks tried), k_fwd_upd's input streams evict_first and its V_j store streaming so

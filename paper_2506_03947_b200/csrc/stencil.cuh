@@ -44,6 +44,18 @@ __device__ __forceinline__ void stv(double* u, long long p, const double* v) {
   }
 }
 
+// Store with an L2 cache-hint policy (createpolicy): w = calA Z_j kept in L2 (evict_last) for the
+// two kernels that read it next.
+template <int VEC>
+__device__ __forceinline__ void stv_hint(double* u, long long p, const double* v, uint64_t pol) {
+  if constexpr (VEC == 2) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(u + p), "d"(v[0]), "d"(v[1]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(u + p), "d"(v[0]), "l"(pol) : "memory");
+  }
+}
+
 // Geometry + face weights of the VEC points p .. p+VEC-1 (same row).
 template <int DIM, int VEC>
 struct PtV {
@@ -213,6 +225,9 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
   const int xx = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (xx >= g.nx) return;
   const bool rev = c_rev & AAC_REV_MATVEC;
+  const bool keep = c_rev & AAC_L2_MATVEC_W;
+  uint64_t pol = 0;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   PtV<DIM, VEC> q;
   load_ptv_xyz<DIM, VEC>(g, xx, rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y,
                          rev ? gridDim.z - 1 - blockIdx.z : blockIdx.z, q);
@@ -230,7 +245,8 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
     stencil_sv<DIM, VEC>(g, q, v0, a0);
 #pragma unroll
     for (int e = 0; e < VEC; ++e) a0[e] -= prev[e];
-    stv<VEC>(y + (long long)j * g.N, p, a0);
+    if (keep) stv_hint<VEC>(y + (long long)j * g.N, p, a0, pol);
+    else stv<VEC>(y + (long long)j * g.N, p, a0);
     if (two) {
       stencil_sv<DIM, VEC>(g, q, v1, a1);
 #pragma unroll
@@ -238,7 +254,8 @@ __global__ void __launch_bounds__(256) k_matvec(Geo g, int ell, const double* __
         a1[e] -= v0.c[e];
         prev[e] = v1.c[e];
       }
-      stv<VEC>(y + (long long)(j + 1) * g.N, p, a1);
+      if (keep) stv_hint<VEC>(y + (long long)(j + 1) * g.N, p, a1, pol);
+      else stv<VEC>(y + (long long)(j + 1) * g.N, p, a1);
     }
   }
 }
