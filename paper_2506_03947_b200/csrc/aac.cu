@@ -768,6 +768,7 @@ static ArnoldiCtx arnoldi_ctx(aac_ctx* ctx) {
   ac.red = ctx->d_red;
   ac.local_only = ctx->multi();
   ac.one_reduce = ctx->one_reduce ? 1 : 0;
+  ac.pub = ctx->pub_fold;
   return ac;
 }
 
@@ -1443,8 +1444,16 @@ static int get_graph(aac_ctx* ctx, int method, int k, GraphEntry** out) {
     if (ge.method == method && ge.k == k) { *out = &ge; return AAC_OK; }
   const long long l0 = ctx->launches;
   CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  // one rank: k_arnoldi's last CTA publishes the state itself (AAC_PUB_KERNEL=1: a k_publish node)
+  static const bool pub_kernel = getenv("AAC_PUB_KERNEL") && atoi(getenv("AAC_PUB_KERNEL")) == 1;
+  if (!ctx->multi() && !pub_kernel) {
+    void* hd = nullptr;
+    if (cudaHostGetDevicePointer(&hd, ctx->h_st, 0) == cudaSuccess) ctx->pub_fold = static_cast<unsigned*>(hd);
+  }
   int rc = arnoldi_step(ctx, method & ~AAC_F32, k, 0);       // (the key keeps the AAC_F32 flag)
-  if (rc == AAC_OK) rc = publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState));
+  const bool folded = ctx->pub_fold != nullptr;
+  ctx->pub_fold = nullptr;
+  if (rc == AAC_OK && !folded) rc = publish(ctx, ctx->d_st, ctx->h_st, sizeof(IterState));
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != AAC_OK) {

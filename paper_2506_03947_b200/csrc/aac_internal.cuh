@@ -163,6 +163,7 @@ struct aac_ctx {
   double* d_gath = nullptr;            // [nranks][AAC_GATHER_MAX]: rank-ordered sums (comm.cuh)
   double* d_ghost = nullptr;           // [2][ell][nx]: final Chebyshev iterates of the slab ghost rows
   bool z_ghost = false;                // this step's preconditioner wrote Z_j's halo rows (d_halo)
+  unsigned* pub_fold = nullptr;        // set while the step graph is captured: k_arnoldi publishes the IterState
   int wave_hd = 0;                     // halo depth (0: slabs too thin, per-step sweeps)
   // plans
   NcPlan nc[2];                        // cached NC plans

@@ -48,7 +48,13 @@ __host__ __device__ constexpr size_t arnoldi_ring_doubles() { return (size_t)AS 
 template <int DIM, int ELLC, bool TMA, bool FUSED>
 __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KAParams P) {
   IterState* st = P.ac.st;
-  if (st->done) return;
+  if (st->done) {                             // (the forward step of this replay converged: the host
+    if (P.ac.pub && blockIdx.x == 0) {        //  poll still has to see it)
+      for (int k = threadIdx.x; k < (int)(sizeof(IterState) / sizeof(unsigned)); k += blockDim.x)
+        P.ac.pub[k] = reinterpret_cast<const unsigned*>(st)[k];
+    }
+    return;
+  }
   const int j = st->j;
   const int nv = j + 1, nv2 = 2 * nv;
   extern __shared__ __align__(16) double smem[];
@@ -236,5 +242,10 @@ __global__ void __launch_bounds__(AT + 32, ARN_OCC) k_arnoldi(Geo g, int ell, KA
     // (lagged: the normalisation of the previous vector first -- it sets sigma_j)
     if (P.ac.one_reduce) arnoldi_norm_step_cta(P.ac, j, tot[nv + j]);
     arnoldi_cgs2_step_cta(P.ac, j, tot, tot + nv);
+    if (P.ac.pub) {
+      __syncthreads();
+      for (int k = t; k < (int)(sizeof(IterState) / sizeof(unsigned)); k += blockDim.x)
+        P.ac.pub[k] = reinterpret_cast<const volatile unsigned*>(st)[k];
+    }
   }
 }

@@ -69,6 +69,8 @@ struct ArnoldiCtx {
   double* G;        // Gram matrix (ldh x ldh)
   double* red;      // multi-rank: locally reduced raw sums before the all-reduce
   int local_only;   // 1 when nranks > 1
+  unsigned* pub;    // graph replay on one rank: the last CTA of k_arnoldi copies the IterState here
+                    // (host-mapped pinned memory) itself -- no k_publish node at the end of the step
   int one_reduce;   // 1: lagged normalisation -- ||V_j||^2 is taken from the Gram column of the
                     // projection pass (one reduction / all-reduce per Arnoldi step), see below
 };
